@@ -1,0 +1,345 @@
+"""Pins for the CPU oracle against what the paper and the mathematics fix.
+
+Every test here runs without a GPU.  None of them re-types the oracle's own
+formula: each compares it with a hand-derived value (SPEC/paper), a closed
+form, an invariant the paper proves, or an independent implementation
+(numpy LAPACK eigh; a covariance-form FD written in numpy below).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import fdgen
+import oracle
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _read_golden_rules():
+    rows = []
+    with open(os.path.join(HERE, "golden", "spec_reduce_rank_examples.txt")) as f:
+        for line in f:
+            line = line.split("#")[0].strip()
+            if not line:
+                continue
+            head, sin, sout, delta = [x.strip() for x in line.split("|")]
+            rule, alpha, ell = head.split()
+            rows.append((rule, float(alpha), int(ell), [float(x) for x in sin.split()],
+                         [float(x) for x in sout.split()], float(delta)))
+    return rows
+
+
+@pytest.mark.parametrize("case", _read_golden_rules())
+def test_reduce_rank_hand_examples(case):
+    """SPEC.md:183-194 hand examples of the FD / alpha-FD / iSVD rules."""
+    rule, alpha, ell, s_in, s_out, delta = case
+    L = len(s_in)
+    d = L + 1
+    # rows of a random rotation scaled by the singular values -> svd(Bf) = those values
+    rng = np.random.default_rng(0)
+    Q, _ = np.linalg.qr(rng.standard_normal((d, d)))
+    Bf = np.diag(s_in) @ Q[:L]
+    r = oracle.RULE_ISVD if rule == "isvd" else oracle.RULE_FD
+    B, dl, removed = oracle.reduce_rank(Bf, ell, r, alpha)
+    sv = np.linalg.svd(B, compute_uv=False)
+    expect = np.zeros(len(sv))
+    expect[: len(s_out)] = s_out
+    # compare sigma'^2 (sigma' = sqrt(sigma^2 - delta) turns eps-level ties into sqrt(eps))
+    np.testing.assert_allclose(sv[: len(expect)] ** 2, expect ** 2, atol=1e-12 * max(1.0, max(s_in) ** 2))
+    assert abs(dl - delta) < 1e-12 * max(1.0, max(s_in) ** 2)
+    # ledger of this single step: removed mass = ||Bf||^2 - ||B'||^2
+    assert abs(removed - (np.sum(np.square(s_in)) - np.sum(np.square(s_out)))) < 1e-10
+    # retained rows are in the span of the input rows and mutually orthogonal
+    G = B @ B.T
+    assert np.allclose(G - np.diag(np.diag(G)), 0, atol=1e-12)
+
+
+def test_stream_spec_example():
+    """ell=2 FD, rows 2e1 then e2 -> spectrum (sqrt3, 0), Delta = 1 (plus final RR, lossless)."""
+    A = np.array([[2, 0], [0, 1]], np.float32)
+    r = oracle.sketch(A, 2, "fd")
+    np.testing.assert_allclose(np.linalg.svd(r.B, compute_uv=False), [np.sqrt(3), 0], atol=1e-12)
+    assert abs(r.delta_total - 1.0) < 1e-12
+    assert r.n_shrinks == 2
+
+
+def test_zero_stream():
+    """all-zero rows -> B = 0, Delta = 0."""
+    A = np.zeros((50, 7), np.float32)
+    for v in oracle.VARIANTS:
+        r = oracle.sketch(A, 4, v)
+        assert np.all(r.B == 0) and r.delta_total == 0 and r.removed == 0
+
+
+def test_jacobi_2x2_closed_form():
+    a, b, c = 3.0, 1.25, -2.0
+    w, V = oracle.jacobi_eig([[a, b], [b, c]])
+    tr, det = a + c, a * c - b * b
+    disc = np.sqrt(tr * tr / 4 - det)
+    np.testing.assert_allclose(sorted(w), [tr / 2 - disc, tr / 2 + disc], rtol=1e-15)
+    M = np.array([[a, b], [b, c]])
+    np.testing.assert_allclose(M @ V, V * w[None, :], atol=1e-14)
+
+
+@pytest.mark.parametrize("n", [5, 37, 128])
+def test_jacobi_vs_lapack(n):
+    rng = np.random.default_rng(n)
+    X = rng.standard_normal((n, n))
+    M = X + X.T
+    w, V = oracle.jacobi_eig(M)
+    np.testing.assert_allclose(np.sort(w), np.linalg.eigvalsh(M), atol=1e-11 * np.abs(M).max() * n)
+    np.testing.assert_allclose(V.T @ V, np.eye(n), atol=1e-13 * n)
+    np.testing.assert_allclose(M @ V, V * w[None, :], atol=1e-11 * n)
+
+
+def test_lanczos_vs_jacobi():
+    rng = np.random.default_rng(3)
+    for d in (50, 200):
+        X = rng.standard_normal((d + 20, d))
+        M = X.T @ X - 0.5 * np.diag(rng.random(d))
+        ev = np.linalg.eigvalsh(M)
+        hi, lo = oracle.lanczos_extremes(M, kmax=d)
+        assert abs(hi - ev[-1]) < 1e-9 * abs(ev[-1]) and abs(lo - ev[0]) < 1e-8 * abs(ev[-1])
+        hj, lj = oracle.sym_extremes(M, jacobi_max=1024)
+        assert abs(hj - ev[-1]) < 1e-10 * abs(ev[-1]) and abs(lj - ev[0]) < 1e-9 * abs(ev[-1])
+
+
+# ---------------------------------------------------------------------------
+# Independent covariance-form implementation (numpy, test-only).
+# A ReduceRank maps the buffer covariance C = Bf^T Bf to V f(Lambda) V^T over the
+# eigenpairs of C (d x d), which share their nonzero spectrum with the Gram form
+# the oracle uses; slot counting is the same (occ -> ell-1 after each shrink).
+# ---------------------------------------------------------------------------
+def _cov_reduce(C, L, ell, rule, m):
+    d = C.shape[0]
+    mu, V = np.linalg.eigh(C)
+    mu, V = mu[::-1], V[:, ::-1]
+    lam = np.zeros(max(L, d))
+    lam[: min(d, L)] = np.maximum(mu[: min(d, L)], 0)
+    delta = lam[ell - 1] if ell <= L else 0.0
+    sp2 = np.zeros_like(lam)
+    for j in range(ell - 1):
+        if rule == "isvd" or j < ell - m:
+            sp2[j] = lam[j]
+        else:
+            sp2[j] = max(lam[j] - delta, 0.0)
+    k = min(d, ell - 1)
+    Cn = (V[:, :k] * sp2[:k][None, :]) @ V[:, :k].T
+    return Cn, delta, float(np.sum(lam[:L] - sp2[:L]))
+
+
+def _cov_sketch(A, ell, rule, m, L):
+    d = A.shape[1]
+    C = np.zeros((d, d))
+    occ = 0
+    Delta = 0.0
+    for a in A.astype(np.float64):
+        C += np.outer(a, a)
+        occ += 1
+        if occ == L:
+            C, dl, _ = _cov_reduce(C, L, ell, rule, m)
+            Delta += dl
+            occ = ell - 1
+    C, dl, _ = _cov_reduce(C, L, ell, rule, m)
+    return C, Delta + dl
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("variant", ["fd", "fast_fd", "alpha_fd", "fast_alpha_fd", "isvd", "fast_isvd"])
+def test_bruteforce_covariance_form(seed, variant):
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(1, 13))
+    d = int(rng.integers(1, 7))
+    ell = int(rng.integers(2, 5))
+    A = rng.standard_normal((n, d)).astype(np.float32) * rng.uniform(0.5, 2.0, size=(n, 1)).astype(np.float32)
+    rule, a0, batched = oracle.VARIANTS[variant]
+    alpha = 0.5 if a0 is None else a0
+    m = ell if rule == oracle.RULE_ISVD else oracle.alpha_m(ell, alpha)
+    L = 2 * ell if batched else ell
+    r = oracle.sketch(A, ell, variant, alpha=alpha)
+    C, Delta = _cov_sketch(A, ell, "isvd" if rule == oracle.RULE_ISVD else "fd", m, L)
+    np.testing.assert_allclose(r.B.T @ r.B, C, atol=1e-10 * max(1.0, np.abs(C).max()))
+    assert abs(r.delta_total - Delta) < 1e-10 * max(1.0, Delta)
+
+
+def _c1():
+    w = fdgen.config("c1")
+    return fdgen.host_rows(w)
+
+
+@pytest.mark.parametrize("variant", list(oracle.VARIANTS))
+def test_properties_lemma1_lemma3(variant):
+    """Props 1-2 via Lemma 1: 0 <= ||Ax||^2-||Bx||^2 <= Delta;
+    Lemma 3: ||A||_F^2 - ||B||_F^2 = removed, = ell*Delta (FD per-row),
+    m*Delta (alpha-FD per-row), Delta (iSVD per-row, one sigma^2 per step), >= m*Delta batched."""
+    A = _c1()
+    ell = 16
+    rule, a0, batched = oracle.VARIANTS[variant]
+    alpha = 0.2 if a0 is None else a0
+    r = oracle.sketch(A, ell, variant, alpha=alpha)
+    AtA, frob = oracle.gram(A)
+    M = AtA - r.B.T @ r.B
+    ev = np.linalg.eigvalsh(M)
+    assert ev[0] >= -1e-10 * frob
+    assert ev[-1] <= r.delta_total * (1 + 1e-10)
+    bF = float(np.sum(r.B ** 2))
+    assert abs((frob - bF) - r.removed) <= 1e-10 * frob
+    m = ell if rule == oracle.RULE_ISVD else oracle.alpha_m(ell, alpha)
+    if rule == oracle.RULE_ISVD:
+        if not batched:
+            assert abs(r.removed - r.delta_total) <= 1e-9 * frob
+    elif not batched:
+        assert abs(r.removed - m * r.delta_total) <= 1e-9 * frob
+    else:
+        assert r.removed >= m * r.delta_total * (1 - 1e-12)
+
+
+@pytest.mark.parametrize("variant", ["fd", "fast_fd", "alpha_fd", "fast_alpha_fd"])
+def test_error_bounds(variant):
+    """Lemma / Theorem (k < alpha*ell reading C19):
+    cov-err <= ||A - A_k||_F^2 / ((m - k) ||A||_F^2) for all integers 0 <= k < m."""
+    A = _c1()
+    ell = 16
+    rule, a0, _ = oracle.VARIANTS[variant]
+    alpha = 0.2 if a0 is None else a0
+    m = oracle.alpha_m(ell, alpha)
+    r = oracle.sketch(A, ell, variant, alpha=alpha)
+    e = oracle.cov_err(A, r.B)
+    s2 = np.linalg.svd(A.astype(np.float64), compute_uv=False) ** 2
+    for k in range(m):
+        tail = s2[k:].sum()
+        assert e["err"] <= tail / ((m - k) * e["frob"]) * (1 + 1e-9)
+    assert e["err"] <= 1.0 / m + 1e-12
+
+
+@pytest.mark.parametrize("variant", list(oracle.VARIANTS))
+def test_exact_when_rank_below_ell(variant):
+    """rank(A) <= ell-1 (or n <= ell-1) => B^T B = A^T A (reading C2: ell-1, not ell)."""
+    rng = np.random.default_rng(7)
+    ell, d = 6, 20
+    A = (rng.standard_normal((300, ell - 1)) @ rng.standard_normal((ell - 1, d))).astype(np.float32)
+    r = oracle.sketch(A, ell, variant)
+    AtA, frob = oracle.gram(A)
+    assert np.abs(AtA - r.B.T @ r.B).max() <= 1e-10 * frob
+    A2 = rng.standard_normal((ell - 1, d)).astype(np.float32)
+    r2 = oracle.sketch(A2, ell, variant)
+    AtA2, f2 = oracle.gram(A2)
+    assert np.abs(AtA2 - r2.B.T @ r2.B).max() <= 1e-12 * f2
+
+
+def test_rank_ell_only_bounded():
+    """With rank(A) = ell the FD sketch is NOT exact in general (off-by-one of reading C2)."""
+    rng = np.random.default_rng(8)
+    ell, d = 6, 20
+    A = (rng.standard_normal((300, ell)) @ rng.standard_normal((ell, d))).astype(np.float32)
+    r = oracle.sketch(A, ell, "fd")
+    e = oracle.cov_err(A, r.B)
+    assert e["err"] > 1e-6
+
+
+def test_cov_err_closed_forms():
+    """cov-err: B=A -> 0; A=I2, B=0 -> 0.5;
+    B=0 -> sigma_1^2/||A||_F^2 = 1/numeric-rank."""
+    A = np.eye(2, dtype=np.float32)
+    assert abs(oracle.cov_err(A, np.zeros((1, 2)))["err"] - 0.5) < 1e-15
+    rng = np.random.default_rng(1)
+    A = rng.standard_normal((40, 9)).astype(np.float32)
+    assert oracle.cov_err(A, A.astype(np.float64))["err"] < 1e-13
+    s = np.linalg.svd(A.astype(np.float64), compute_uv=False)
+    e = oracle.cov_err(A, np.zeros((3, 9)))
+    assert abs(e["err"] - s[0] ** 2 / np.sum(s ** 2)) < 1e-13
+    with pytest.raises(ValueError):
+        oracle.cov_err(np.zeros((3, 4), np.float32), np.zeros((2, 4)))
+
+
+def test_cov_err_lanczos_path_matches_jacobi_path():
+    rng = np.random.default_rng(2)
+    A = rng.standard_normal((400, 80)).astype(np.float32)
+    B = rng.standard_normal((10, 80)) * 3
+    e1 = oracle.cov_err(A, B, jacobi_max=1024)
+    e2 = oracle.cov_err(A, B, jacobi_max=10, kmax=80)
+    assert abs(e1["err"] - e2["err"]) < 1e-10 * e1["err"]
+
+
+@pytest.mark.parametrize("variant", ["fd", "fast_alpha_fd", "isvd"])
+def test_merge_symmetry_and_tree(variant):
+    """B^T B of merge(X, Y) depends only on X^T X + Y^T Y (reading C10)."""
+    A = _c1()
+    r = oracle.sketch(A, 16, variant, n_shards=4, want_shards=True)
+    X, Y = r.shards[0], r.shards[1]
+    B1, _ = oracle.merge(np.stack([X, Y]), 16, variant)
+    B2, _ = oracle.merge(np.stack([Y, X]), 16, variant)
+    assert np.abs(B1.T @ B1 - B2.T @ B2).max() < 1e-10 * r.frob_sq
+    # the P-shard sketch = recursive-halving tree over its shard sketches
+    B, _ = oracle.merge(r.shards, 16, variant)
+    assert np.abs(B.T @ B - r.B.T @ r.B).max() < 1e-12 * r.frob_sq
+    # each shard sketch = the sketch of that shard's contiguous rows
+    sizes = [500, 500, 500, 500]
+    r0 = oracle.sketch(A[:500], 16, variant)
+    assert np.abs(r0.B.T @ r0.B - r.shards[0].T @ r.shards[0]).max() < 1e-12 * r.frob_sq
+    # merged sketch still satisfies Props 1-2 with the summed Delta
+    AtA, frob = oracle.gram(A)
+    ev = np.linalg.eigvalsh(AtA - r.B.T @ r.B)
+    assert ev[0] > -1e-10 * frob and ev[-1] <= r.delta_total * (1 + 1e-10)
+    assert abs(frob - np.sum(r.B ** 2) - r.removed) < 1e-10 * frob
+    del sizes
+
+
+def test_appends_split_per_call():
+    """Each append call's rows are split into P contiguous ranges (C10)."""
+    A = _c1()
+    r = oracle.sketch(A, 16, "fast_fd", n_shards=2, appends=[1200, 800], want_shards=True)
+    part0 = np.concatenate([A[:600], A[1200:1600]])
+    r0 = oracle.sketch(part0, 16, "fast_fd")
+    assert np.abs(r0.B - r.shards[0]).max() == 0.0
+
+
+def test_table1_numeric_rank():
+    """Table 1: Random Noisy numeric rank 14.93 with m=30 and D_ii=1-(i-1)/m."""
+    g = {}
+    with open(os.path.join(HERE, "golden", "table1_random_noisy.txt")) as f:
+        for line in f:
+            line = line.split("#")[0].strip()
+            if line:
+                k, v = line.split()
+                g[k] = float(v)
+    w = fdgen.noisy_lowrank("t1", int(g["n"]), int(g["d"]), int(g["m"]), seed=0, zeta=g["zeta"])
+    A = fdgen.host_rows(w).astype(np.float64)
+    s = np.linalg.svd(A, compute_uv=False)
+    nr = np.sum(s ** 2) / s[0] ** 2
+    assert g["lo"] <= nr <= g["hi"], nr
+
+
+def test_generator_expected_frobenius():
+    """E||A||_F^2 = n (sum_i D_ii^2 + d / zeta^2) (SPEC.md:441 for the PAPER.md:539-541 construction)."""
+    w = fdgen.config("c2")
+    A = fdgen.host_rows(w).astype(np.float64)
+    D = 1 - np.arange(50) / 50
+    expect = w.n * (np.sum(D ** 2) + w.d / 100.0)
+    assert abs(np.sum(A ** 2) / expect - 1) < 0.02
+
+
+def test_generator_deterministic_and_rowwise():
+    w = fdgen.config("c1")
+    A = fdgen.host_rows(w)
+    B = fdgen.host_rows(w, 700, 300)
+    assert np.array_equal(A[700:1000], B)
+    w5 = fdgen.config("c5", n=20000)
+    w5.extra["block_rows"] = 10000
+    C = fdgen.host_rows(w5, 0, 200)
+    e = C[99].astype(np.float64)
+    assert abs(np.linalg.norm(e) - 3.0) < 1e-6 and np.array_equal(C[99], C[199])
+
+
+def test_paper_qualitative_order_c2():
+    """PAPER.md:649-652 (qualitative, smoke only — parity unpinned for printed errors):
+    on Random Noisy, FD is the worst and iSVD / 0.2-FD the best at small ell."""
+    w = fdgen.config("c2")
+    A = fdgen.host_rows(w)
+    errs = {}
+    for v in ("fd", "alpha_fd", "isvd"):
+        r = oracle.sketch(A, 20, v)
+        errs[v] = oracle.cov_err(A, r.B)["err"]
+    assert errs["fd"] > errs["alpha_fd"] and errs["fd"] > errs["isvd"]
+    assert errs["fd"] <= 1 / 20
