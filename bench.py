@@ -1,0 +1,396 @@
+#!/usr/bin/env python
+"""Benchmark: rows/sec sketched (fp32, ell given) on 1..8 B200, % of roofline, cov-err.
+
+Workload (BASELINE.json config 4, the largest single-GPU configuration and the
+one north_star's >=60% roofline / >=75% scaling targets are read on):
+    noisy low-rank stream n = 8,388,608 rows, d = 1024, k = 64, zeta = 10 (32 GiB fp32),
+    ell = 128, Fast FD (2*ell buffer), P_total = 1184 shard streams (8 x 148),
+    rows split evenly across the N GPUs (strong scaling; the shard DAG depends on
+    P_total only, so every N computes the same sketch), per-GPU sketches
+    all-gathered (NCCL) and tree-merged.
+A step = fd_reset + fd_append_rows(all local rows) + fd_sketch (+ all_gather +
+fd_merge for N > 1), with A already resident in HBM (32 GiB >> 126 MB L2, so
+every step streams A from HBM; no flush needed).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c4|c2|c1] [--variant fast_fd] [--no-e2e] [--no-cpu]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rows/sec sketched (fp32, ell given) at 1/2/4/8 B200 + % roofline; cov err"
+WORKLOADS = {
+    # name: (fdgen config, ell, default variant, P_total)
+    "c4": ("c4", 128, "fast_fd", 1184),
+    "c2": ("c2", 100, "fast_fd", 8),
+    "c1": ("c1", 16, "fast_fd", 8),
+}
+
+
+def peaks():
+    p = {"hbm_gbs": 6551.4, "bf16_tflops": 1687.5, "bf16_tflops_sustained": 1390.6, "sm_max_mhz": 1965.0,
+         "source": "fallback"}
+    f = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(f):
+        with open(f) as fh:
+            p.update(json.load(fh))
+        p["source"] = "measured (MEASURED_PEAKS.json)"
+    return p
+
+
+def algorithmic_flops_per_shrink(ell, d, N):
+    """Per-ReduceRank algorithmic flops:
+    gram  = [2(ell^2-1) + (ell+1)(ell+2)] d   (cross + new blocks; the retained block is diag(sigma'^2))
+    recon = 4 ell (ell-1) d                    (Wt (ell-1 x 2ell) . Bf (2ell x d))
+    eig   = 4/3 N^3 + 2 N^2 (ell-1)            (Householder tridiagonalisation + back-transform)"""
+    return {
+        "gram": (2 * (ell * ell - 1) + (ell + 1) * (ell + 2)) * d,
+        "recon": 4 * ell * (ell - 1) * d,
+        "eig": (4.0 / 3.0) * N ** 3 + 2.0 * N * N * (ell - 1),
+    }
+
+
+def fp32_simt_peak_tflops(mhz):
+    # 148 SMs x 128 FP32 lanes x 2 flops (FFMA) x clock
+    return 148 * 128 * 2 * mhz * 1e6 / 1e12
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if self.proc is None:
+            return out
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return out
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower().startswith("active")})
+        loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        out.update(sm_mhz=statistics.median(loaded) if loaded else None, sm_max_mhz=max(mx) if mx else None,
+                   reasons=reasons, samples=len(rows))
+        return out
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline and the --impl reference arm)
+# ---------------------------------------------------------------------------
+def oracle_sample(wl, rows_per_shard=None, nshards=None):
+    """Time the oracle (as it stands) on a bounded sample of the workload: `nshards`
+    shard streams of the bench DAG (one thread each, all host cores)."""
+    import numpy as np  # noqa: F401
+    import concurrent.futures as cf
+    import fdgen
+    import oracle
+    cfgname, ell, variant, P = WORKLOADS[wl]
+    w = fdgen.config(cfgname)
+    cores = os.cpu_count() or 1
+    nshards = nshards or cores
+    q, r = divmod(w.n, P)
+    picks = [int(s * P / nshards) for s in range(nshards)]
+    jobs = []
+    for s in picks:
+        start = s * q + min(s, r)
+        ln = q + (1 if s < r else 0)
+        if rows_per_shard:
+            ln = min(ln, rows_per_shard)
+        jobs.append((start, ln))
+    rows = [fdgen.host_rows(w, a, b) for a, b in jobs]
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(nshards) as ex:
+        list(ex.map(lambda A: oracle.sketch(A, ell, variant, nthreads=1), rows))
+    dt = time.perf_counter() - t0
+    nrows = sum(b for _, b in jobs)
+    return {"value": nrows / dt, "unit": "rows/s", "cores": min(cores, nshards), "kind": "oracle",
+            "sample": f"{nshards} of the {P} shard streams of {wl} ({nrows} rows, "
+                      f"{'first ' + str(rows_per_shard) + ' rows of ' if rows_per_shard else ''}each shard), "
+                      f"fp64 oracle, one thread per shard, {dt:.1f} s"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    wl = args.workload
+    cfgname, ell, variant, P = WORKLOADS[wl]
+    rows_per_shard = 2064 if wl == "c4" else None  # 256 + 14*129 rows: 15 ReduceRanks per shard
+    times = []
+    res = None
+    for i in range(args.warmup + args.steps):
+        res = oracle_sample(wl, rows_per_shard=rows_per_shard)
+        if i >= args.warmup:
+            times.append(res)
+    vals = [t["value"] for t in times]
+    value = statistics.median(vals) if vals else 0.0
+    ms = [float(t["sample"].split(", ")[-1].split(" s")[0]) * 1e3 for t in times]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.median(ms) if ms else None,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(wl, variant, P, world),
+        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": res["cores"], "kind": "oracle",
+                         "sample": res["sample"]},
+        "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(wl, variant, P, world):
+    cfgname, ell, _, _ = WORKLOADS[wl]
+    import fdgen
+    w = fdgen.config(cfgname)
+    return {"workload": f"{wl}: noisy low-rank n={w.n} d={w.d} k={w.k} zeta=10 fp32, ell={ell}, {variant}",
+            "n": w.n, "d": w.d, "ell": ell, "variant": variant, "n_shards_total": P,
+            "parallelism": f"rows dp{world}", "l2": "inputs larger than L2 (A is streamed from HBM every step)"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import fdgen
+    import paper_1501_06561_b200 as fd
+    from paper_1501_06561_b200.dist import gather_and_merge, local_range
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    wl = args.workload
+    cfgname, ell, variant, P = WORKLOADS[wl]
+    variant = args.variant or variant
+    if P % world:
+        raise SystemExit(f"P_total={P} not divisible by world={world}")
+    w = fdgen.config(cfgname)
+    r0, r1 = local_range(w.n, rank, world)
+    nloc = r1 - r0
+    gen = fdgen.DeviceGenerator(w, device=dev)
+    A = torch.empty((nloc, w.d), dtype=torch.float32, device=dev)
+    gen.fill(A, r0)
+    torch.cuda.synchronize()
+    sk = fd.Sketcher(w.d, ell, variant, n_shards=P // world, device=dev)
+
+    def step():
+        sk.reset()
+        sk.append(A)
+        B, _ = sk.sketch(stats=False)
+        if world > 1:
+            B, _ = gather_and_merge(B, {"frob_sq": 0, "delta_total": 0, "removed_mass": 0, "n_shrinks": 0,
+                                        "rows_seen": 0}, lambda S: sk.merge(S), None)
+        return B
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    sk.profile(True)
+    sk.profile_read()
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        B = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_total = e0.elapsed_time(e1)
+    kern = sk.profile_read()
+    sk.profile(False)
+    clk = clocks.stop()
+    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = w.n / (ms_step / 1e3)
+
+    # ---- roofline of the dominant kernel (live CUDA-event times of this run) ----
+    pk = peaks()
+    N = 2 * ell if fd.is_batched(variant) else ell
+    fl = algorithmic_flops_per_shrink(ell, w.d, N)
+    shrinks_per_step = sk_stats_shrinks = None
+    dom = max(("ingest", "gram", "eig", "recon"), key=lambda k: kern[k][0])
+    # shrinks per step on this rank: every ReduceRank launch processes a batch of problems
+    sk.reset()
+    sk.append(A)
+    Bst, st = sk.sketch(stats=True)
+    shrinks_per_step = st["n_shrinks"]
+    mhz = clk["sm_mhz"] or pk.get("sm_max_mhz", 1965.0)
+    simt_peak = fp32_simt_peak_tflops(pk.get("sm_max_mhz", 1965.0))
+    dom_ms = kern[dom][0] / args.steps
+    if dom == "ingest":
+        bytes_step = 2.0 * nloc * w.d * 4
+        achieved = bytes_step / (dom_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s"}
+    else:
+        flops_step = fl[dom] * shrinks_per_step
+        achieved = flops_step / (dom_ms / 1e3) / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": simt_peak, "unit": "TFLOP/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["kernel"] = f"{dom}_kernel"
+    roof["kernel_share_of_step"] = kern[dom][0] / ms_total
+    roof["per_kernel_ms_per_step"] = {k: v[0] / args.steps for k, v in kern.items()}
+    roof["launches_per_step"] = {k: v[1] / args.steps for k, v in kern.items()}
+    roof["peak_source"] = (f"FP32 SIMT 148 SM x 128 lanes x 2 x {pk.get('sm_max_mhz', 1965.0):.0f} MHz (derived)"
+                           if roof["bound"] == "alu" else f"hbm_gbs {pk['source']}")
+    traffic_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    roof["traffic"] = None
+    if os.path.exists(traffic_file):
+        with open(traffic_file) as f:
+            roof["traffic"] = json.load(f).get(roof["kernel"])
+    # end-to-end north_star roofline (GEMM pipe + HBM) for context
+    gemm_flops_row = (7 * ell * ell - ell) * w.d / (ell + 1)
+    gemm_peak = simt_peak * 1e12
+    roof["step_vs_north_star_roofline"] = {
+        "R_roof_rows_per_s_per_gpu": min(pk["hbm_gbs"] * 1e9 / (4 * w.d), gemm_peak / gemm_flops_row),
+        "pipe": "FP32 SIMT (v1 kernels)",
+    }
+    roof["step_vs_north_star_roofline"]["frac"] = (value / world) / roof["step_vs_north_star_roofline"]["R_roof_rows_per_s_per_gpu"]
+
+    gpu_launches = int(sum(v[1] for v in kern.values()))
+
+    # ---- cov err of the final sketch (GPU evaluator, outside the timed region) ----
+    from paper_1501_06561_b200.dist import dist_cov_err
+    ce = dist_cov_err(A, B)
+
+    # ---- e2e: host buffers through the public API, H2D + D2H inside the timed region ----
+    e2e = None
+    if not args.no_e2e:
+        Ah = torch.empty((nloc, w.d), dtype=torch.float32, pin_memory=True)
+        Ah.copy_(A)
+        del A
+        torch.cuda.empty_cache()
+        sk2 = sk
+
+        def e2e_step():
+            sk2.reset()
+            sk2.append(Ah)              # public API: host tensor -> device copy -> fd_append_rows
+            Bq, _ = sk2.sketch(stats=False)
+            if world > 1:
+                Bq, _ = gather_and_merge(Bq, {"frob_sq": 0, "delta_total": 0, "removed_mass": 0, "n_shrinks": 0,
+                                              "rows_seen": 0}, lambda S: sk2.merge(S), None)
+            return Bq.cpu()             # D2H of the result
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ks = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
+        for _ in range(ks):
+            e2e_step()
+        torch.cuda.synchronize()
+        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        sec = float(el.item()) / ks
+        e2e = {"value": w.n / sec, "unit": "rows/s", "h2d_bytes_per_step": int(w.n * w.d * 4),
+               "d2h_bytes_per_step": int(ell * w.d * 4 * world), "steps": ks,
+               "note": "wall clock over host-pinned input -> H2D -> sketch -> D2H of B"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded fdgen, generated on device)",
+        "config": config_dict(wl, variant, P, world),
+        "roofline": roof,
+        "gpu_launches": gpu_launches,
+        "clocks": {"sm_mhz": clk["sm_mhz"], "sm_max_mhz": clk["sm_max_mhz"], "reasons": clk["reasons"]},
+        "cov_err": ce["err"], "cov_err_lmin": ce["lmin"],
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = oracle_sample(wl, rows_per_shard=2064 if wl == "c4" else None)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    sk.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--variant", default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("note: warmup < 3 is below the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

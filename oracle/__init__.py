@@ -113,8 +113,10 @@ def sketch(A, ell, variant="fd", alpha=None, n_shards=1, appends=None, nthreads=
     A = np.ascontiguousarray(A, dtype=np.float32)
     n, d = A.shape
     rule, a0, batched = VARIANTS[variant]
-    if alpha is None:
-        alpha = a0 if a0 is not None else 0.2
+    if a0 is not None:          # FD / Fast FD / iSVD: alpha is fixed (1), any argument ignored
+        alpha = a0
+    elif alpha is None:
+        alpha = 0.2
     L = 2 * ell if batched else ell
     B = np.zeros((ell, d))
     shards = np.zeros((n_shards, ell, d)) if want_shards else None
@@ -138,8 +140,10 @@ def merge(sketches, ell, variant="fd", alpha=None):
     count, l2, d = S.shape
     assert l2 == ell
     rule, a0, _ = VARIANTS[variant]
-    if alpha is None:
-        alpha = a0 if a0 is not None else 0.2
+    if a0 is not None:
+        alpha = a0
+    elif alpha is None:
+        alpha = 0.2
     m = ell if rule == RULE_ISVD else alpha_m(ell, alpha)
     B = np.zeros((ell, d))
     st = np.zeros(5)

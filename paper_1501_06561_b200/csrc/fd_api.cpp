@@ -1,0 +1,626 @@
+// fd_api.cpp — C ABI of libfd (include/fd.h): handle, workspace carving, the
+// lockstep round scheduler over shard streams, the merge tree and the
+// evaluator entry points.  All arithmetic runs in the kernels of fd_kernels.cu.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "fd.h"
+#include "fd_internal.h"
+
+using fdk::Ingest;
+using fdk::Params;
+using fdk::Prob;
+using fdk::Stats;
+
+namespace {
+
+thread_local std::string g_err;
+
+fd_status fail(fd_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+fd_status cuda_fail(cudaError_t e, const char* where) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return FD_ERR_CUDA;
+}
+
+#define FD_CUDA(call)                                   \
+  do {                                                  \
+    cudaError_t e__ = (call);                           \
+    if (e__ != cudaSuccess) return cuda_fail(e__, #call); \
+  } while (0)
+
+constexpr size_t kAlign = 256;
+constexpr int kMergeMax = 64;                 // fd_merge: max sketches per call
+constexpr size_t kArenaHalf = 8u << 20;       // descriptor arena half (bytes)
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Layout {
+  size_t buf0, buf1, nodes, G, Wt, stats, flag, eig, arena, total;
+  int nnodes, nslots;
+};
+
+struct Derived {
+  int64_t d, ldb;
+  int ell, L, P, rule, m, ldg, nmax;
+  bool perrow;   // Alg. 1 per-row chain (buffer L = ell)
+  size_t gbytes; // element size of the Gram / Wt scratch
+};
+
+// Precision of a ReduceRank of size N: per-row chains run one
+// dependent ReduceRank per row, so the sketch is built in fp64 there (fp32
+// eigenvalue noise on rank-deficient buffers would be clamped at 0 and
+// accumulate as a bias); batched buffers run in fp32.
+bool use_f64(const Derived& D, int N) { return D.perrow && N <= fdk::kMaxN64; }
+
+bool derive(const fd_config* c, Derived* D, std::string* why) {
+  if (!c) { *why = "cfg is NULL"; return false; }
+  if (c->d < 1) { *why = "d < 1"; return false; }
+  if (c->ell < 2) { *why = "ell < 2"; return false; }
+  if (c->n_shards < 1) { *why = "n_shards < 1"; return false; }
+  if (c->variant < FD_FD || c->variant > FD_FAST_ISVD) { *why = "unknown variant"; return false; }
+  const bool batched = (c->variant == FD_FAST_FD || c->variant == FD_FAST_ALPHA_FD || c->variant == FD_FAST_ISVD);
+  const bool isvd = (c->variant == FD_ISVD || c->variant == FD_FAST_ISVD);
+  const bool alpha_v = (c->variant == FD_ALPHA_FD || c->variant == FD_FAST_ALPHA_FD);
+  D->d = c->d;
+  D->ldb = (c->d + 3) / 4 * 4;
+  D->ell = c->ell;
+  D->L = batched ? 2 * c->ell : c->ell;
+  D->P = c->n_shards;
+  D->rule = isvd ? fdk::RULE_ISVD : fdk::RULE_FD;
+  D->m = c->ell;
+  if (alpha_v) {
+    if (!(c->alpha > 0.0 && c->alpha <= 1.0)) { *why = "alpha must be in (0,1]"; return false; }
+    // m = max(1, round(alpha*ell)) (reading C5; round half away from zero)
+    D->m = std::max(1, (int)(c->alpha * c->ell + 0.5));
+  }
+  D->perrow = !batched;
+  D->gbytes = D->perrow ? sizeof(double) : sizeof(float);
+  D->nmax = std::max(D->L, 2 * c->ell - 2);
+  if (c->n_shards == 1) D->nmax = D->L;  // merges only via fd_merge (checked there)
+  D->ldg = (std::max(D->nmax, 2 * c->ell - 2) + 3) / 4 * 4;
+  return true;
+}
+
+Layout layout(const Derived& D) {
+  Layout Lo;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, kAlign); return o; };
+  const size_t bufb = (size_t)D.P * D.L * D.ldb * sizeof(float);
+  Lo.nnodes = std::max(2 * D.P - 1, 2 * kMergeMax - 1);
+  Lo.nslots = std::max(D.P, kMergeMax);
+  Lo.buf0 = take(bufb);
+  Lo.buf1 = take(bufb);
+  Lo.nodes = take((size_t)Lo.nnodes * D.ell * D.ldb * sizeof(float));
+  Lo.G = take((size_t)Lo.nslots * D.ldg * D.ldg * D.gbytes);
+  Lo.Wt = take((size_t)Lo.nslots * D.ell * D.ldg * D.gbytes);
+  Lo.stats = take((size_t)(D.P + Lo.nnodes) * sizeof(Stats));
+  Lo.flag = take(sizeof(int) * 4);
+  Lo.eig = take(fdk::eig_scratch_bytes());
+  Lo.arena = take(2 * kArenaHalf);
+  Lo.total = off;
+  return Lo;
+}
+
+}  // namespace
+
+struct fd_handle {
+  fd_config cfg;
+  Derived D;
+  Params prm;
+  Layout Lo;
+  char* ws;
+  cudaStream_t stream;
+  int device;
+  float* buf[2];
+  float* nodes;
+  char* G;
+  char* Wt;
+  Stats* stats;       // [P] shard stats, then [nnodes] node stats
+  int* flag;
+  double* eig;
+  char* arena;        // device descriptor arena (2 halves)
+  char* host_arena;   // pinned host mirror
+  cudaEvent_t ev[2];
+  int half;
+  size_t half_used;
+  std::vector<int> occ, cur;
+  int64_t rows_seen;
+  bool dead;
+  // live profiling: event pairs around launches
+  bool prof;
+  struct Rec { int kind; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+};
+
+namespace {
+
+Stats* node_stats(fd_handle* h, int node) { return h->stats + h->D.P + node; }
+float* node_buf(fd_handle* h, int node) { return h->nodes + (size_t)node * h->D.ell * h->D.ldb; }
+float* shard_buf(fd_handle* h, int s, int which) { return h->buf[which] + (size_t)s * h->D.L * h->D.ldb; }
+
+// Copy a block of descriptors to the device arena; returns the device pointer.
+template <typename T>
+fd_status push_desc(fd_handle* h, const std::vector<T>& v, const T** out) {
+  const size_t bytes = align_up(v.size() * sizeof(T), 64);
+  if (bytes > kArenaHalf) return fail(FD_ERR_INVALID_ARG, "descriptor batch larger than arena");
+  if (h->half_used + bytes > kArenaHalf) {
+    // switch halves: the other half's previous H2D copy must be done before
+    // its pinned host mirror is overwritten
+    FD_CUDA(cudaEventRecord(h->ev[h->half], h->stream));
+    h->half ^= 1;
+    FD_CUDA(cudaEventSynchronize(h->ev[h->half]));
+    h->half_used = 0;
+  }
+  char* hp = h->host_arena + (size_t)h->half * kArenaHalf + h->half_used;
+  char* dp = h->arena + (size_t)h->half * kArenaHalf + h->half_used;
+  memcpy(hp, v.data(), v.size() * sizeof(T));
+  FD_CUDA(cudaMemcpyAsync(dp, hp, v.size() * sizeof(T), cudaMemcpyHostToDevice, h->stream));
+  h->half_used += bytes;
+  *out = reinterpret_cast<const T*>(dp);
+  return FD_OK;
+}
+
+enum { K_INGEST = 0, K_GRAM = 1, K_EIG = 2, K_RECON = 3, K_COUNT = 4 };
+
+cudaEvent_t get_event(fd_handle* h) {
+  if (!h->pool.empty()) {
+    cudaEvent_t e = h->pool.back();
+    h->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// launch `f` on the handle's stream, bracketed by an event pair when profiling
+template <typename F>
+cudaError_t timed(fd_handle* h, int kind, F f) {
+  if (!h->prof) return f();
+  fd_handle::Rec r{kind, get_event(h), get_event(h)};
+  cudaEventRecord(r.a, h->stream);
+  cudaError_t e = f();
+  cudaEventRecord(r.b, h->stream);
+  h->recs.push_back(r);
+  return e;
+}
+
+fd_status run_reduce(fd_handle* h, const std::vector<Prob>& probs) {
+  if (probs.empty()) return FD_OK;
+  int nmax = 0;
+  for (const Prob& p : probs) nmax = std::max(nmax, p.rows0 + p.rows1);
+  const Prob* dp = nullptr;
+  fd_status s = push_desc(h, probs, &dp);
+  if (s != FD_OK) return s;
+  const int n = (int)probs.size();
+  Params prm = h->prm;
+  prm.f64 = use_f64(h->D, nmax) ? 1 : 0;
+  cudaError_t e;
+  if ((e = timed(h, K_GRAM, [&] { return fdk::launch_gram(dp, n, nmax, prm, h->stream); })) != cudaSuccess)
+    return cuda_fail(e, "gram");
+  if ((e = timed(h, K_EIG, [&] { return fdk::launch_eig(dp, n, prm, h->eig, h->stream); })) != cudaSuccess)
+    return cuda_fail(e, "eig");
+  if ((e = timed(h, K_RECON, [&] { return fdk::launch_recon(dp, n, nmax, prm, h->stream); })) != cudaSuccess)
+    return cuda_fail(e, "recon");
+  return FD_OK;
+}
+
+Prob make_prob(fd_handle* h, int slot, const float* s0, int r0, const float* s1, int r1, float* dst, Stats* st,
+               const Stats* c0 = nullptr, const Stats* c1 = nullptr) {
+  Prob p;
+  p.src0 = s0; p.rows0 = r0;
+  p.src1 = s1; p.rows1 = r1;
+  p.dst = dst;
+  p.G = h->G + (size_t)slot * h->D.ldg * h->D.ldg * h->D.gbytes;
+  p.Wt = h->Wt + (size_t)slot * h->D.ell * h->D.ldg * h->D.gbytes;
+  p.stats = st;
+  p.child0 = c0; p.child1 = c1;
+  return p;
+}
+
+// Recursive-halving tree over leaves [lo, hi) (left half = ceil).  Appends
+// internal nodes to `plan` as (left, right, node) and returns the root id.
+struct Merge { int a, b, node, height; };
+int build_tree(int lo, int hi, int* next_id, std::vector<Merge>* plan, std::vector<int>* height) {
+  if (hi - lo == 1) return lo;
+  const int mid = lo + (hi - lo + 1) / 2;
+  const int a = build_tree(lo, mid, next_id, plan, height);
+  const int b = build_tree(mid, hi, next_id, plan, height);
+  const int id = (*next_id)++;
+  const int hgt = std::max((*height)[a], (*height)[b]) + 1;
+  if ((int)height->size() <= id) height->resize(id + 1, 0);
+  (*height)[id] = hgt;
+  plan->push_back({a, b, id, hgt});
+  return id;
+}
+
+// Merge the `count` leaves already in node slots 0..count-1 (node stats set).
+fd_status run_tree(fd_handle* h, int count, int* root) {
+  if (count == 1) { *root = 0; return FD_OK; }
+  if (2 * h->D.ell - 2 > fdk::kMaxN)
+    return fail(FD_ERR_UNSUPPORTED, "merge Gram size 2*ell-2 exceeds FD_MAX_N");
+  std::vector<Merge> plan;
+  std::vector<int> height(count, 0);
+  int next = count;
+  *root = build_tree(0, count, &next, &plan, &height);
+  int maxh = 0;
+  for (const Merge& m : plan) maxh = std::max(maxh, m.height);
+  const int ell = h->D.ell;
+  for (int lvl = 1; lvl <= maxh; ++lvl) {
+    std::vector<Prob> probs;
+    for (const Merge& m : plan) {
+      if (m.height != lvl) continue;
+      const int slot = (int)probs.size();
+      // [X; Y] without their zero last rows: Gram size 2*ell-2 (same nonzero spectrum)
+      probs.push_back(make_prob(h, slot, node_buf(h, m.a), ell - 1, node_buf(h, m.b), ell - 1, node_buf(h, m.node),
+                                node_stats(h, m.node), node_stats(h, m.a), node_stats(h, m.b)));
+    }
+    fd_status s = run_reduce(h, probs);
+    if (s != FD_OK) return s;
+  }
+  return FD_OK;
+}
+
+fd_status check_flag(fd_handle* h) {
+  int flag = 0;
+  FD_CUDA(cudaMemcpyAsync(&flag, h->flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  FD_CUDA(cudaStreamSynchronize(h->stream));
+  if (flag) {
+    h->dead = true;
+    return fail(FD_ERR_NONFINITE, "non-finite value in the appended rows");
+  }
+  return FD_OK;
+}
+
+fd_status read_stats(fd_handle* h, const Stats* dev, fd_stats* st) {
+  Stats s;
+  int flag = 0;
+  FD_CUDA(cudaMemcpyAsync(&s, dev, sizeof(Stats), cudaMemcpyDeviceToHost, h->stream));
+  FD_CUDA(cudaMemcpyAsync(&flag, h->flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  FD_CUDA(cudaStreamSynchronize(h->stream));
+  st->rows_seen = h->rows_seen;
+  st->n_shrinks = (int64_t)(s.shrinks + 0.5);
+  st->frob_sq = s.frob;
+  st->delta_total = s.delta;
+  st->removed_mass = s.removed;
+  st->nonfinite = flag;
+  if (flag) {
+    h->dead = true;
+    return fail(FD_ERR_NONFINITE, "non-finite value in the appended rows");
+  }
+  return FD_OK;
+}
+
+// Final ReduceRank of shards [s0, s1) into node slots (non-destructive snapshot).
+fd_status finalize_shards(fd_handle* h, int s0, int s1) {
+  // leaf node stats start as copies of the shard stats
+  FD_CUDA(cudaMemcpyAsync(node_stats(h, s0), h->stats + s0, sizeof(Stats) * (s1 - s0), cudaMemcpyDeviceToDevice,
+                          h->stream));
+  std::vector<Prob> probs;
+  for (int s = s0; s < s1; ++s) {
+    probs.push_back(make_prob(h, (int)probs.size(), shard_buf(h, s, h->cur[s]), h->occ[s], nullptr, 0,
+                              node_buf(h, s), node_stats(h, s)));
+  }
+  return run_reduce(h, probs);
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t fd_workspace_bytes(const fd_config* cfg) {
+  Derived D;
+  std::string why;
+  if (!derive(cfg, &D, &why)) return 0;
+  return layout(D).total;
+}
+
+fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_stream, fd_handle** out) {
+  if (!out) return fail(FD_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  Derived D;
+  std::string why;
+  if (!derive(cfg, &D, &why)) return fail(FD_ERR_INVALID_ARG, why);
+  if (D.L > fdk::kMaxN) return fail(FD_ERR_UNSUPPORTED, "buffer Gram size exceeds FD_MAX_N");
+  if (D.P > 1 && 2 * D.ell - 2 > fdk::kMaxN) return fail(FD_ERR_UNSUPPORTED, "merge Gram size exceeds FD_MAX_N");
+  Layout Lo = layout(D);
+  if (!ws || ws_bytes < Lo.total) return fail(FD_ERR_WORKSPACE, "workspace too small");
+  fd_handle* h = new fd_handle();
+  h->cfg = *cfg;
+  h->D = D;
+  h->Lo = Lo;
+  h->ws = static_cast<char*>(ws);
+  h->stream = static_cast<cudaStream_t>(cuda_stream);
+  h->device = cfg->device;
+  h->prm.d = D.d; h->prm.ldb = D.ldb; h->prm.ldg = D.ldg; h->prm.ell = D.ell; h->prm.rule = D.rule; h->prm.m = D.m;
+  h->prm.f64 = 0;
+  h->buf[0] = reinterpret_cast<float*>(h->ws + Lo.buf0);
+  h->buf[1] = reinterpret_cast<float*>(h->ws + Lo.buf1);
+  h->nodes = reinterpret_cast<float*>(h->ws + Lo.nodes);
+  h->G = h->ws + Lo.G;
+  h->Wt = h->ws + Lo.Wt;
+  h->stats = reinterpret_cast<Stats*>(h->ws + Lo.stats);
+  h->flag = reinterpret_cast<int*>(h->ws + Lo.flag);
+  h->eig = reinterpret_cast<double*>(h->ws + Lo.eig);
+  h->arena = h->ws + Lo.arena;
+  h->half = 0;
+  h->half_used = 0;
+  h->occ.assign(D.P, 0);
+  h->cur.assign(D.P, 0);
+  h->rows_seen = 0;
+  h->dead = false;
+  h->prof = false;
+  cudaError_t e = cudaSetDevice(h->device);
+  if (e == cudaSuccess) e = cudaMallocHost(&h->host_arena, 2 * kArenaHalf);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev[0], cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev[1], cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(h->ev[0], h->stream);
+  if (e == cudaSuccess) e = cudaEventRecord(h->ev[1], h->stream);
+  // zero the shard buffers' statistics and the flag
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->stats, 0, sizeof(Stats) * (D.P + Lo.nnodes), h->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->flag, 0, sizeof(int) * 4, h->stream);
+  if (e != cudaSuccess) {
+    fd_status st = cuda_fail(e, "fd_create");
+    delete h;
+    return st;
+  }
+  *out = h;
+  return FD_OK;
+}
+
+fd_status fd_append_rows(fd_handle* h, const float* rows, int64_t n_rows, int64_t ld) {
+  if (!h) return fail(FD_ERR_INVALID_ARG, "handle is NULL");
+  if (h->dead) return fail(FD_ERR_STATE, "handle refuses work after a sticky error");
+  if (n_rows < 0) return fail(FD_ERR_INVALID_ARG, "n_rows < 0");
+  if (n_rows == 0) return FD_OK;
+  if (!rows) return fail(FD_ERR_INVALID_ARG, "rows is NULL");
+  if (ld < h->D.d) return fail(FD_ERR_SHAPE, "ld < d");
+  const int P = h->D.P, L = h->D.L, ell = h->D.ell;
+  // contiguous ranges of this call (reading C10)
+  const int64_t q = n_rows / P, r = n_rows % P;
+  std::vector<int64_t> start(P), rem(P);
+  int64_t off = 0;
+  for (int s = 0; s < P; ++s) {
+    start[s] = off;
+    rem[s] = q + (s < r ? 1 : 0);
+    off += rem[s];
+  }
+  std::vector<Ingest> ing;
+  std::vector<Prob> probs;
+  ing.reserve(P);
+  probs.reserve(P);
+  for (;;) {
+    ing.clear();
+    probs.clear();
+    for (int s = 0; s < P; ++s) {
+      if (rem[s] == 0) continue;
+      const int c = (int)std::min<int64_t>(L - h->occ[s], rem[s]);
+      Ingest g;
+      g.src = rows + start[s] * ld;
+      g.ld = ld;
+      g.dst = shard_buf(h, s, h->cur[s]) + (size_t)h->occ[s] * h->D.ldb;
+      g.nrows = c;
+      g.pad = 0;
+      g.stats = h->stats + s;
+      ing.push_back(g);
+      start[s] += c;
+      rem[s] -= c;
+      h->occ[s] += c;
+      if (h->occ[s] == L) {
+        const int slot = (int)probs.size();
+        probs.push_back(make_prob(h, slot, shard_buf(h, s, h->cur[s]), L, nullptr, 0, shard_buf(h, s, h->cur[s] ^ 1),
+                                  h->stats + s));
+        h->cur[s] ^= 1;
+        h->occ[s] = ell - 1;
+      }
+    }
+    if (ing.empty()) break;
+    const Ingest* di = nullptr;
+    fd_status st = push_desc(h, ing, &di);
+    if (st != FD_OK) return st;
+    const int ni = (int)ing.size();
+    cudaError_t e = timed(h, K_INGEST, [&] { return fdk::launch_ingest(di, ni, h->prm, h->flag, h->stream); });
+    if (e != cudaSuccess) return cuda_fail(e, "ingest");
+    st = run_reduce(h, probs);
+    if (st != FD_OK) return st;
+  }
+  h->rows_seen += n_rows;
+  return FD_OK;
+}
+
+fd_status fd_sketch(fd_handle* h, float* B_out, fd_stats* st) {
+  if (!h || !B_out) return fail(FD_ERR_INVALID_ARG, "NULL argument");
+  if (h->dead) return fail(FD_ERR_STATE, "handle refuses work after a sticky error");
+  fd_status s = finalize_shards(h, 0, h->D.P);
+  if (s != FD_OK) return s;
+  int root = 0;
+  s = run_tree(h, h->D.P, &root);
+  if (s != FD_OK) return s;
+  FD_CUDA(cudaMemcpy2DAsync(B_out, h->D.d * sizeof(float), node_buf(h, root), h->D.ldb * sizeof(float),
+                            h->D.d * sizeof(float), h->D.ell, cudaMemcpyDeviceToDevice, h->stream));
+  if (st) return read_stats(h, node_stats(h, root), st);
+  return FD_OK;
+}
+
+fd_status fd_merge(fd_handle* h, const float* sketches, int32_t count, float* B_out, fd_stats* st) {
+  if (!h || !sketches || !B_out) return fail(FD_ERR_INVALID_ARG, "NULL argument");
+  if (h->dead) return fail(FD_ERR_STATE, "handle refuses work after a sticky error");
+  if (count < 1 || count > kMergeMax) return fail(FD_ERR_INVALID_ARG, "count must be in [1, 64]");
+  const int ell = h->D.ell;
+  FD_CUDA(cudaMemcpy2DAsync(node_buf(h, 0), h->D.ldb * sizeof(float), sketches, h->D.d * sizeof(float),
+                            h->D.d * sizeof(float), (size_t)count * ell, cudaMemcpyDeviceToDevice, h->stream));
+  if (h->D.ldb != h->D.d) {
+    // zero the padding columns of the copied rows
+    FD_CUDA(cudaMemset2DAsync(node_buf(h, 0) + h->D.d, h->D.ldb * sizeof(float), 0,
+                              (h->D.ldb - h->D.d) * sizeof(float), (size_t)count * ell, h->stream));
+  }
+  FD_CUDA(cudaMemsetAsync(node_stats(h, 0), 0, sizeof(Stats) * (2 * count), h->stream));
+  int root = 0;
+  fd_status s = run_tree(h, count, &root);
+  if (s != FD_OK) return s;
+  FD_CUDA(cudaMemcpy2DAsync(B_out, h->D.d * sizeof(float), node_buf(h, root), h->D.ldb * sizeof(float),
+                            h->D.d * sizeof(float), ell, cudaMemcpyDeviceToDevice, h->stream));
+  if (st) {
+    s = read_stats(h, node_stats(h, root), st);
+    st->frob_sq = 0.0;
+    st->rows_seen = 0;
+    return s;
+  }
+  return FD_OK;
+}
+
+fd_status fd_shard_sketch(fd_handle* h, int32_t shard, float* B_out) {
+  if (!h || !B_out) return fail(FD_ERR_INVALID_ARG, "NULL argument");
+  if (shard < 0 || shard >= h->D.P) return fail(FD_ERR_INVALID_ARG, "shard out of range");
+  if (h->dead) return fail(FD_ERR_STATE, "handle refuses work after a sticky error");
+  fd_status s = finalize_shards(h, shard, shard + 1);
+  if (s != FD_OK) return s;
+  FD_CUDA(cudaMemcpy2DAsync(B_out, h->D.d * sizeof(float), node_buf(h, shard), h->D.ldb * sizeof(float),
+                            h->D.d * sizeof(float), h->D.ell, cudaMemcpyDeviceToDevice, h->stream));
+  return check_flag(h);
+}
+
+fd_status fd_reset(fd_handle* h) {
+  if (!h) return fail(FD_ERR_INVALID_ARG, "handle is NULL");
+  std::fill(h->occ.begin(), h->occ.end(), 0);
+  std::fill(h->cur.begin(), h->cur.end(), 0);
+  h->rows_seen = 0;
+  h->dead = false;
+  FD_CUDA(cudaMemsetAsync(h->stats, 0, sizeof(Stats) * (h->D.P + h->Lo.nnodes), h->stream));
+  FD_CUDA(cudaMemsetAsync(h->flag, 0, sizeof(int) * 4, h->stream));
+  return FD_OK;
+}
+
+fd_status fd_profile(fd_handle* h, int32_t enable) {
+  if (!h) return fail(FD_ERR_INVALID_ARG, "handle is NULL");
+  h->prof = enable != 0;
+  return FD_OK;
+}
+
+int32_t fd_profile_read(fd_handle* h, double* ms, int64_t* launches, int32_t max_kernels) {
+  if (!h) return 0;
+  cudaStreamSynchronize(h->stream);
+  double acc[K_COUNT] = {0, 0, 0, 0};
+  int64_t cnt[K_COUNT] = {0, 0, 0, 0};
+  for (auto& r : h->recs) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) acc[r.kind] += t;
+    cnt[r.kind] += 1;
+    h->pool.push_back(r.a);
+    h->pool.push_back(r.b);
+  }
+  h->recs.clear();
+  for (int k = 0; k < K_COUNT && k < max_kernels; ++k) {
+    if (ms) ms[k] = acc[k];
+    if (launches) launches[k] = cnt[k];
+  }
+  return K_COUNT;
+}
+
+fd_status fd_destroy(fd_handle* h) {
+  if (!h) return FD_OK;
+  cudaStreamSynchronize(h->stream);
+  for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto e : h->pool) cudaEventDestroy(e);
+  cudaEventDestroy(h->ev[0]);
+  cudaEventDestroy(h->ev[1]);
+  cudaFreeHost(h->host_arena);
+  delete h;
+  return FD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Evaluator
+// ---------------------------------------------------------------------------
+static int lanczos_k(int64_t d) { return (int)std::min<int64_t>(d, 512); }
+
+size_t fd_cov_workspace_bytes(int64_t d) {
+  if (d < 1) return 0;
+  const int k = lanczos_k(d);
+  size_t off = 0;
+  off = align_up(off + (size_t)d * d * sizeof(double), kAlign);                 // M / AtA scratch
+  off = align_up(off + (size_t)(k + 1) * d * sizeof(double), kAlign);           // Q
+  off = align_up(off + (size_t)(2 * k + 2 + d + k + 64) * sizeof(double), kAlign);  // work
+  off = align_up(off + 4 * sizeof(double), kAlign);                             // out
+  off = align_up(off + (size_t)d * d * sizeof(double), kAlign);                 // AtA for fd_cov_err
+  return off;
+}
+
+fd_status fd_cov_gram_partial(const float* A, int64_t n, int64_t ld, int64_t d, double* AtA, void* ws,
+                              size_t ws_bytes, void* cuda_stream) {
+  (void)ws;
+  (void)ws_bytes;
+  if (!AtA || (n > 0 && !A) || d < 1 || n < 0) return fail(FD_ERR_INVALID_ARG, "bad argument");
+  if (ld < d) return fail(FD_ERR_SHAPE, "ld < d");
+  if (n == 0) return FD_OK;
+  cudaError_t e = fdk::launch_syrk_f64(A, n, ld, d, AtA, static_cast<cudaStream_t>(cuda_stream));
+  if (e != cudaSuccess) return cuda_fail(e, "syrk");
+  return FD_OK;
+}
+
+fd_status fd_cov_err_from_gram(const double* AtA, const float* B, int32_t ell, int64_t d, double frob_sq,
+                               double* err, double* lam_max, double* lam_min, void* ws, size_t ws_bytes,
+                               void* cuda_stream) {
+  if (!AtA || !B || !err || ell < 1 || d < 1) return fail(FD_ERR_INVALID_ARG, "bad argument");
+  if (!(frob_sq > 0.0)) return fail(FD_ERR_ZERO_NORM, "||A||_F^2 = 0: cov-err undefined");
+  if (!ws || ws_bytes < fd_cov_workspace_bytes(d)) return fail(FD_ERR_WORKSPACE, "evaluator workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+  const int k = lanczos_k(d);
+  char* w = static_cast<char*>(ws);
+  size_t off = 0;
+  double* M = reinterpret_cast<double*>(w + off); off = align_up(off + (size_t)d * d * sizeof(double), kAlign);
+  double* Q = reinterpret_cast<double*>(w + off); off = align_up(off + (size_t)(k + 1) * d * sizeof(double), kAlign);
+  double* work = reinterpret_cast<double*>(w + off); off = align_up(off + (size_t)(2 * k + 2 + d + k + 64) * sizeof(double), kAlign);
+  double* out = reinterpret_cast<double*>(w + off);
+  cudaError_t e = fdk::launch_sub_btb(M, AtA, B, ell, d, s);
+  if (e != cudaSuccess) return cuda_fail(e, "sub_btb");
+  e = fdk::launch_lanczos(M, d, k, Q, work, out, s);
+  if (e != cudaSuccess) return cuda_fail(e, "lanczos");
+  double ex[2];
+  e = cudaMemcpyAsync(ex, out, sizeof(ex), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "lanczos result");
+  const double nrm = std::max(std::fabs(ex[0]), std::fabs(ex[1]));
+  *err = nrm / frob_sq;
+  if (lam_max) *lam_max = ex[0] / frob_sq;
+  if (lam_min) *lam_min = ex[1] / frob_sq;
+  return FD_OK;
+}
+
+fd_status fd_cov_err(const float* A, int64_t n, int64_t ld, const float* B, int32_t ell, int64_t d, double* err,
+                     double* lam_max, double* lam_min, void* ws, size_t ws_bytes, void* cuda_stream) {
+  if (!ws || ws_bytes < fd_cov_workspace_bytes(d)) return fail(FD_ERR_WORKSPACE, "evaluator workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+  const size_t tot = fd_cov_workspace_bytes(d);
+  double* AtA = reinterpret_cast<double*>(static_cast<char*>(ws) + tot - align_up((size_t)d * d * sizeof(double), kAlign));
+  cudaError_t e = cudaMemsetAsync(AtA, 0, (size_t)d * d * sizeof(double), s);
+  if (e != cudaSuccess) return cuda_fail(e, "memset");
+  fd_status st = fd_cov_gram_partial(A, n, ld, d, AtA, ws, ws_bytes, cuda_stream);
+  if (st != FD_OK) return st;
+  // frob = trace(A^T A)
+  std::vector<double> diag(d);
+  e = cudaMemcpy2DAsync(diag.data(), sizeof(double), AtA, (d + 1) * sizeof(double), sizeof(double), d,
+                        cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "trace");
+  double frob = 0.0;
+  for (double x : diag) frob += x;
+  return fd_cov_err_from_gram(AtA, B, ell, d, frob, err, lam_max, lam_min, ws, ws_bytes, cuda_stream);
+}
+
+const char* fd_last_error(void) { return g_err.c_str(); }
+
+const char* fd_version(void) { return "fd-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,72 @@
+// fd_internal.h — device-side descriptors and kernel launchers of libfd.
+// Internal to the CUDA path (never included by the oracle).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fdk {
+
+constexpr int kNumSMs = 148;
+constexpr int kMaxN = 256;          // largest buffer Gram (eigen-problem) size (fp32 path)
+constexpr int kMaxN64 = 160;        // largest problem run in fp64 (per-row chains)
+constexpr int kEigThreads = 512;
+
+enum Rule : int { RULE_FD = 0, RULE_ISVD = 1 };
+
+// Per-shard / per-node statistics, fp64 (device).
+struct Stats {
+  double frob;     // sum ||a_i||^2
+  double delta;    // Delta = sum delta_i
+  double removed;  // sum (lambda_j - sigma'_j^2)
+  double shrinks;  // number of ReduceRanks
+};
+
+// One ReduceRank problem: buffer Bf = [src0 rows0; src1 rows1] (ld = ldb each),
+// Gram size N = rows0 + rows1 (<= kMaxN).  Output: dst rows 0..ell-1 (row ell-1 = 0).
+struct Prob {
+  const float* src0;
+  const float* src1;
+  int rows0, rows1;
+  float* dst;
+  void* G;       // N x N (ldg), element type float or double (Params.f64)
+  void* Wt;      // (ell-1) x N (ldg), same element type
+  Stats* stats;  // accumulates delta / removed / shrinks of this ReduceRank
+  const Stats* child0;  // merges: stats = child0 + child1 before accumulating
+  const Stats* child1;
+};
+
+// Ingest of one shard in one round: copy nrows rows of the user's A into the
+// shard buffer (row stride ldb, zero-padded to ldb columns), accumulate ||a||^2.
+struct Ingest {
+  const float* src;
+  int64_t ld;
+  float* dst;
+  int nrows;
+  int pad;
+  Stats* stats;
+};
+
+struct Params {
+  int64_t d;     // true row length
+  int64_t ldb;   // internal row stride (d rounded up to 4)
+  int ldg;       // Gram / Wt row stride (= max problem size)
+  int ell;
+  int rule;
+  int m;         // alpha-FD: number of trailing values that shrink
+  int f64;       // 1: Gram / eigen / reconstruct accumulate in fp64 (per-row chains)
+};
+
+// All launchers return cudaGetLastError() after enqueueing.
+cudaError_t launch_ingest(const Ingest* dev_desc, int count, const Params& p, int* nonfinite, cudaStream_t s);
+cudaError_t launch_gram(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s);
+cudaError_t launch_eig(const Prob* dev_probs, int count, const Params& p, double* scratch, cudaStream_t s);
+cudaError_t launch_recon(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s);
+size_t eig_scratch_bytes();   // device scratch the eig kernel needs (all CTA slots)
+
+// Evaluator.
+cudaError_t launch_syrk_f64(const float* A, int64_t n, int64_t ld, int64_t d, double* AtA, cudaStream_t s);
+cudaError_t launch_sub_btb(double* M, const double* AtA, const float* B, int ell, int64_t d, cudaStream_t s);
+cudaError_t launch_lanczos(const double* M, int64_t d, int kmax, double* Q, double* work, double* out2,
+                           cudaStream_t s);
+
+}  // namespace fdk

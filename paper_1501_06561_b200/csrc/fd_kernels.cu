@@ -1,0 +1,848 @@
+// fd_kernels.cu — sm_100a kernels of the Frequent Directions hot path.
+//
+// One ReduceRank (Alg. 1 lines "svd(B_[i]) ... B_[i] <- S'V^T")
+// of a batch of independent shard buffers is three kernels:
+//   gram_kernel   G = Bf Bf^T                         (buffer Gram, fp32)
+//   eig_kernel    G = U diag(lambda) U^T; delta = lambda_ell; rule -> w_j;
+//                 Wt = diag(w) U[:, :ell-1]^T         (one CTA per problem)
+//   recon_kernel  B' = Wt Bf   (= S'V^T since V^T = S^-1 U^T Bf)
+// plus ingest_kernel (rows of A -> shard buffers, ||a||^2 in fp64) and the
+// cov-err evaluator (fp64 A^T A, M = A^T A - B^T B, Lanczos).
+//
+// The eigen-solver is Householder tridiagonalisation (LAPACK ssytd2 order,
+// fp32, packed lower triangle resident in shared memory), multisection
+// bisection on Sturm counts for the top ell eigenvalues, fp64 inverse
+// iteration (with modified Gram-Schmidt inside eigenvalue clusters) for the
+// ell-1 retained eigenvectors, and a fp32 Householder back-transform.
+#include <cuda_runtime.h>
+#include <float.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "fd_internal.h"
+
+namespace fdk {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ============================================================================
+// ingest: rows of A (user layout, any ld / alignment) -> shard buffer (ldb),
+// fp64 sum of squares, non-finite detection.  One CTA per shard-round.
+// ============================================================================
+__global__ void __launch_bounds__(256) ingest_kernel(const Ingest* __restrict__ desc, Params p,
+                                                     int* __restrict__ nonfinite) {
+  const Ingest D = desc[blockIdx.x];
+  const int64_t d = p.d, ldb = p.ldb;
+  double acc = 0.0;
+  int bad = 0;
+  const bool vec = ((D.ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(D.src) & 15) == 0) && ((d & 3) == 0);
+  if (vec) {
+    const int64_t nq = d >> 2;
+    const int64_t total = (int64_t)D.nrows * nq;
+    for (int64_t q = threadIdx.x; q < total; q += blockDim.x) {
+      const int64_t r = q / nq, c = q - r * nq;
+      float4 v = __ldcs(reinterpret_cast<const float4*>(D.src + r * D.ld) + c);
+      bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+      acc += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
+      reinterpret_cast<float4*>(D.dst + r * ldb)[c] = v;
+    }
+  } else {
+    const int64_t total = (int64_t)D.nrows * ldb;
+    for (int64_t q = threadIdx.x; q < total; q += blockDim.x) {
+      const int64_t r = q / ldb, c = q - r * ldb;
+      float v = 0.f;
+      if (c < d) {
+        v = D.src[r * D.ld + c];
+        bad |= !isfinite(v);
+        acc += (double)v * v;
+      }
+      D.dst[r * ldb + c] = v;
+    }
+  }
+  __shared__ double red[8];
+  acc = warp_sum_d(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    D.stats->frob += s;
+    if (bad) atomicOr(nonfinite, 1);
+  }
+}
+
+cudaError_t launch_ingest(const Ingest* dev_desc, int count, const Params& p, int* nonfinite, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  ingest_kernel<<<count, 256, 0, s>>>(dev_desc, p, nonfinite);
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// Gram: G = Bf Bf^T for Bf = [src0 (rows0); src1 (rows1)] in precision T
+// (fp32 rows are exact in fp64), 64x64 lower-triangular output tiles, both
+// triangles written.
+// ============================================================================
+__device__ __forceinline__ const float* prob_row(const Prob& P, int r, int64_t ldb) {
+  if (r < P.rows0) return P.src0 + (int64_t)r * ldb;
+  r -= P.rows0;
+  if (r < P.rows1) return P.src1 + (int64_t)r * ldb;
+  return nullptr;
+}
+
+__device__ __forceinline__ void tri_index(int t, int& ti, int& tj) {
+  int i = (int)((sqrtf(8.f * (float)t + 1.f) - 1.f) * 0.5f);
+  while ((i + 1) * (i + 2) / 2 <= t) ++i;
+  while (i * (i + 1) / 2 > t) --i;
+  ti = i;
+  tj = t - i * (i + 1) / 2;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) gram_kernel(const Prob* __restrict__ probs, Params p) {
+  const Prob P = probs[blockIdx.y];
+  const int N = P.rows0 + P.rows1;
+  int ti, tj;
+  tri_index(blockIdx.x, ti, tj);
+  if (ti * 64 >= N) return;
+  __shared__ __align__(16) T As[16][68];
+  __shared__ __align__(16) T Bs[16][68];
+  const int lr = threadIdx.x >> 2, lk = (threadIdx.x & 3) * 4;
+  const float* arow = (ti * 64 + lr < N) ? prob_row(P, ti * 64 + lr, p.ldb) : nullptr;
+  const float* brow = (tj * 64 + lr < N) ? prob_row(P, tj * 64 + lr, p.ldb) : nullptr;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  T acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t k0 = 0; k0 < p.ldb; k0 += 16) {
+    const bool kin = (k0 + lk) < p.ldb;
+    const float4 av = (arow && kin) ? *reinterpret_cast<const float4*>(arow + k0 + lk) : z4;
+    const float4 bv = (brow && kin) ? *reinterpret_cast<const float4*>(brow + k0 + lk) : z4;
+    As[lk + 0][lr] = av.x; As[lk + 1][lr] = av.y; As[lk + 2][lr] = av.z; As[lk + 3][lr] = av.w;
+    Bs[lk + 0][lr] = bv.x; Bs[lk + 1][lr] = bv.y; Bs[lk + 2][lr] = bv.z; Bs[lk + 3][lr] = bv.w;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      T a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { a[q] = As[k][ty * 4 + q]; b[q] = Bs[k][tx * 4 + q]; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  T* G = static_cast<T*>(P.G);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = ti * 64 + ty * 4 + i, c = tj * 64 + tx * 4 + j;
+      if (r < N && c < N) {
+        G[(int64_t)r * p.ldg + c] = acc[i][j];
+        G[(int64_t)c * p.ldg + r] = acc[i][j];
+      }
+    }
+}
+
+cudaError_t launch_gram(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s) {
+  if (count <= 0 || nmax <= 0) return cudaSuccess;
+  const int nt = (nmax + 63) / 64;
+  dim3 grid(nt * (nt + 1) / 2, count);
+  if (p.f64) gram_kernel<double><<<grid, 256, 0, s>>>(dev_probs, p);
+  else gram_kernel<float><<<grid, 256, 0, s>>>(dev_probs, p);
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// Reconstruct: dst[j] = sum_r Wt[j][r] Bf[r] (j < ell-1) accumulated in T,
+// stored fp32; dst[ell-1] = 0.
+// ============================================================================
+template <typename T>
+__global__ void __launch_bounds__(256) recon_kernel(const Prob* __restrict__ probs, Params p) {
+  const Prob P = probs[blockIdx.z];
+  const int N = P.rows0 + P.rows1;
+  const int c0 = blockIdx.x * 64, j0 = blockIdx.y * 64;
+  if (j0 >= p.ell) return;
+  __shared__ __align__(16) T Ws[16][68];  // Ws[k][jj] = Wt[j0+jj][r0+k]
+  __shared__ __align__(16) T Bs[16][68];  // Bs[k][cc] = Bf[r0+k][c0+cc]
+  const T* Wt = static_cast<const T*>(P.Wt);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int wj = threadIdx.x >> 2, wk = (threadIdx.x & 3) * 4;    // Wt loader: 64 rows x 16
+  const int bk = threadIdx.x >> 4, bc = (threadIdx.x & 15) * 4;   // Bf loader: 16 rows x 64
+  T acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int jrow = j0 + wj;
+  for (int r0 = 0; r0 < N; r0 += 16) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = r0 + wk + q;
+      Ws[wk + q][wj] = (jrow < p.ell - 1 && r < N) ? Wt[(int64_t)jrow * p.ldg + r] : T(0);
+    }
+    float4 bv = z4;
+    const int r = r0 + bk;
+    if (r < N && c0 + bc < p.ldb) bv = *reinterpret_cast<const float4*>(prob_row(P, r, p.ldb) + c0 + bc);
+    Bs[bk][bc + 0] = bv.x; Bs[bk][bc + 1] = bv.y; Bs[bk][bc + 2] = bv.z; Bs[bk][bc + 3] = bv.w;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      T a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { a[q] = Ws[k][ty * 4 + q]; b[q] = Bs[k][tx * 4 + q]; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int j = j0 + ty * 4 + i;
+    if (j >= p.ell) continue;
+    const int c = c0 + tx * 4;
+    if (c >= p.ldb) continue;
+    float4 o = z4;
+    if (j < p.ell - 1) o = make_float4((float)acc[i][0], (float)acc[i][1], (float)acc[i][2], (float)acc[i][3]);
+    *reinterpret_cast<float4*>(P.dst + (int64_t)j * p.ldb + c) = o;
+  }
+}
+
+cudaError_t launch_recon(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  (void)nmax;
+  dim3 grid((unsigned)((p.ldb + 63) / 64), (unsigned)((p.ell + 63) / 64), count);
+  if (p.f64) recon_kernel<double><<<grid, 256, 0, s>>>(dev_probs, p);
+  else recon_kernel<float><<<grid, 256, 0, s>>>(dev_probs, p);
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// Eigen-solver + ReduceRank rule (one CTA per problem, persistent over
+// problems), precision T, max size NM.
+// ============================================================================
+constexpr int kNW = kEigThreads / 32;  // 16 warps
+// fp64 scratch per CTA slot: LDL^T factors (2N per cluster thread) + Z (N per vector)
+constexpr size_t kSlotDoubles = (size_t)kMaxN * 2 * kMaxN + (size_t)kMaxN * kMaxN;
+
+size_t eig_scratch_bytes() { return (size_t)kNumSMs * kSlotDoubles * sizeof(double); }
+
+template <typename T, int NM>
+struct EigCfg {
+  static constexpr int kPk = NM * (NM + 1) / 2;
+  static constexpr int kWork = 32 * NM;
+  static constexpr size_t kT = (size_t)kPk + kWork + 10 * NM + 64;  // elements of T
+  static constexpr size_t kBytes = kT * sizeof(T) + 2 * NM * sizeof(int) + 16;
+};
+
+__device__ __forceinline__ int pk_off(int c, int N) { return c * N - (c * (c - 1)) / 2; }
+
+template <typename T>
+__device__ __forceinline__ T wsum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = wsum(v);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  T s = T(0);
+#pragma unroll
+  for (int w = 0; w < kNW; ++w) s += red[w];
+  __syncthreads();
+  return s;
+}
+
+// number of eigenvalues of the tridiagonal (d, e2) strictly less than x
+// (Sturm count with the LAPACK xSTEBZ pivot guard)
+template <typename T>
+__device__ __forceinline__ int sturm_count(const T* dd, const T* e2, int N, T x, T pivmin) {
+  T q = dd[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  int cnt = q < T(0);
+  for (int i = 1; i < N; ++i) {
+    q = (dd[i] - x) - e2[i - 1] / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < T(0);
+  }
+  return cnt;
+}
+
+template <typename T> struct Lim;
+template <> struct Lim<float> {
+  static __device__ float eps() { return FLT_EPSILON; }
+  static __device__ float tiny() { return FLT_MIN; }
+  static __device__ float big() { return FLT_MAX; }
+  static constexpr float bits = 27.f;
+};
+template <> struct Lim<double> {
+  static __device__ double eps() { return DBL_EPSILON; }
+  static __device__ double tiny() { return DBL_MIN; }
+  static __device__ double big() { return DBL_MAX; }
+  static constexpr float bits = 56.f;
+};
+
+template <typename T, int NM>
+__global__ void __launch_bounds__(kEigThreads, 1)
+eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restrict__ scratch) {
+  using C = EigCfg<T, NM>;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* sm = reinterpret_cast<T*>(smraw);
+  T* Apk = sm;
+  T* work = Apk + C::kPk;
+  T* vs = work + C::kWork;
+  T* wsv = vs + NM;
+  T* pcol = wsv + NM;
+  T* dd = pcol + NM;
+  T* ee = dd + NM;
+  T* e2 = ee + NM;
+  T* tau = e2 + NM;
+  T* lam = tau + NM;
+  T* wgt = lam + NM;
+  T* spv = wgt + NM;
+  T* red = spv + NM;
+  int* cstart = reinterpret_cast<int*>(red + 64);
+  int* clen = cstart + NM;
+  __shared__ int s_ncl;
+  __shared__ T s_gl, s_gu;
+  constexpr int NT = (NM + 31) / 32;  // row-blocks of 32 per column
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* slot = scratch + (size_t)blockIdx.x * kSlotDoubles;
+  double* LDs = slot;                              // [cluster][2*kMaxN]
+  double* Zs = slot + (size_t)kMaxN * 2 * kMaxN;   // [j][kMaxN]
+
+  for (int pi = blockIdx.x; pi < count; pi += gridDim.x) {
+    const Prob P = probs[pi];
+    const int N = P.rows0 + P.rows1;
+    const int ell = p.ell;
+    const T* G = static_cast<const T*>(P.G);
+    T* Wt = static_cast<T*>(P.Wt);
+    // ---------------- load lower triangle (packed, column-major) ----------------
+    for (int c = warp; c < N; c += kNW) {
+      const int oc = pk_off(c, N);
+      for (int r = c + lane; r < N; r += 32) Apk[oc + r - c] = G[(int64_t)r * p.ldg + c];
+    }
+    __syncthreads();
+    // ---------------- Householder tridiagonalisation (lower, xSYTD2 order) ----------------
+    for (int i = 0; i < N - 2; ++i) {
+      const int n = N - i - 1;
+      const int oi = pk_off(i, N);
+      if (warp == 0) {
+        const T alpha = Apk[oi + 1];
+        T s = T(0);
+        for (int k = 1 + lane; k < n; k += 32) {
+          const T x = Apk[oi + 1 + k];
+          s = fma(x, x, s);
+        }
+        s = wsum(s);
+        T t_, beta, scale;
+        if (s == T(0)) {
+          t_ = T(0); beta = alpha; scale = T(0);
+        } else {
+          const T nrm = sqrt(fma(alpha, alpha, s));
+          beta = (alpha <= T(0)) ? nrm : -nrm;
+          t_ = (beta - alpha) / beta;
+          scale = T(1) / (alpha - beta);
+        }
+        for (int k = lane; k < n; k += 32) {
+          T vk = T(1);
+          if (k > 0) {
+            vk = Apk[oi + 1 + k] * scale;
+            Apk[oi + 1 + k] = vk;
+          }
+          vs[k] = vk;
+        }
+        if (lane == 0) { tau[i] = t_; dd[i] = Apk[oi]; ee[i] = beta; }
+      }
+      __syncthreads();
+      const T t_ = tau[i];
+      if (t_ == T(0)) continue;
+      // p = A22 v (packed SYMV), column-owner warps, register row accumulators
+      T acc[NT];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) acc[t] = T(0);
+      for (int c = warp; c < n; c += kNW) {
+        const int base = pk_off(i + 1 + c, N);
+        const T vc = vs[c];
+        T colsum = T(0);
+        const int t0 = c >> 5;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          if (t < t0 || 32 * t >= n) continue;
+          const int r = 32 * t + lane;
+          if (r >= c && r < n) {
+            const T a = Apk[base + r - c];
+            colsum = fma(a, vs[r], colsum);
+            if (r > c) acc[t] = fma(a, vc, acc[t]);
+          }
+        }
+        colsum = wsum(colsum);
+        if (lane == 0) pcol[c] = colsum;
+      }
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const int r = 32 * t + lane;
+        if (r < n) work[warp * NM + r] = acc[t];
+      }
+      __syncthreads();
+      T pr = T(0), prod = T(0);
+      if (tid < n) {
+        T s2 = pcol[tid];
+#pragma unroll
+        for (int w2 = 0; w2 < kNW; ++w2) s2 += work[w2 * NM + tid];
+        pr = t_ * s2;
+        prod = pr * vs[tid];
+      }
+      const T K = block_sum(prod, red);
+      if (tid < n) wsv[tid] = fma(T(-0.5) * t_ * K, vs[tid], pr);
+      __syncthreads();
+      // A22 -= v w^T + w v^T
+      for (int c = warp; c < n; c += kNW) {
+        const int base = pk_off(i + 1 + c, N);
+        const T vc = vs[c], wc = wsv[c];
+        for (int r = c + lane; r < n; r += 32) {
+          T a = Apk[base + r - c];
+          a = fma(-vs[r], wc, a);
+          a = fma(-wsv[r], vc, a);
+          Apk[base + r - c] = a;
+        }
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      if (N >= 2) {
+        dd[N - 2] = Apk[pk_off(N - 2, N)];
+        ee[N - 2] = Apk[pk_off(N - 2, N) + 1];
+        tau[N - 2] = T(0);
+        dd[N - 1] = Apk[pk_off(N - 1, N)];
+      } else if (N == 1) {
+        dd[0] = Apk[0];
+      }
+      if (N >= 1) { ee[N - 1] = T(0); tau[N - 1] = T(0); }
+    }
+    __syncthreads();
+    // ---------------- eigenvalues: multisection bisection ----------------
+    const int K = min(ell, N);        // top-K eigenvalues needed (lambda_ell = delta)
+    const int J = min(ell - 1, N);    // retained eigenvectors
+    T glo = Lim<T>::big(), ghi = -Lim<T>::big(), emax2 = T(0);
+    for (int i = tid; i < N; i += blockDim.x) {
+      const T em = (i > 0) ? fabs(ee[i - 1]) : T(0);
+      const T ep = (i < N - 1) ? fabs(ee[i]) : T(0);
+      glo = fmin(glo, dd[i] - em - ep);
+      ghi = fmax(ghi, dd[i] + em + ep);
+      e2[i] = (i < N - 1) ? ee[i] * ee[i] : T(0);
+      emax2 = fmax(emax2, e2[i]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      glo = fmin(glo, __shfl_xor_sync(0xffffffffu, glo, o));
+      ghi = fmax(ghi, __shfl_xor_sync(0xffffffffu, ghi, o));
+      emax2 = fmax(emax2, __shfl_xor_sync(0xffffffffu, emax2, o));
+    }
+    if (lane == 0) { red[warp] = glo; red[16 + warp] = ghi; red[32 + warp] = emax2; }
+    __syncthreads();
+    if (tid == 0) {
+      T a = Lim<T>::big(), b = -Lim<T>::big(), e = T(0);
+      for (int w = 0; w < kNW; ++w) { a = fmin(a, red[w]); b = fmax(b, red[16 + w]); e = fmax(e, red[32 + w]); }
+      const T bn = fmax(fabs(a), fabs(b));
+      const T slack = T(2) * Lim<T>::eps() * bn * (T)N + Lim<T>::tiny();
+      s_gl = a - slack; s_gu = b + slack;
+      red[48] = fmax(Lim<T>::tiny(), Lim<T>::tiny() * e);   // pivmin
+      red[49] = bn;
+    }
+    __syncthreads();
+    const T pivmin = red[48];
+    const T bnorm = red[49];
+    if (N > 0) {
+      int kp = 1;
+      while (kp < K) kp <<= 1;
+      int g = kEigThreads / kp;  // threads per eigenvalue (power of two)
+      if (g > 32) g = 32;
+      if (g < 1) g = 1;
+      const int j = tid / g, sub = tid % g;
+      const unsigned gmask = (g == 32) ? 0xffffffffu : (((1u << g) - 1u) << ((lane / g) * g));
+      T lo = s_gl, hi = s_gu;
+      const int niter = (int)ceilf(Lim<T>::bits / log2f((float)g + 1.f));
+      for (int it = 0; it < niter; ++it) {
+        const T step = (hi - lo) / (T)(g + 1);
+        const T x = lo + step * (T)(sub + 1);
+        const bool below = (j < K) ? (sturm_count(dd, e2, N, x, pivmin) >= N - j) : false;
+        const unsigned b = __ballot_sync(0xffffffffu, below) & gmask;
+        const int base = (lane / g) * g;
+        const int ss = b ? (__ffs(b) - 1 - base) : g;
+        const T nlo = (ss == 0) ? lo : lo + step * (T)ss;
+        const T nhi = (ss == g) ? hi : lo + step * (T)(ss + 1);
+        lo = nlo;
+        hi = fmax(nhi, nlo);
+      }
+      if (sub == 0 && j < K) lam[j] = fmax(T(0.5) * (lo + hi), T(0));  // clamp (reading C8)
+    }
+    __syncthreads();
+    // ---------------- ReduceRank rule ----------------
+    const T delta = (ell <= N) ? lam[ell - 1] : T(0);
+    if (tid < J) {
+      const T l = lam[tid];
+      T sp2;
+      if (p.rule == RULE_ISVD || tid < ell - p.m) sp2 = l;
+      else sp2 = fmax(l - delta, T(0));
+      spv[tid] = sp2;
+      wgt[tid] = (l > T(0)) ? sqrt(sp2 / l) : T(0);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double tr = 0.0, sp = 0.0;
+      for (int i = 0; i < N; ++i) tr += (double)dd[i];
+      for (int j = 0; j < J; ++j) sp += (double)spv[j];
+      if (P.stats) {
+        Stats st;
+        if (P.child0) {
+          const Stats a = *P.child0, b = *P.child1;
+          st.frob = a.frob + b.frob; st.delta = a.delta + b.delta;
+          st.removed = a.removed + b.removed; st.shrinks = a.shrinks + b.shrinks;
+        } else {
+          st = *P.stats;
+        }
+        st.delta += (double)delta;
+        st.removed += tr - sp;
+        st.shrinks += 1.0;
+        *P.stats = st;
+      }
+      // clusters of close eigenvalues among 0..J-1 (vectors orthogonalised together)
+      const T ctol = T(1e-5) * bnorm;
+      int ncl = 0;
+      for (int j = 0; j < J; ++j) {
+        if (j == 0 || lam[j - 1] - lam[j] > ctol) { cstart[ncl] = j; clen[ncl] = 0; ++ncl; }
+        clen[ncl - 1]++;
+      }
+      s_ncl = ncl;
+    }
+    __syncthreads();
+    // ---------------- eigenvectors of T: fp64 inverse iteration ----------------
+    const int ncl = s_ncl;
+    const double tiny = 2.3e-16 * (double)bnorm + 1e-300;
+    for (int cl = tid; cl < ncl; cl += blockDim.x) {
+      double* lf = LDs + (size_t)cl * 2 * kMaxN;
+      double* dp = lf + kMaxN;
+      const int j0 = cstart[cl], j1 = cstart[cl] + clen[cl];
+      for (int j = j0; j < j1; ++j) {
+        if (wgt[j] == T(0)) continue;
+        double* z = Zs + (size_t)j * kMaxN;
+        const double mu = (double)lam[j];
+        // T - mu I = L D L^T
+        double dpi = (double)dd[0] - mu;
+        if (fabs(dpi) < tiny) dpi = (dpi < 0.0) ? -tiny : tiny;
+        dp[0] = dpi;
+        for (int i = 0; i < N - 1; ++i) {
+          const double li = (double)ee[i] / dpi;
+          lf[i] = li;
+          dpi = ((double)dd[i + 1] - mu) - li * (double)ee[i];
+          if (fabs(dpi) < tiny) dpi = (dpi < 0.0) ? -tiny : tiny;
+          dp[i + 1] = dpi;
+        }
+        for (int i = 0; i < N; ++i) z[i] = 1.0 + 0.5 * (double)(((i + 1) * 7919 + (j + 3) * 104729) % 211) / 211.0;
+        for (int it = 0; it < 3; ++it) {
+          for (int i = 1; i < N; ++i) z[i] -= lf[i - 1] * z[i - 1];
+          for (int i = 0; i < N; ++i) z[i] /= dp[i];
+          for (int i = N - 2; i >= 0; --i) z[i] -= lf[i] * z[i + 1];
+          double mx = 0.0;
+          for (int i = 0; i < N; ++i) mx = fmax(mx, fabs(z[i]));
+          const double inv = (mx > 0.0) ? 1.0 / mx : 1.0;
+          for (int i = 0; i < N; ++i) z[i] *= inv;
+          for (int pass = 0; pass < 2; ++pass)
+            for (int k = j0; k < j; ++k) {
+              if (wgt[k] == T(0)) continue;
+              const double* zk = Zs + (size_t)k * kMaxN;
+              double h = 0.0;
+              for (int i = 0; i < N; ++i) h += zk[i] * z[i];
+              for (int i = 0; i < N; ++i) z[i] -= h * zk[i];
+            }
+          double nr = 0.0;
+          for (int i = 0; i < N; ++i) nr += z[i] * z[i];
+          nr = (nr > 0.0) ? 1.0 / sqrt(nr) : 0.0;
+          for (int i = 0; i < N; ++i) z[i] *= nr;
+        }
+      }
+    }
+    __syncthreads();
+    // ---------------- back-transform U = H_0 ... H_{N-3} Z ; Wt = diag(w) U^T ----------------
+    for (int c0 = 0; c0 < J; c0 += 32) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int jj = warp + kNW * q;
+        const int j = c0 + jj;
+        if (j >= J) continue;
+        T* zc = work + jj * NM;
+        const T wj = wgt[j];
+        if (wj == T(0)) {
+          for (int r = lane; r < N; r += 32) Wt[(int64_t)j * p.ldg + r] = T(0);
+          continue;
+        }
+        const double* zg = Zs + (size_t)j * kMaxN;
+        for (int r = lane; r < N; r += 32) zc[r] = (T)zg[r];
+        __syncwarp();
+        for (int i = N - 3; i >= 0; --i) {
+          const T ti = tau[i];
+          if (ti == T(0)) continue;
+          const int oi = pk_off(i, N);
+          T s = T(0);
+          for (int r = i + 1 + lane; r < N; r += 32) {
+            const T vr = (r == i + 1) ? T(1) : Apk[oi + (r - i)];
+            s = fma(vr, zc[r], s);
+          }
+          s = wsum(s) * ti;
+          for (int r = i + 1 + lane; r < N; r += 32) {
+            const T vr = (r == i + 1) ? T(1) : Apk[oi + (r - i)];
+            zc[r] = fma(-s, vr, zc[r]);
+          }
+          __syncwarp();
+        }
+        for (int r = lane; r < N; r += 32) Wt[(int64_t)j * p.ldg + r] = wj * zc[r];
+        __syncwarp();
+      }
+    }
+    // rows J..ell-2 of Wt (only when N < ell-1) are zero
+    for (int j = J + warp; j < ell - 1; j += kNW)
+      for (int r = lane; r < p.ldg; r += 32) Wt[(int64_t)j * p.ldg + r] = T(0);
+    __syncthreads();
+  }
+}
+
+template <typename T, int NM>
+static cudaError_t launch_eig_t(const Prob* dev_probs, int count, const Params& p, double* scratch, cudaStream_t s) {
+  using C = EigCfg<T, NM>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(eig_kernel<T, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kBytes);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int grid = count < kNumSMs ? count : kNumSMs;
+  eig_kernel<T, NM><<<grid, kEigThreads, C::kBytes, s>>>(dev_probs, count, p, scratch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_eig(const Prob* dev_probs, int count, const Params& p, double* scratch, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  if (p.f64) return launch_eig_t<double, kMaxN64>(dev_probs, count, p, scratch, s);
+  return launch_eig_t<float, kMaxN>(dev_probs, count, p, scratch, s);
+}
+
+// ============================================================================
+// Evaluator: AtA += A^T A (fp64 products / accumulation), one CTA per 64x64
+// lower tile, fixed row order -> deterministic.
+// ============================================================================
+__global__ void __launch_bounds__(256) syrk_f64_kernel(const float* __restrict__ A, int64_t n, int64_t ld,
+                                                       int64_t d, double* __restrict__ AtA) {
+  int ti, tj;
+  tri_index(blockIdx.x, ti, tj);
+  const int64_t i0 = (int64_t)ti * 64, j0 = (int64_t)tj * 64;
+  __shared__ double As[16][65];
+  __shared__ double Bs[16][65];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  const int lrow = threadIdx.x >> 4, lcol = (threadIdx.x & 15) * 4;
+  for (int64_t r0 = 0; r0 < n; r0 += 16) {
+    const int64_t r = r0 + lrow;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t ci = i0 + lcol + q, cj = j0 + lcol + q;
+      As[lrow][lcol + q] = (r < n && ci < d) ? (double)A[r * ld + ci] : 0.0;
+      Bs[lrow][lcol + q] = (r < n && cj < d) ? (double)A[r * ld + cj] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      double a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { a[q] = As[k][ty * 4 + q]; b[q] = Bs[k][tx * 4 + q]; }
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const int64_t i = i0 + ty * 4 + x, j = j0 + tx * 4 + y;
+      if (i < d && j < d) {
+        AtA[i * d + j] += acc[x][y];
+        if (ti != tj) AtA[j * d + i] += acc[x][y];
+      }
+    }
+}
+
+cudaError_t launch_syrk_f64(const float* A, int64_t n, int64_t ld, int64_t d, double* AtA, cudaStream_t s) {
+  const int nt = (int)((d + 63) / 64);
+  syrk_f64_kernel<<<nt * (nt + 1) / 2, 256, 0, s>>>(A, n, ld, d, AtA);
+  return cudaGetLastError();
+}
+
+__global__ void sub_btb_kernel(double* __restrict__ M, const double* __restrict__ AtA, const float* __restrict__ B,
+                               int ell, int64_t d) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = blockIdx.y;
+  if (j >= d) return;
+  double s = 0.0;
+  for (int r = 0; r < ell; ++r) s = fma((double)B[(int64_t)r * d + i], (double)B[(int64_t)r * d + j], s);
+  M[i * d + j] = AtA[i * d + j] - s;
+}
+
+cudaError_t launch_sub_btb(double* M, const double* AtA, const float* B, int ell, int64_t d, cudaStream_t s) {
+  dim3 grid((unsigned)((d + 255) / 256), (unsigned)d);
+  sub_btb_kernel<<<grid, 256, 0, s>>>(M, AtA, B, ell, d);
+  return cudaGetLastError();
+}
+
+// Lanczos with full re-orthogonalisation (single CTA).  work layout (doubles):
+// alpha[kmax] | beta[kmax+1] | z[d] | h[kmax] | red[64]
+__device__ double block_sum_d(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum_d(v);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+  __syncthreads();
+  return s;
+}
+
+__device__ int sturm_count_d(const double* a, const double* b, int k, double x) {
+  int cnt = 0;
+  double q = a[0] - x;
+  const double piv = 1e-300;
+  if (fabs(q) < piv) q = -piv;
+  cnt += q < 0.0;
+  for (int i = 1; i < k; ++i) {
+    q = (a[i] - x) - b[i] * b[i] / q;
+    if (fabs(q) < piv) q = -piv;
+    cnt += q < 0.0;
+  }
+  return cnt;
+}
+
+__global__ void __launch_bounds__(1024, 1) lanczos_kernel(const double* __restrict__ M, int64_t d, int kmax,
+                                                          double* __restrict__ Q, double* __restrict__ work,
+                                                          double* __restrict__ out2) {
+  double* alpha = work;
+  double* beta = alpha + kmax;       // beta[j] couples q_{j-1}, q_j (beta[0] unused)
+  double* z = beta + kmax + 1;
+  double* h = z + d;
+  __shared__ double red[32];
+  __shared__ int s_k;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  // q0
+  double ss = 0.0;
+  for (int64_t i = tid; i < d; i += blockDim.x) {
+    const double v = 1.0 + 0.001 * (double)((i * 7919) % 101);
+    Q[i] = v;
+    ss += v * v;
+  }
+  ss = block_sum_d(ss, red);
+  const double inv0 = 1.0 / sqrt(ss);
+  for (int64_t i = tid; i < d; i += blockDim.x) Q[i] *= inv0;
+  if (tid == 0) s_k = kmax;
+  __syncthreads();
+  double amax = 0.0;
+  for (int j = 0; j < kmax; ++j) {
+    const double* q = Q + (int64_t)j * d;
+    for (int64_t r = warp; r < d; r += nw) {
+      const double* Mr = M + r * d;
+      double s = 0.0;
+      for (int64_t c = lane; c < d; c += 32) s = fma(Mr[c], q[c], s);
+      s = warp_sum_d(s);
+      if (lane == 0) z[r] = s;
+    }
+    __syncthreads();
+    double a = 0.0;
+    for (int64_t r = tid; r < d; r += blockDim.x) a = fma(q[r], z[r], a);
+    a = block_sum_d(a, red);
+    if (tid == 0) alpha[j] = a;
+    amax = fmax(amax, fabs(a));
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int i = warp; i <= j; i += nw) {
+        const double* qi = Q + (int64_t)i * d;
+        double s = 0.0;
+        for (int64_t c = lane; c < d; c += 32) s = fma(qi[c], z[c], s);
+        s = warp_sum_d(s);
+        if (lane == 0) h[i] = s;
+      }
+      __syncthreads();
+      for (int64_t r = tid; r < d; r += blockDim.x) {
+        double zr = z[r];
+        for (int i = 0; i <= j; ++i) zr = fma(-h[i], Q[(int64_t)i * d + r], zr);
+        z[r] = zr;
+      }
+      __syncthreads();
+    }
+    double b = 0.0;
+    for (int64_t r = tid; r < d; r += blockDim.x) b = fma(z[r], z[r], b);
+    b = sqrt(block_sum_d(b, red));
+    if (tid == 0) beta[j + 1] = b;
+    if (j + 1 == kmax || b <= 1e-12 * amax) {
+      if (tid == 0) s_k = j + 1;
+      break;
+    }
+    double* qn = Q + (int64_t)(j + 1) * d;
+    const double ib = 1.0 / b;
+    for (int64_t r = tid; r < d; r += blockDim.x) qn[r] = z[r] * ib;
+    __syncthreads();
+  }
+  __syncthreads();
+  // extreme eigenvalues of the k x k tridiagonal by bisection (fp64)
+  const int k = s_k;
+  if (tid < 2) {
+    double gl = 1e308, gu = -1e308;
+    for (int i = 0; i < k; ++i) {
+      const double em = (i > 0) ? fabs(beta[i]) : 0.0;
+      const double ep = (i + 1 < k) ? fabs(beta[i + 1]) : 0.0;
+      gl = fmin(gl, alpha[i] - em - ep);
+      gu = fmax(gu, alpha[i] + em + ep);
+    }
+    double lo = gl - 1e-12 * fabs(gl) - 1e-300, hi = gu + 1e-12 * fabs(gu) + 1e-300;
+    const int target = (tid == 0) ? k : 1;  // tid0: largest (count < x == k), tid1: smallest
+    for (int it = 0; it < 200; ++it) {
+      const double mid = 0.5 * (lo + hi);
+      if (mid <= lo || mid >= hi) break;
+      const int cnt = sturm_count_d(alpha, beta, k, mid);
+      if (cnt >= target) hi = mid;
+      else lo = mid;
+    }
+    out2[tid] = 0.5 * (lo + hi);
+  }
+}
+
+cudaError_t launch_lanczos(const double* M, int64_t d, int kmax, double* Q, double* work, double* out2,
+                           cudaStream_t s) {
+  lanczos_kernel<<<1, 1024, 0, s>>>(M, d, kmax, Q, work, out2);
+  return cudaGetLastError();
+}
+
+}  // namespace fdk

@@ -1,0 +1,332 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Tolerances (north_star / DESIGN.md reading C12):
+  sketch : ||B_gpu^T B_gpu - B_ora^T B_ora||_2 <= 1e-4 ||A||_F^2
+  err    : |err_gpu(A, B_gpu) - err_ora(A, B_ora)| <= 1e-3 err_ora  (relative)
+  evaluator alone (same B): relative 1e-6
+Inputs are seeded synthetic rows from fdgen (shared input module); no expected
+value comes from the CUDA path.
+"""
+import concurrent.futures as cf
+import os
+
+import numpy as np
+import pytest
+
+import fdgen
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+SKETCH_TOL = 1e-4
+ERR_TOL = 1e-3
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("-m gpu tests need a CUDA device")
+    yield
+
+
+def fd():
+    import paper_1501_06561_b200 as m
+    return m
+
+
+def spec_norm(M):
+    w = np.linalg.eigvalsh((M + M.T) / 2)
+    return max(abs(w[0]), abs(w[-1]))
+
+
+def gpu_sketch(A, ell, variant, alpha=0.2, n_shards=1, appends=None, ld_pad=0):
+    m = fd()
+    d = A.shape[1]
+    sk = m.Sketcher(d, ell, variant, alpha=alpha, n_shards=n_shards)
+    if ld_pad:
+        big = torch.zeros((A.shape[0], d + ld_pad), dtype=torch.float32, device="cuda")
+        big[:, :d] = torch.from_numpy(A)
+        Ad = big[:, :d]
+    else:
+        Ad = torch.from_numpy(A).cuda()
+    if appends is None:
+        sk.append(Ad)
+    else:
+        o = 0
+        for a in appends:
+            sk.append(Ad[o:o + a])
+            o += a
+    B, st = sk.sketch()
+    torch.cuda.synchronize()
+    Bn = B.cpu().numpy().astype(np.float64)
+    sk.close()
+    return Bn, st, Ad
+
+
+def check_parity(A, ell, variant, alpha=0.2, n_shards=1, appends=None, ld_pad=0, err_tol=ERR_TOL, err_abs=1e-7):
+    Bg, st, Ad = gpu_sketch(A, ell, variant, alpha, n_shards, appends, ld_pad)
+    r = oracle.sketch(A, ell, variant, alpha=alpha, n_shards=n_shards, appends=appends)
+    frob = r.frob_sq
+    diff = spec_norm(Bg.T @ Bg - r.B.T @ r.B)
+    assert diff <= SKETCH_TOL * frob, f"sketch diff {diff / frob:.3e} * frob"
+    # statistics
+    assert st["rows_seen"] == A.shape[0]
+    assert st["n_shrinks"] == r.n_shrinks
+    assert abs(st["frob_sq"] - frob) <= 1e-9 * frob
+    assert abs(st["delta_total"] - r.delta_total) <= 1e-4 * frob + 1e-5 * r.delta_total
+    assert abs(st["removed_mass"] - r.removed) <= 2e-4 * frob
+    # the GPU ledger identity ||A||_F^2 - ||B||_F^2 = removed (Lemma 3)
+    assert abs((st["frob_sq"] - np.sum(Bg ** 2)) - st["removed_mass"]) <= 1e-4 * frob
+    # last row zero, rows orthogonal
+    assert np.all(Bg[-1] == 0)
+    if frob > 0:
+        eg = fd().cov_err(Ad, torch.from_numpy(Bg.astype(np.float32)).cuda())["err"]
+        eo = oracle.cov_err(A, r.B)["err"]
+        assert abs(eg - eo) <= err_tol * eo + err_abs, f"err gpu {eg} oracle {eo}"
+    return Bg, r
+
+
+# ---------------------------------------------------------------------------
+def test_generator_host_device_bitexact():
+    cases = [("c1", 0, 2000), ("c2", 0, 3000), ("c4", 4_000_000, 2048), ("c5", 0, 20000), ("c3", 0, 1500)]
+    for cfg, r0, nr in cases:
+        w = fdgen.config(cfg, n=(1500 if cfg == "c3" else None))
+        gen = fdgen.DeviceGenerator(w)
+        if cfg == "c3":
+            w.xminmax = fdgen.host_minmax(w)
+            assert w.xminmax == gen.minmax()
+        out = torch.empty((nr, w.d), dtype=torch.float32, device="cuda")
+        gen.fill(out, r0)
+        h = fdgen.host_rows(w, r0, nr)
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), h.view(np.uint32)), cfg
+
+
+@pytest.mark.parametrize("variant", ["fd", "fast_fd", "alpha_fd", "fast_alpha_fd", "isvd", "fast_isvd"])
+@pytest.mark.parametrize("shards", [1, 4])
+def test_parity_c1(variant, shards):
+    A = fdgen.host_rows(fdgen.config("c1"))
+    check_parity(A, 16, variant, n_shards=shards)
+
+
+_C2 = None
+
+
+def _c2():
+    global _C2
+    if _C2 is None:
+        _C2 = fdgen.host_rows(fdgen.config("c2"))
+    return _C2
+
+
+@pytest.mark.parametrize("variant", ["fd", "fast_fd", "alpha_fd", "fast_alpha_fd", "isvd", "fast_isvd"])
+def test_parity_c2_ell20(variant):
+    check_parity(_c2(), 20, variant)
+
+
+@pytest.mark.parametrize("ell", [40, 60, 80, 100])
+@pytest.mark.parametrize("variant", ["fast_fd", "fast_alpha_fd", "fast_isvd"])
+def test_parity_c2_batched(variant, ell):
+    check_parity(_c2(), ell, variant)
+
+
+@pytest.mark.parametrize("variant", ["fd", "alpha_fd", "isvd"])
+def test_parity_c2_perrow_ell40(variant):
+    check_parity(_c2(), 40, variant)
+
+
+def test_parity_c5_prefix_perrow():
+    w = fdgen.config("c5", n=20000)
+    w.extra["block_rows"] = 10000  # keep c5's 10000-row blocks on the prefix
+    A = fdgen.host_rows(w)
+    for v in ("fd", "alpha_fd", "isvd"):
+        check_parity(A, 32, v)
+
+
+def test_evaluator_parity_same_B():
+    """GPU evaluator vs oracle evaluator on identical (A, B_oracle): relative 1e-6 (C12 iii)."""
+    for cfg, ell, v in (("c1", 16, "fd"), ("c2", 20, "fast_fd")):
+        A = fdgen.host_rows(fdgen.config(cfg)) if cfg == "c1" else _c2()
+        r = oracle.sketch(A, ell, v)
+        eo = oracle.cov_err(A, r.B)
+        eg = fd().cov_err(torch.from_numpy(A).cuda(), torch.from_numpy(r.B.astype(np.float32)).cuda())
+        eo32 = oracle.cov_err(A, r.B.astype(np.float32).astype(np.float64))
+        assert abs(eg["err"] - eo32["err"]) <= 1e-6 * eo32["err"]
+        assert abs(eg["lmin"] - eo32["lmin"]) <= 1e-6 * eo32["err"]
+        assert abs(eo32["err"] - eo["err"]) <= 1e-5 * eo["err"]
+
+
+# ---------------------------------------------------------------------------
+# edge cases
+# ---------------------------------------------------------------------------
+def test_fewer_rows_than_ell_is_lossless():
+    rng = np.random.default_rng(1)
+    A = rng.standard_normal((9, 33)).astype(np.float32)
+    for v in ("fd", "fast_fd", "isvd"):
+        Bg, r = check_parity(A, 12, v)
+        assert spec_norm(Bg.T @ Bg - A.T.astype(np.float64) @ A) <= 1e-5 * np.sum(A.astype(np.float64) ** 2)
+
+
+def test_empty_and_zero_streams():
+    m = fd()
+    sk = m.Sketcher(20, 4, "fast_fd", n_shards=3)
+    B, st = sk.sketch()
+    assert torch.count_nonzero(B).item() == 0 and st["rows_seen"] == 0 and st["frob_sq"] == 0
+    sk.append(torch.zeros((50, 20), device="cuda"))
+    B, st = sk.sketch()
+    assert torch.count_nonzero(B).item() == 0 and st["delta_total"] == 0 and st["frob_sq"] == 0
+    sk.close()
+
+
+def test_ragged_shards_and_multiple_appends():
+    A = fdgen.host_rows(fdgen.config("c1"))[:1003]
+    check_parity(A, 8, "fast_alpha_fd", n_shards=7, appends=[500, 503])
+    check_parity(A, 8, "fd", n_shards=3, appends=[1, 2, 1000])
+
+
+def test_odd_d_and_strided_rows():
+    rng = np.random.default_rng(2)
+    A = (rng.standard_normal((700, 37)) * np.linspace(3, 0.1, 37)).astype(np.float32)
+    check_parity(A, 10, "fast_fd", ld_pad=3)
+    check_parity(A, 10, "alpha_fd", n_shards=2, ld_pad=5)
+
+
+def test_exact_low_rank():
+    rng = np.random.default_rng(3)
+    ell = 16
+    A = (rng.standard_normal((3000, ell - 1)) @ rng.standard_normal((ell - 1, 96))).astype(np.float32)
+    for v in ("fast_fd", "fd"):
+        # err_oracle ~ 1e-14 (exact); the fp32 path reaches its rounding floor ~1e-6
+        Bg, r = check_parity(A, ell, v, err_abs=1e-5)
+        e = fd().cov_err(torch.from_numpy(A).cuda(), torch.from_numpy(Bg.astype(np.float32)).cuda())
+        assert e["err"] < 1e-5
+
+
+def test_degenerate_ties():
+    """Repeated orthogonal rows -> exactly tied singular values.  The FD rule is
+    continuous in lambda, so B^T B is unique and must match the oracle; alpha-FD /
+    iSVD are discontinuous at the shrink boundary, so with ties several sketches
+    are correct: check that the GPU one is valid (Lemma 1 / Lemma 3 / Theorem)."""
+    d = 24
+    A = np.tile(np.eye(d, dtype=np.float32) * 2.0, (30, 1))
+    for v in ("fd", "fast_fd"):
+        check_parity(A, 8, v, err_tol=2e-2)
+    m = fd()
+    AtA = A.T.astype(np.float64) @ A
+    frob = float(np.trace(AtA))
+    for v in ("alpha_fd", "fast_alpha_fd", "isvd", "fast_isvd"):
+        Bg, st, _ = gpu_sketch(A, 8, v)
+        ev = np.linalg.eigvalsh(AtA - Bg.T @ Bg)
+        assert ev[0] >= -1e-5 * frob                               # Property 1
+        assert ev[-1] <= st["delta_total"] * (1 + 1e-5) + 1e-5 * frob  # Property 2
+        assert abs(frob - np.sum(Bg ** 2) - st["removed_mass"]) <= 1e-5 * frob  # Lemma 3 ledger
+        if not v.endswith("isvd"):
+            mm = oracle.alpha_m(8, 0.2)
+            s2 = np.linalg.svd(A.astype(np.float64), compute_uv=False) ** 2
+            assert ev[-1] <= s2.sum() / mm * (1 + 1e-5)                 # Theorem, k = 0
+    del m
+
+
+def test_max_perrow_size():
+    rng = np.random.default_rng(4)
+    A = (rng.standard_normal((300, 300)) * np.linspace(2, 0.05, 300)).astype(np.float32)
+    check_parity(A, 256, "fd")  # per-row Gram size N = 256 = FD_MAX_N
+
+
+def test_unsupported_and_invalid():
+    m = fd()
+    with pytest.raises(m.FdError) as e:
+        m.Sketcher(64, 129, "fast_fd")
+    assert "UNSUPPORTED" in str(e.value)
+    with pytest.raises(m.FdError):
+        m.Sketcher(64, 8, "alpha_fd", alpha=1.5)
+
+
+def test_nonfinite_is_sticky():
+    m = fd()
+    A = torch.randn((100, 16), device="cuda")
+    A[37, 5] = float("nan")
+    sk = m.Sketcher(16, 4, "fast_fd")
+    sk.append(A)
+    with pytest.raises(m.FdError) as e:
+        sk.sketch()
+    assert "NONFINITE" in str(e.value)
+    with pytest.raises(m.FdError) as e:
+        sk.append(A)
+    assert "STATE" in str(e.value)
+
+
+def test_snapshot_is_non_destructive():
+    A = fdgen.host_rows(fdgen.config("c1"))
+    m = fd()
+    sk = m.Sketcher(64, 16, "fast_fd", n_shards=2)
+    Ad = torch.from_numpy(A).cuda()
+    sk.append(Ad[:1000])
+    sk.sketch()
+    sk.append(Ad[1000:])
+    B, _ = sk.sketch()
+    r = oracle.sketch(A, 16, "fast_fd", n_shards=2, appends=[1000, 1000])
+    Bn = B.cpu().numpy().astype(np.float64)
+    assert spec_norm(Bn.T @ Bn - r.B.T @ r.B) <= SKETCH_TOL * r.frob_sq
+
+
+def test_merge_api_matches_oracle_tree():
+    A = fdgen.host_rows(fdgen.config("c1"))
+    r = oracle.sketch(A, 16, "fast_fd", n_shards=5, want_shards=True)
+    m = fd()
+    sk = m.Sketcher(64, 16, "fast_fd")
+    S = torch.from_numpy(r.shards.astype(np.float32)).cuda()
+    B, st = sk.merge(S, stats=True)
+    Bo, sto = oracle.merge(r.shards.astype(np.float32).astype(np.float64), 16, "fast_fd")
+    Bn = B.cpu().numpy().astype(np.float64)
+    assert spec_norm(Bn.T @ Bn - Bo.T @ Bo) <= SKETCH_TOL * r.frob_sq
+    assert st["n_shrinks"] == 4
+
+
+# ---------------------------------------------------------------------------
+# full-size c4 at the bench launch configuration: properties + sampled shards
+# ---------------------------------------------------------------------------
+C4_SHARDS = 1184
+
+
+def test_c4_fullsize_bench_config():
+    m = fd()
+    w = fdgen.config("c4")
+    gen = fdgen.DeviceGenerator(w)
+    A = torch.empty((w.n, w.d), dtype=torch.float32, device="cuda")
+    gen.fill(A)
+    ell = 128
+    sk = m.Sketcher(w.d, ell, "fast_fd", n_shards=C4_SHARDS)
+    sk.append(A)
+    B, st = sk.sketch()
+    # sampled shard parity: shard s's rows through the oracle (one by one)
+    q, rr = divmod(w.n, C4_SHARDS)
+    picks = [0, 593, C4_SHARDS - 1]
+
+    def one(s):
+        start = s * q + min(s, rr)
+        ln = q + (1 if s < rr else 0)
+        rows = fdgen.host_rows(w, start, ln, nthreads=1)
+        return s, rows, oracle.sketch(rows, ell, "fast_fd", nthreads=1)
+
+    with cf.ThreadPoolExecutor(len(picks)) as ex:
+        res = list(ex.map(one, picks))
+    for s, rows, r in res:
+        Bs = sk.shard_sketch(s).cpu().numpy().astype(np.float64)
+        assert spec_norm(Bs.T @ Bs - r.B.T @ r.B) <= SKETCH_TOL * r.frob_sq, s
+    # properties at full size (GPU evaluator): PSD difference (Lemma 1), bound, ledger
+    e = m.cov_err(A, B)
+    frob = st["frob_sq"]
+    assert e["lmin"] >= -1e-6
+    assert e["err"] <= 1.0 / ell
+    assert e["err"] * frob <= st["delta_total"] * (1 + 1e-4)
+    Bn = B.cpu().numpy().astype(np.float64)
+    assert abs(frob - np.sum(Bn ** 2) - st["removed_mass"]) <= 1e-4 * frob
+    assert st["rows_seen"] == w.n
+    # sampled entries of A^T A (evaluator Gram) vs fp64 dot products of columns
+    AtA = torch.zeros((w.d, w.d), dtype=torch.float64, device="cuda")
+    m.cov_gram_partial(A, AtA)
+    for (i, j) in ((0, 0), (5, 700), (1023, 17)):
+        ref = torch.dot(A[:, i].double(), A[:, j].double()).item()
+        assert abs(AtA[i, j].item() - ref) <= 1e-9 * frob
+    sk.close()
