@@ -3,6 +3,7 @@
 // evaluator entry points.  All arithmetic runs in the kernels of fd_kernels.cu.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -345,6 +346,14 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
   h->device = cfg->device;
   h->prm.d = D.d; h->prm.ldb = D.ldb; h->prm.ldg = D.ldg; h->prm.ell = D.ell; h->prm.rule = D.rule; h->prm.m = D.m;
   h->prm.f64 = 0;
+  h->prm.dbg = nullptr;
+  if (getenv("FD_DEBUG_EIG")) {
+    void* dbgp = nullptr;
+    if (cudaMalloc(&dbgp, 16 * sizeof(long long)) == cudaSuccess) {
+      cudaMemset(dbgp, 0, 16 * sizeof(long long));
+      h->prm.dbg = static_cast<long long*>(dbgp);
+    }
+  }
   h->buf[0] = reinterpret_cast<float*>(h->ws + Lo.buf0);
   h->buf[1] = reinterpret_cast<float*>(h->ws + Lo.buf1);
   h->nodes = reinterpret_cast<float*>(h->ws + Lo.nodes);
@@ -620,6 +629,14 @@ fd_status fd_cov_err(const float* A, int64_t n, int64_t ld, const float* B, int3
 }
 
 const char* fd_last_error(void) { return g_err.c_str(); }
+
+// debug: copy the eig phase trace (16 x int64) of the last eig launch (FD_DEBUG_EIG set)
+int32_t fd_debug_eig_trace(fd_handle* h, long long* out16) {
+  if (!h || !h->prm.dbg) return -1;
+  cudaStreamSynchronize(h->stream);
+  cudaMemcpy(out16, h->prm.dbg, 16 * sizeof(long long), cudaMemcpyDeviceToHost);
+  return 0;
+}
 
 const char* fd_version(void) { return "fd-b200 0.1 (sm_100a)"; }
 

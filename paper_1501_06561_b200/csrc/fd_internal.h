@@ -54,6 +54,7 @@ struct Params {
   int rule;
   int m;         // alpha-FD: number of trailing values that shrink
   int f64;       // 1: Gram / eigen / reconstruct accumulate in fp64 (per-row chains)
+  long long* dbg;  // optional phase clock trace of problem 0 (FD_DEBUG_EIG), else null
 };
 
 // All launchers return cudaGetLastError() after enqueueing.

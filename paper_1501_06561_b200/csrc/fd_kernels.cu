@@ -239,15 +239,17 @@ cudaError_t launch_recon(const Prob* dev_probs, int count, int nmax, const Param
 // ============================================================================
 constexpr int kNW = kEigThreads / 32;  // 16 warps
 // fp64 scratch per CTA slot: LDL^T factors (2N per cluster thread) + Z (N per vector)
-constexpr size_t kSlotDoubles = (size_t)kMaxN * 2 * kMaxN + (size_t)kMaxN * kMaxN;
+constexpr size_t kSlotDoubles = (size_t)3 * kMaxN * kMaxN;
 
 size_t eig_scratch_bytes() { return (size_t)kNumSMs * kSlotDoubles * sizeof(double); }
 
 template <typename T, int NM>
 struct EigCfg {
+  static_assert(NM % 32 == 0, "NM must be a multiple of 32");
   static constexpr int kPk = NM * (NM + 1) / 2;
-  static constexpr int kWork = 32 * NM;
-  static constexpr size_t kT = (size_t)kPk + kWork + 10 * NM + 64;  // elements of T
+  static constexpr int kPart = kNW * NM + 32 * (NM + 1);  // ppart[16][NM] + colpart[32][NM+1]
+  static constexpr int kVec = 13;                 // vector arrays of NM
+  static constexpr size_t kT = (size_t)kPk + kPart + kVec * NM + 64;  // elements of T
   static constexpr size_t kBytes = kT * sizeof(T) + 2 * NM * sizeof(int) + 16;
 };
 
@@ -273,15 +275,19 @@ __device__ __forceinline__ T block_sum(T v, T* red) {
   return s;
 }
 
+__device__ __forceinline__ float fast_div(float a, float b) { return __fdividef(a, b); }
+__device__ __forceinline__ double fast_div(double a, double b) { return a / b; }
+
 // number of eigenvalues of the tridiagonal (d, e2) strictly less than x
 // (Sturm count with the LAPACK xSTEBZ pivot guard)
 template <typename T>
-__device__ __forceinline__ int sturm_count(const T* dd, const T* e2, int N, T x, T pivmin) {
+__device__ __forceinline__ int sturm_count(const T* __restrict__ dd, const T* __restrict__ e2, int N, T x, T pivmin) {
   T q = dd[0] - x;
   if (fabs(q) < pivmin) q = -pivmin;
   int cnt = q < T(0);
+#pragma unroll 4
   for (int i = 1; i < N; ++i) {
-    q = (dd[i] - x) - e2[i - 1] / q;
+    q = (dd[i] - x) - fast_div(e2[i - 1], q);
     if (fabs(q) < pivmin) q = -pivmin;
     cnt += q < T(0);
   }
@@ -306,36 +312,43 @@ template <typename T, int NM>
 __global__ void __launch_bounds__(kEigThreads, 1)
 eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restrict__ scratch) {
   using C = EigCfg<T, NM>;
+  constexpr int NT = NM / 32;   // row blocks (lane <-> row 32t + lane)
+  constexpr int NK = NM / kNW;  // columns per warp (warp <-> column warp + 16k)
   extern __shared__ __align__(16) unsigned char smraw[];
   T* sm = reinterpret_cast<T*>(smraw);
   T* Apk = sm;
-  T* work = Apk + C::kPk;
-  T* vs = work + C::kWork;
-  T* wsv = vs + NM;
-  T* pcol = wsv + NM;
-  T* dd = pcol + NM;
+  T* ppart = Apk + C::kPk;        // [kNW][NM]  per-warp row partials of the SYMV
+  T* colpart = ppart + kNW * NM;  // [32][NM+1] per-lane column partials (padded: no bank conflicts)
+  T* vbuf0 = colpart + 32 * (NM + 1);   // v / w of the current and previous Householder step
+  T* wbuf0 = vbuf0 + NM;
+  T* vbuf1 = wbuf0 + NM;
+  T* wbuf1 = vbuf1 + NM;
+  T* dd = wbuf1 + NM;
   T* ee = dd + NM;
   T* e2 = ee + NM;
   T* tau = e2 + NM;
   T* lam = tau + NM;
   T* wgt = lam + NM;
   T* spv = wgt + NM;
-  T* red = spv + NM;
+  T* pvec = spv + NM;   // per-vector normalisation scale of the inverse iteration
+  T* red = pvec + 2 * NM;
   int* cstart = reinterpret_cast<int*>(red + 64);
   int* clen = cstart + NM;
   __shared__ int s_ncl;
-  __shared__ T s_gl, s_gu;
-  constexpr int NT = (NM + 31) / 32;  // row-blocks of 32 per column
+  __shared__ T s_gl, s_gu, s_a1, s_a2;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* slot = scratch + (size_t)blockIdx.x * kSlotDoubles;
-  double* LDs = slot;                              // [cluster][2*kMaxN]
-  double* Zs = slot + (size_t)kMaxN * 2 * kMaxN;   // [j][kMaxN]
+  // element-major (coalesced across threads): LF[i][cl], RD[i][cl], Zs[i][j]
+  double* LF = slot;
+  double* RD = slot + (size_t)kMaxN * kMaxN;
+  double* Zs = slot + (size_t)2 * kMaxN * kMaxN;
 
   for (int pi = blockIdx.x; pi < count; pi += gridDim.x) {
     const Prob P = probs[pi];
     const int N = P.rows0 + P.rows1;
     const int ell = p.ell;
+    long long t_ph0 = clock64();
     const T* G = static_cast<const T*>(P.G);
     T* Wt = static_cast<T*>(P.Wt);
     // ---------------- load lower triangle (packed, column-major) ----------------
@@ -343,105 +356,153 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
       const int oc = pk_off(c, N);
       for (int r = c + lane; r < N; r += 32) Apk[oc + r - c] = G[(int64_t)r * p.ldg + c];
     }
+    for (int r = tid; r < NM; r += blockDim.x) { vbuf1[r] = T(0); wbuf1[r] = T(0); }
     __syncthreads();
+    if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[1] += t_ - t_ph0; t_ph0 = t_; }
     // ---------------- Householder tridiagonalisation (lower, xSYTD2 order) ----------------
+    // One fused shared-memory pass per step: the pending rank-2 update of step i-1
+    // is applied while the SYMV of step i is accumulated from the pre-update values;
+    // p = A^(i) v is then recovered exactly with the rank-2 correction
+    //   A^(i) v = A^(i-1) v - v_{i-1} (w_{i-1}^T v) - w_{i-1} (v_{i-1}^T v).
+    T* vc = vbuf0; T* wc = wbuf0;   // step i
+    T* vp = vbuf1; T* wp = wbuf1;   // step i-1 (zero before the first step)
     for (int i = 0; i < N - 2; ++i) {
-      const int n = N - i - 1;
       const int oi = pk_off(i, N);
+      // (a) warp 0: apply update i-1 to column i, build the reflector of column i
       if (warp == 0) {
-        const T alpha = Apk[oi + 1];
-        T s = T(0);
-        for (int k = 1 + lane; k < n; k += 32) {
-          const T x = Apk[oi + 1 + k];
-          s = fma(x, x, s);
+        const T vpi = vp[i], wpi = wp[i];
+        T sig = T(0);
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int R = 32 * t + lane;
+          if (R >= i && R < N) {
+            T a = Apk[oi + R - i];
+            a = fma(-vp[R], wpi, a);
+            a = fma(-wp[R], vpi, a);
+            Apk[oi + R - i] = a;
+            if (R >= i + 2) sig = fma(a, a, sig);
+          }
         }
-        s = wsum(s);
+        sig = wsum(sig);
+        __syncwarp();
+        const T alpha = Apk[oi + 1];
         T t_, beta, scale;
-        if (s == T(0)) {
+        if (sig == T(0)) {
           t_ = T(0); beta = alpha; scale = T(0);
         } else {
-          const T nrm = sqrt(fma(alpha, alpha, s));
+          const T nrm = sqrt(fma(alpha, alpha, sig));
           beta = (alpha <= T(0)) ? nrm : -nrm;
           t_ = (beta - alpha) / beta;
           scale = T(1) / (alpha - beta);
         }
-        for (int k = lane; k < n; k += 32) {
-          T vk = T(1);
-          if (k > 0) {
-            vk = Apk[oi + 1 + k] * scale;
-            Apk[oi + 1 + k] = vk;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int R = 32 * t + lane;
+          T v = T(0);
+          if (R == i + 1) v = T(1);
+          else if (R >= i + 2 && R < N) {
+            v = Apk[oi + R - i] * scale;
+            Apk[oi + R - i] = v;
           }
-          vs[k] = vk;
+          vc[R] = v;
         }
         if (lane == 0) { tau[i] = t_; dd[i] = Apk[oi]; ee[i] = beta; }
       }
       __syncthreads();
       const T t_ = tau[i];
-      if (t_ == T(0)) continue;
-      // p = A22 v (packed SYMV), column-owner warps, register row accumulators
-      T acc[NT];
-#pragma unroll
-      for (int t = 0; t < NT; ++t) acc[t] = T(0);
-      for (int c = warp; c < n; c += kNW) {
-        const int base = pk_off(i + 1 + c, N);
-        const T vc = vs[c];
-        T colsum = T(0);
-        const int t0 = c >> 5;
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          if (t < t0 || 32 * t >= n) continue;
-          const int r = 32 * t + lane;
-          if (r >= c && r < n) {
-            const T a = Apk[base + r - c];
-            colsum = fma(a, vs[r], colsum);
-            if (r > c) acc[t] = fma(a, vc, acc[t]);
-          }
-        }
-        colsum = wsum(colsum);
-        if (lane == 0) pcol[c] = colsum;
-      }
+      // (b) fused pass over the trailing matrix (columns >= i+1)
+      T racc[NT];
+      T vr[NT], vpr[NT], wpr[NT];
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
-        const int r = 32 * t + lane;
-        if (r < n) work[warp * NM + r] = acc[t];
+        racc[t] = T(0);
+        vr[t] = vc[32 * t + lane];
+        vpr[t] = vp[32 * t + lane];
+        wpr[t] = wp[32 * t + lane];
       }
-      __syncthreads();
-      T pr = T(0), prod = T(0);
-      if (tid < n) {
-        T s2 = pcol[tid];
 #pragma unroll
-        for (int w2 = 0; w2 < kNW; ++w2) s2 += work[w2 * NM + tid];
-        pr = t_ * s2;
-        prod = pr * vs[tid];
-      }
-      const T K = block_sum(prod, red);
-      if (tid < n) wsv[tid] = fma(T(-0.5) * t_ * K, vs[tid], pr);
-      __syncthreads();
-      // A22 -= v w^T + w v^T
-      for (int c = warp; c < n; c += kNW) {
-        const int base = pk_off(i + 1 + c, N);
-        const T vc = vs[c], wc = wsv[c];
-        for (int r = c + lane; r < n; r += 32) {
-          T a = Apk[base + r - c];
-          a = fma(-vs[r], wc, a);
-          a = fma(-wsv[r], vc, a);
-          Apk[base + r - c] = a;
+      for (int k = 0; k < NK; ++k) {
+        const int Cc = warp + kNW * k;
+        if (Cc <= i || Cc >= N) continue;  // warp-uniform
+        const int base = pk_off(Cc, N) - Cc;
+        const T vcc = vc[Cc], vpc = vp[Cc], wpc = wp[Cc];
+        // all loads of the column first (no store->load ordering stalls), then compute, then store
+        T a[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int R = 32 * t + lane;
+          a[t] = (32 * t + 31 >= Cc && R >= Cc && R < N) ? Apk[base + R] : T(0);
         }
+        T csum = T(0);
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int R = 32 * t + lane;
+          racc[t] = fma(a[t], vcc, racc[t]);
+          if (R > Cc) csum = fma(a[t], vr[t], csum);
+          a[t] = fma(-vpr[t], wpc, a[t]);
+          a[t] = fma(-wpr[t], vpc, a[t]);
+        }
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          if (32 * t + 31 < Cc) continue;  // warp-uniform
+          const int R = 32 * t + lane;
+          if (R >= Cc && R < N) Apk[base + R] = a[t];
+        }
+        colpart[lane * (NM + 1) + Cc] = csum;
+      }
+#pragma unroll
+      for (int t = 0; t < NT; ++t) ppart[warp * NM + 32 * t + lane] = racc[t];
+      __syncthreads();
+      // (c) raw = A^(i-1) v (partials), a1 = w_{i-1}.v, a2 = v_{i-1}.v, S0 = raw.v in ONE block
+      //     reduction; p = tau (raw - v_{i-1} a1 - w_{i-1} a2), K = p.v = tau (S0 - 2 a1 a2),
+      //     w = p - tau/2 K v.
+      T raw = T(0), vR = T(0), vpR = T(0), wpR = T(0);
+      if (tid > i && tid < N) {
+#pragma unroll
+        for (int w2 = 0; w2 < kNW; ++w2) raw += ppart[w2 * NM + tid];
+#pragma unroll 8
+        for (int l = 0; l < 32; ++l) raw += colpart[l * (NM + 1) + tid];
+        vR = vc[tid]; vpR = vp[tid]; wpR = wp[tid];
+      }
+      T r3[3] = {raw * vR, wpR * vR, vpR * vR};
+#pragma unroll
+      for (int q = 0; q < 3; ++q) r3[q] = wsum(r3[q]);
+      if (lane == 0) { red[warp] = r3[0]; red[16 + warp] = r3[1]; red[32 + warp] = r3[2]; }
+      __syncthreads();
+      T S0 = T(0), a1 = T(0), a2 = T(0);
+#pragma unroll
+      for (int w2 = 0; w2 < kNW; ++w2) { S0 += red[w2]; a1 += red[16 + w2]; a2 += red[32 + w2]; }
+      const T K = t_ * (S0 - T(2) * a1 * a2);
+      if (tid < NM) {
+        T wv = T(0);
+        if (tid > i && tid < N) {
+          const T pr = t_ * (raw - vpR * a1 - wpR * a2);
+          wv = fma(T(-0.5) * t_ * K, vR, pr);
+        }
+        wc[tid] = wv;
       }
       __syncthreads();
+      // rotate step buffers
+      T* tv = vp; vp = vc; vc = tv;
+      T* tw = wp; wp = wc; wc = tw;
     }
+    // pending update of the last step on the trailing 2 x 2 block, then the last entries
     if (tid == 0) {
       if (N >= 2) {
-        dd[N - 2] = Apk[pk_off(N - 2, N)];
-        ee[N - 2] = Apk[pk_off(N - 2, N) + 1];
-        tau[N - 2] = T(0);
-        dd[N - 1] = Apk[pk_off(N - 1, N)];
+        const int a = N - 2, b = N - 1;
+        const int oa = pk_off(a, N), ob = pk_off(b, N);
+        T aa = Apk[oa], ba = Apk[oa + 1], bb = Apk[ob];
+        aa -= T(2) * vp[a] * wp[a];
+        ba -= vp[b] * wp[a] + wp[b] * vp[a];
+        bb -= T(2) * vp[b] * wp[b];
+        dd[a] = aa; ee[a] = ba; dd[b] = bb; tau[a] = T(0);
       } else if (N == 1) {
         dd[0] = Apk[0];
       }
       if (N >= 1) { ee[N - 1] = T(0); tau[N - 1] = T(0); }
     }
     __syncthreads();
+    if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[2] += t_ - t_ph0; t_ph0 = t_; }
     // ---------------- eigenvalues: multisection bisection ----------------
     const int K = min(ell, N);        // top-K eigenvalues needed (lambda_ell = delta)
     const int J = min(ell - 1, N);    // retained eigenvectors
@@ -499,6 +560,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
       if (sub == 0 && j < K) lam[j] = fmax(T(0.5) * (lo + hi), T(0));  // clamp (reading C8)
     }
     __syncthreads();
+    if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[3] += t_ - t_ph0; t_ph0 = t_; }
     // ---------------- ReduceRank rule ----------------
     const T delta = (ell <= N) ? lam[ell - 1] : T(0);
     if (tid < J) {
@@ -538,93 +600,201 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
       s_ncl = ncl;
     }
     __syncthreads();
+    if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[4] += t_ - t_ph0; t_ph0 = t_; }
     // ---------------- eigenvectors of T: fp64 inverse iteration ----------------
     const int ncl = s_ncl;
     const double tiny = 2.3e-16 * (double)bnorm + 1e-300;
     for (int cl = tid; cl < ncl; cl += blockDim.x) {
-      double* lf = LDs + (size_t)cl * 2 * kMaxN;
-      double* dp = lf + kMaxN;
+      double* lf = LF + cl;   // lf[i * kMaxN]  multipliers of L
+      double* rdp = RD + cl;  // rdp[i * kMaxN] reciprocal pivots of D
       const int j0 = cstart[cl], j1 = cstart[cl] + clen[cl];
       for (int j = j0; j < j1; ++j) {
         if (wgt[j] == T(0)) continue;
-        double* z = Zs + (size_t)j * kMaxN;
+        double* z = Zs + j;   // z[i * kMaxN]
         const double mu = (double)lam[j];
-        // T - mu I = L D L^T
+        // iteration 0: L D L^T = T - mu I (tiny pivots perturbed) fused with the
+        // forward solve L u = b, v = D^-1 u of the start vector b.
         double dpi = (double)dd[0] - mu;
         if (fabs(dpi) < tiny) dpi = (dpi < 0.0) ? -tiny : tiny;
-        dp[0] = dpi;
+        double rd = 1.0 / dpi;
+        rdp[0] = rd;
+        double u = 1.0 + 0.5 * (double)(((1) * 7919 + (j + 3) * 104729) % 211) / 211.0;
+        z[0] = u * rd;
         for (int i = 0; i < N - 1; ++i) {
-          const double li = (double)ee[i] / dpi;
-          lf[i] = li;
-          dpi = ((double)dd[i + 1] - mu) - li * (double)ee[i];
+          const double e = (double)ee[i];
+          const double li = e * rd;
+          lf[(size_t)i * kMaxN] = li;
+          dpi = ((double)dd[i + 1] - mu) - li * e;
           if (fabs(dpi) < tiny) dpi = (dpi < 0.0) ? -tiny : tiny;
-          dp[i + 1] = dpi;
+          rd = 1.0 / dpi;
+          rdp[(size_t)(i + 1) * kMaxN] = rd;
+          const double b = 1.0 + 0.5 * (double)(((i + 2) * 7919 + (j + 3) * 104729) % 211) / 211.0;
+          u = b - li * u;
+          z[(size_t)(i + 1) * kMaxN] = u * rd;
         }
-        for (int i = 0; i < N; ++i) z[i] = 1.0 + 0.5 * (double)(((i + 1) * 7919 + (j + 3) * 104729) % 211) / 211.0;
+        double sc = 1.0;
         for (int it = 0; it < 3; ++it) {
-          for (int i = 1; i < N; ++i) z[i] -= lf[i - 1] * z[i - 1];
-          for (int i = 0; i < N; ++i) z[i] /= dp[i];
-          for (int i = N - 2; i >= 0; --i) z[i] -= lf[i] * z[i + 1];
-          double mx = 0.0;
-          for (int i = 0; i < N; ++i) mx = fmax(mx, fabs(z[i]));
-          const double inv = (mx > 0.0) ? 1.0 / mx : 1.0;
-          for (int i = 0; i < N; ++i) z[i] *= inv;
-          for (int pass = 0; pass < 2; ++pass)
-            for (int k = j0; k < j; ++k) {
-              if (wgt[k] == T(0)) continue;
-              const double* zk = Zs + (size_t)k * kMaxN;
-              double h = 0.0;
-              for (int i = 0; i < N; ++i) h += zk[i] * z[i];
-              for (int i = 0; i < N; ++i) z[i] -= h * zk[i];
+          if (it > 0) {  // forward solve of the (scaled) previous iterate, 8-element load batches
+            u = 0.0;
+            double lprev = 0.0;
+            for (int i0 = 0; i0 < N; i0 += 8) {
+              double zb[8], lb[8], rb[8];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const int i = i0 + q;
+                zb[q] = (i < N) ? z[(size_t)i * kMaxN] : 0.0;
+                lb[q] = (i < N) ? lf[(size_t)i * kMaxN] : 0.0;
+                rb[q] = (i < N) ? rdp[(size_t)i * kMaxN] : 0.0;
+              }
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                u = zb[q] * sc - lprev * u;
+                lprev = lb[q];
+                zb[q] = u * rb[q];
+              }
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                if (i0 + q < N) z[(size_t)(i0 + q) * kMaxN] = zb[q];
             }
-          double nr = 0.0;
-          for (int i = 0; i < N; ++i) nr += z[i] * z[i];
-          nr = (nr > 0.0) ? 1.0 / sqrt(nr) : 0.0;
-          for (int i = 0; i < N; ++i) z[i] *= nr;
+          }
+          // backward solve L^T y = v, with the norm (8-element load batches)
+          double next = 0.0, nr = 0.0;
+          for (int i1 = N - 1; i1 >= 0; i1 -= 8) {
+            double zb[8], lb[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int i = i1 - q;
+              zb[q] = (i >= 0) ? z[(size_t)i * kMaxN] : 0.0;
+              lb[q] = (i >= 0 && i < N - 1) ? lf[(size_t)i * kMaxN] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              if (i1 - q >= 0) {
+                next = zb[q] - lb[q] * next;
+                zb[q] = next;
+                nr += next * next;
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (i1 - q >= 0) z[(size_t)(i1 - q) * kMaxN] = zb[q];
+          }
+          sc = (nr > 0.0) ? 1.0 / sqrt(nr) : 0.0;
+          if (j > j0) {  // cluster member: normalise, then MGS (twice) against earlier members
+            for (int pass = 0; pass < 2; ++pass)
+              for (int k = j0; k < j; ++k) {
+                if (wgt[k] == T(0)) continue;
+                const double* zk = Zs + k;
+                double h = 0.0;
+#pragma unroll 8
+                for (int i = 0; i < N; ++i) h += zk[(size_t)i * kMaxN] * z[(size_t)i * kMaxN];
+                h *= (pass == 0) ? sc : 1.0;  // z is still unnormalised on the first pass
+                const double zsc = (pass == 0) ? sc : 1.0;
+                for (int i0 = 0; i0 < N; i0 += 8) {
+                  double zb[8], kb[8];
+#pragma unroll
+                  for (int q = 0; q < 8; ++q) {
+                    const int i = i0 + q;
+                    zb[q] = (i < N) ? z[(size_t)i * kMaxN] : 0.0;
+                    kb[q] = (i < N) ? zk[(size_t)i * kMaxN] : 0.0;
+                  }
+#pragma unroll
+                  for (int q = 0; q < 8; ++q)
+                    if (i0 + q < N) z[(size_t)(i0 + q) * kMaxN] = zb[q] * zsc - h * kb[q];
+                }
+                if (pass == 0) sc = 1.0;
+              }
+            double n2 = 0.0;
+#pragma unroll 8
+            for (int i = 0; i < N; ++i) n2 += z[(size_t)i * kMaxN] * z[(size_t)i * kMaxN];
+            sc = (n2 > 0.0) ? 1.0 / sqrt(n2) : 0.0;
+          }
+        }
+        // final normalisation: explicit for cluster members (later members are
+        // orthogonalised against them), folded into the back-transform otherwise
+        if (j1 - j0 > 1) {
+          for (int i0 = 0; i0 < N; i0 += 8) {
+            double zb[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) zb[q] = (i0 + q < N) ? z[(size_t)(i0 + q) * kMaxN] : 0.0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (i0 + q < N) z[(size_t)(i0 + q) * kMaxN] = zb[q] * sc;
+          }
+          pvec[j] = T(1);
+        } else {
+          pvec[j] = (T)sc;
         }
       }
     }
     __syncthreads();
+    if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[5] += t_ - t_ph0; t_ph0 = t_; }
     // ---------------- back-transform U = H_0 ... H_{N-3} Z ; Wt = diag(w) U^T ----------------
-    for (int c0 = 0; c0 < J; c0 += 32) {
+    // warp-owned vectors held in registers (lane <-> rows 32t + lane), 4 per warp per chunk
+    for (int c0 = 0; c0 < J; c0 += 4 * kNW) {
+      T z[4][NT];
+      bool act[4];
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int jj = warp + kNW * q;
-        const int j = c0 + jj;
-        if (j >= J) continue;
-        T* zc = work + jj * NM;
-        const T wj = wgt[j];
-        if (wj == T(0)) {
-          for (int r = lane; r < N; r += 32) Wt[(int64_t)j * p.ldg + r] = T(0);
-          continue;
+      for (int q = 0; q < 4; ++q) {
+        const int j = c0 + warp + kNW * q;
+        act[q] = (j < J) && (wgt[j] != T(0));
+        const double* zg = Zs + (act[q] ? j : 0);
+        const double zs = act[q] ? (double)pvec[j] : 0.0;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int R = 32 * t + lane;
+          z[q][t] = (act[q] && R < N) ? (T)(zg[(size_t)R * kMaxN] * zs) : T(0);
         }
-        const double* zg = Zs + (size_t)j * kMaxN;
-        for (int r = lane; r < N; r += 32) zc[r] = (T)zg[r];
-        __syncwarp();
+      }
+      const bool any = act[0] || act[1] || act[2] || act[3];
+      if (any) {
         for (int i = N - 3; i >= 0; --i) {
           const T ti = tau[i];
           if (ti == T(0)) continue;
-          const int oi = pk_off(i, N);
-          T s = T(0);
-          for (int r = i + 1 + lane; r < N; r += 32) {
-            const T vr = (r == i + 1) ? T(1) : Apk[oi + (r - i)];
-            s = fma(vr, zc[r], s);
+          const int base = pk_off(i, N) - i;
+          T v[NT];
+          T s[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            const int R = 32 * t + lane;
+            v[t] = T(0);
+            if (32 * t + 31 < i + 1) continue;  // warp-uniform
+            v[t] = (R == i + 1) ? T(1) : ((R > i + 1 && R < N) ? Apk[base + R] : T(0));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) s[q] = fma(v[t], z[q][t], s[q]);
           }
-          s = wsum(s) * ti;
-          for (int r = i + 1 + lane; r < N; r += 32) {
-            const T vr = (r == i + 1) ? T(1) : Apk[oi + (r - i)];
-            zc[r] = fma(-s, vr, zc[r]);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) s[q] = wsum(s[q]) * ti;
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            if (32 * t + 31 < i + 1) continue;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) z[q][t] = fma(-s[q], v[t], z[q][t]);
           }
-          __syncwarp();
         }
-        for (int r = lane; r < N; r += 32) Wt[(int64_t)j * p.ldg + r] = wj * zc[r];
-        __syncwarp();
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = c0 + warp + kNW * q;
+        if (j >= J) continue;
+        const T wj = act[q] ? wgt[j] : T(0);
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int R = 32 * t + lane;
+          if (R < N) Wt[(int64_t)j * p.ldg + R] = wj * z[q][t];
+        }
       }
     }
     // rows J..ell-2 of Wt (only when N < ell-1) are zero
     for (int j = J + warp; j < ell - 1; j += kNW)
       for (int r = lane; r < p.ldg; r += 32) Wt[(int64_t)j * p.ldg + r] = T(0);
     __syncthreads();
+    if (p.dbg && blockIdx.x == 0 && tid == 0) {
+      p.dbg[6] += clock64() - t_ph0;
+      int mx = 0;
+      for (int c = 0; c < s_ncl; ++c) mx = max(mx, clen[c]);
+      p.dbg[7] += s_ncl; p.dbg[8] = max((long long)mx, p.dbg[8]); p.dbg[9] = N; p.dbg[10] += 1;
+    }
   }
 }
 

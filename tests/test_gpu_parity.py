@@ -21,6 +21,10 @@ pytestmark = pytest.mark.gpu
 
 SKETCH_TOL = 1e-4
 ERR_TOL = 1e-3
+# absolute floor of the err comparison: B is stored in fp32, so B^T B carries a
+# quantisation error ~2 eps32 ||B||_F^2 <= 2.4e-7 ||A||_F^2 even when the oracle's
+# err is ~1e-12 (exactly representable streams); reading C12.
+ERR_ABS = 1e-6
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -64,7 +68,7 @@ def gpu_sketch(A, ell, variant, alpha=0.2, n_shards=1, appends=None, ld_pad=0):
     return Bn, st, Ad
 
 
-def check_parity(A, ell, variant, alpha=0.2, n_shards=1, appends=None, ld_pad=0, err_tol=ERR_TOL, err_abs=1e-7):
+def check_parity(A, ell, variant, alpha=0.2, n_shards=1, appends=None, ld_pad=0, err_tol=ERR_TOL, err_abs=ERR_ABS):
     Bg, st, Ad = gpu_sketch(A, ell, variant, alpha, n_shards, appends, ld_pad)
     r = oracle.sketch(A, ell, variant, alpha=alpha, n_shards=n_shards, appends=appends)
     frob = r.frob_sq
@@ -135,9 +139,11 @@ def test_parity_c2_perrow_ell40(variant):
     check_parity(_c2(), 40, variant)
 
 
-def test_parity_c5_prefix_perrow():
+def test_parity_c5_scaled_perrow():
+    """Config 5's generator with 1000-row blocks (20 subspaces in 20000 rows, rank
+    ~161 > ell): the drifting-subspace structure at a size the per-row oracle runs fast."""
     w = fdgen.config("c5", n=20000)
-    w.extra["block_rows"] = 10000  # keep c5's 10000-row blocks on the prefix
+    w.extra["block_rows"] = 1000
     A = fdgen.host_rows(w)
     for v in ("fd", "alpha_fd", "isvd"):
         check_parity(A, 32, v)
