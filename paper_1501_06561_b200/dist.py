@@ -30,7 +30,10 @@ def gather_and_merge(B_local, stats_local: dict, merge_fn, group=None):
     if world == 1:
         return B_local, dict(stats_local)
     gathered = torch.empty((world,) + tuple(B_local.shape), dtype=B_local.dtype, device=B_local.device)
-    dist.all_gather_into_tensor(gathered, B_local.contiguous(), group=group)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(gathered, B_local.contiguous(), group=group)
+    else:  # gloo (CPU tests): list form of the same gather
+        dist.all_gather(list(gathered.unbind(0)), B_local.contiguous(), group=group)
     vec = torch.tensor([float(stats_local[k]) for k in STAT_KEYS], dtype=torch.float64, device=B_local.device)
     dist.all_reduce(vec, group=group)
     B, mst = merge_fn(gathered)
@@ -50,13 +53,19 @@ def dist_sketch(sketcher, group=None):
     return gather_and_merge(B_local, st, lambda S: sketcher.merge(S, stats=True), group)
 
 
+def reduce_gram(AtA, group=None):
+    """Sum the per-rank d x d fp64 partial Grams in place (one all_reduce);
+    returns (AtA, ||A||_F^2 = trace(AtA))."""
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(AtA, group=group)
+    return AtA, float(torch.diagonal(AtA).sum().item())
+
+
 def dist_cov_err(A_local, B, group=None):
     """cov-err of B for the row-sharded A (sum of partial Grams by all_reduce)."""
     from . import cov_err_from_gram, cov_gram_partial
     d = B.shape[1]
     AtA = torch.zeros((d, d), dtype=torch.float64, device=B.device)
     cov_gram_partial(A_local, AtA)
-    if dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(AtA, group=group)
-    frob = float(torch.diagonal(AtA).sum().item())
+    AtA, frob = reduce_gram(AtA, group)
     return cov_err_from_gram(AtA, B, frob)
