@@ -250,7 +250,7 @@ struct EigCfg {
   static constexpr int kPart = kNW * NM + 32 * (NM + 1);  // ppart[16][NM] + colpart[32][NM+1]
   static constexpr int kVec = 13;                 // vector arrays of NM
   static constexpr size_t kT = (size_t)kPk + kPart + kVec * NM + 64;  // elements of T
-  static constexpr size_t kBytes = kT * sizeof(T) + 2 * NM * sizeof(int) + 16;
+  static constexpr size_t kBytes = kT * sizeof(T) + 4 * NM * sizeof(int) + NM * sizeof(double) + 16;
 };
 
 __device__ __forceinline__ int pk_off(int c, int N) { return c * N - (c * (c - 1)) / 2; }
@@ -334,7 +334,11 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
   T* red = pvec + 2 * NM;
   int* cstart = reinterpret_cast<int*>(red + 64);
   int* clen = cstart + NM;
-  __shared__ int s_ncl;
+  int* cid = clen + NM;                       // Rayleigh-Ritz cluster list
+  int* ord = cid + NM;                        // Ritz-vector order
+  constexpr size_t kOffD = C::kT * sizeof(T) + 4 * NM * sizeof(int);
+  double* pscl = reinterpret_cast<double*>(smraw + kOffD + 8 - (kOffD & 7));  // per-vector scale (fp64)
+  __shared__ int s_ncl, s_jx, s_nrr;
   __shared__ T s_gl, s_gu, s_a1, s_a2;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -506,6 +510,9 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
     // ---------------- eigenvalues: multisection bisection ----------------
     const int K = min(ell, N);        // top-K eigenvalues needed (lambda_ell = delta)
     const int J = min(ell - 1, N);    // retained eigenvectors
+    // iSVD's weights jump between J-1 (kept) and J (dropped): a cluster straddling
+    // that boundary needs its members beyond J, so a margin of eigenvalues is found
+    const int KC = (p.rule == RULE_ISVD) ? min(N, ell + 16) : K;
     T glo = Lim<T>::big(), ghi = -Lim<T>::big(), emax2 = T(0);
     for (int i = tid; i < N; i += blockDim.x) {
       const T em = (i > 0) ? fabs(ee[i - 1]) : T(0);
@@ -537,7 +544,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
     const T bnorm = red[49];
     if (N > 0) {
       int kp = 1;
-      while (kp < K) kp <<= 1;
+      while (kp < KC) kp <<= 1;
       int g = kEigThreads / kp;  // threads per eigenvalue (power of two)
       if (g > 32) g = 32;
       if (g < 1) g = 1;
@@ -548,7 +555,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
       for (int it = 0; it < niter; ++it) {
         const T step = (hi - lo) / (T)(g + 1);
         const T x = lo + step * (T)(sub + 1);
-        const bool below = (j < K) ? (sturm_count(dd, e2, N, x, pivmin) >= N - j) : false;
+        const bool below = (j < KC) ? (sturm_count(dd, e2, N, x, pivmin) >= N - j) : false;
         const unsigned b = __ballot_sync(0xffffffffu, below) & gmask;
         const int base = (lane / g) * g;
         const int ss = b ? (__ffs(b) - 1 - base) : g;
@@ -557,7 +564,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
         lo = nlo;
         hi = fmax(nhi, nlo);
       }
-      if (sub == 0 && j < K) lam[j] = fmax(T(0.5) * (lo + hi), T(0));  // clamp (reading C8)
+      if (sub == 0 && j < KC) lam[j] = fmax(T(0.5) * (lo + hi), T(0));  // clamp (reading C8)
     }
     __syncthreads();
     if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[3] += t_ - t_ph0; t_ph0 = t_; }
@@ -571,6 +578,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
       spv[tid] = sp2;
       wgt[tid] = (l > T(0)) ? sqrt(sp2 / l) : T(0);
     }
+    for (int j = J + tid; j < KC; j += blockDim.x) wgt[j] = T(0);
     __syncthreads();
     if (tid == 0) {
       double tr = 0.0, sp = 0.0;
@@ -590,51 +598,82 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
         st.shrinks += 1.0;
         *P.stats = st;
       }
-      // clusters of close eigenvalues among 0..J-1 (vectors orthogonalised together)
+      // Clusters of close eigenvalues among 0..KC-1 (consecutive gaps <= ctol).
+      // Members of a cluster are computed together and orthonormalised.  Only the
+      // clusters that contain a retained vector (< J) are kept; JX = end of the
+      // last one.  A cluster is marked for Rayleigh-Ritz when the rule's weight is
+      // discontinuous inside it (alpha-FD boundary ell-m, iSVD boundary J).
       const T ctol = T(1e-5) * bnorm;
-      int ncl = 0;
-      for (int j = 0; j < J; ++j) {
-        if (j == 0 || lam[j - 1] - lam[j] > ctol) { cstart[ncl] = j; clen[ncl] = 0; ++ncl; }
+      const int bnd = (p.rule == RULE_ISVD) ? J : ((p.m < ell) ? ell - p.m : -1);
+      int ncl = 0, jx = 0;
+      for (int j = 0; j < KC; ++j) {
+        const bool cont = (j > 0) && (lam[j - 1] - lam[j] <= ctol);
+        if (!cont) {
+          if (j >= J) break;
+          cstart[ncl] = j; clen[ncl] = 0; ++ncl;
+        }
         clen[ncl - 1]++;
+        jx = j + 1;
       }
-      s_ncl = ncl;
+      int nrr = 0;
+      for (int c = 0; c < ncl; ++c) {
+        const int a = cstart[c], b = cstart[c] + clen[c];
+        if (bnd > a && bnd < b) cid[nrr++] = c;   // Rayleigh-Ritz list
+      }
+      s_ncl = ncl; s_jx = jx; s_nrr = nrr;
     }
     __syncthreads();
     if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[4] += t_ - t_ph0; t_ph0 = t_; }
     // ---------------- eigenvectors of T: fp64 inverse iteration ----------------
+    // One thread per vector j < JX (3 iterations, shift lam[j]); after every
+    // iteration the members of each multi-member cluster are orthonormalised by
+    // one warp (modified Gram-Schmidt, twice), so a member converges inside the
+    // complement of the earlier ones.  Scratch is element-major (z[i * kMaxN + j]):
+    // the per-thread recurrences are coalesced across threads.
     const int ncl = s_ncl;
-    const double tiny = 2.3e-16 * (double)bnorm + 1e-300;
-    for (int cl = tid; cl < ncl; cl += blockDim.x) {
-      double* lf = LF + cl;   // lf[i * kMaxN]  multipliers of L
-      double* rdp = RD + cl;  // rdp[i * kMaxN] reciprocal pivots of D
-      const int j0 = cstart[cl], j1 = cstart[cl] + clen[cl];
-      for (int j = j0; j < j1; ++j) {
-        if (wgt[j] == T(0)) continue;
-        double* z = Zs + j;   // z[i * kMaxN]
-        const double mu = (double)lam[j];
-        // iteration 0: L D L^T = T - mu I (tiny pivots perturbed) fused with the
-        // forward solve L u = b, v = D^-1 u of the start vector b.
-        double dpi = (double)dd[0] - mu;
-        if (fabs(dpi) < tiny) dpi = (dpi < 0.0) ? -tiny : tiny;
-        double rd = 1.0 / dpi;
-        rdp[0] = rd;
-        double u = 1.0 + 0.5 * (double)(((1) * 7919 + (j + 3) * 104729) % 211) / 211.0;
-        z[0] = u * rd;
-        for (int i = 0; i < N - 1; ++i) {
-          const double e = (double)ee[i];
-          const double li = e * rd;
-          lf[(size_t)i * kMaxN] = li;
-          dpi = ((double)dd[i + 1] - mu) - li * e;
-          if (fabs(dpi) < tiny) dpi = (dpi < 0.0) ? -tiny : tiny;
-          rd = 1.0 / dpi;
-          rdp[(size_t)(i + 1) * kMaxN] = rd;
-          const double b = 1.0 + 0.5 * (double)(((i + 2) * 7919 + (j + 3) * 104729) % 211) / 211.0;
-          u = b - li * u;
-          z[(size_t)(i + 1) * kMaxN] = u * rd;
+    const int JX = s_jx;
+    {
+      const double tiny = 2.3e-16 * (double)bnorm + 1e-300;
+      const int j = tid;
+      bool act = false;
+      if (j < JX) {  // singletons with zero weight are not needed
+        act = wgt[j] != T(0);
+        if (!act) {
+          int c = 0;
+          while (c + 1 < ncl && cstart[c + 1] <= j) ++c;
+          act = clen[c] > 1;
         }
-        double sc = 1.0;
-        for (int it = 0; it < 3; ++it) {
-          if (it > 0) {  // forward solve of the (scaled) previous iterate, 8-element load batches
+      }
+      double* lf = LF + j;   // lf[i * kMaxN]  multipliers of L
+      double* rdp = RD + j;  // rdp[i * kMaxN] reciprocal pivots of D
+      double* z = Zs + j;    // z[i * kMaxN]
+      double sc = 1.0;
+      for (int it = 0; it < 3; ++it) {
+        if (act) {
+          double u;
+          if (it == 0) {
+            // L D L^T = T - mu I (tiny pivots perturbed) fused with the forward
+            // solve L u = b, v = D^-1 u of the start vector b.
+            const double mu = (double)lam[j];
+            double dpi = (double)dd[0] - mu;
+            if (fabs(dpi) < tiny) dpi = (dpi < 0.0) ? -tiny : tiny;
+            double rd = 1.0 / dpi;
+            rdp[0] = rd;
+            u = 1.0 + 0.5 * (double)(((1) * 7919 + (j + 3) * 104729) % 211) / 211.0;
+            z[0] = u * rd;
+            for (int i = 0; i < N - 1; ++i) {
+              const double e = (double)ee[i];
+              const double li = e * rd;
+              lf[(size_t)i * kMaxN] = li;
+              dpi = ((double)dd[i + 1] - mu) - li * e;
+              if (fabs(dpi) < tiny) dpi = (dpi < 0.0) ? -tiny : tiny;
+              rd = 1.0 / dpi;
+              rdp[(size_t)(i + 1) * kMaxN] = rd;
+              const double b = 1.0 + 0.5 * (double)(((i + 2) * 7919 + (j + 3) * 104729) % 211) / 211.0;
+              u = b - li * u;
+              z[(size_t)(i + 1) * kMaxN] = u * rd;
+            }
+          } else {  // forward solve of the (scaled) previous iterate, 8-element load batches
             u = 0.0;
             double lprev = 0.0;
             for (int i0 = 0; i0 < N; i0 += 8) {
@@ -680,52 +719,142 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
               if (i1 - q >= 0) z[(size_t)(i1 - q) * kMaxN] = zb[q];
           }
           sc = (nr > 0.0) ? 1.0 / sqrt(nr) : 0.0;
-          if (j > j0) {  // cluster member: normalise, then MGS (twice) against earlier members
+          pscl[j] = sc;
+        }
+        __syncthreads();
+        // multi-member clusters: warp-parallel MGS (normalise, orthogonalise twice, renormalise)
+        for (int c = warp; c < ncl; c += kNW) {
+          const int j0 = cstart[c], j1 = cstart[c] + clen[c];
+          if (j1 - j0 < 2) continue;
+          for (int k = j0; k < j1; ++k) {
+            double* zk = Zs + k;
+            double zr[kMaxN / 32];
+            const double s0 = pscl[k];
+#pragma unroll
+            for (int t = 0; t < kMaxN / 32; ++t) {
+              const int i = 32 * t + lane;
+              zr[t] = (i < N) ? zk[(size_t)i * kMaxN] * s0 : 0.0;
+            }
             for (int pass = 0; pass < 2; ++pass)
-              for (int k = j0; k < j; ++k) {
-                if (wgt[k] == T(0)) continue;
-                const double* zk = Zs + k;
+              for (int q = j0; q < k; ++q) {
+                const double* zq = Zs + q;
+                double zqr[kMaxN / 32];
                 double h = 0.0;
-#pragma unroll 8
-                for (int i = 0; i < N; ++i) h += zk[(size_t)i * kMaxN] * z[(size_t)i * kMaxN];
-                h *= (pass == 0) ? sc : 1.0;  // z is still unnormalised on the first pass
-                const double zsc = (pass == 0) ? sc : 1.0;
-                for (int i0 = 0; i0 < N; i0 += 8) {
-                  double zb[8], kb[8];
 #pragma unroll
-                  for (int q = 0; q < 8; ++q) {
-                    const int i = i0 + q;
-                    zb[q] = (i < N) ? z[(size_t)i * kMaxN] : 0.0;
-                    kb[q] = (i < N) ? zk[(size_t)i * kMaxN] : 0.0;
-                  }
-#pragma unroll
-                  for (int q = 0; q < 8; ++q)
-                    if (i0 + q < N) z[(size_t)(i0 + q) * kMaxN] = zb[q] * zsc - h * kb[q];
+                for (int t = 0; t < kMaxN / 32; ++t) {
+                  const int i = 32 * t + lane;
+                  zqr[t] = (i < N) ? zq[(size_t)i * kMaxN] : 0.0;
+                  h = fma(zqr[t], zr[t], h);
                 }
-                if (pass == 0) sc = 1.0;
+                h = warp_sum_d(h);
+#pragma unroll
+                for (int t = 0; t < kMaxN / 32; ++t) zr[t] = fma(-h, zqr[t], zr[t]);
               }
             double n2 = 0.0;
-#pragma unroll 8
-            for (int i = 0; i < N; ++i) n2 += z[(size_t)i * kMaxN] * z[(size_t)i * kMaxN];
-            sc = (n2 > 0.0) ? 1.0 / sqrt(n2) : 0.0;
+#pragma unroll
+            for (int t = 0; t < kMaxN / 32; ++t) n2 = fma(zr[t], zr[t], n2);
+            n2 = warp_sum_d(n2);
+            const double inv = (n2 > 0.0) ? 1.0 / sqrt(n2) : 0.0;
+#pragma unroll
+            for (int t = 0; t < kMaxN / 32; ++t) {
+              const int i = 32 * t + lane;
+              if (i < N) zk[(size_t)i * kMaxN] = zr[t] * inv;
+            }
+            __syncwarp();
+            if (lane == 0) pscl[k] = 1.0;
           }
         }
-        // final normalisation: explicit for cluster members (later members are
-        // orthogonalised against them), folded into the back-transform otherwise
-        if (j1 - j0 > 1) {
-          for (int i0 = 0; i0 < N; i0 += 8) {
-            double zb[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) zb[q] = (i0 + q < N) ? z[(size_t)(i0 + q) * kMaxN] : 0.0;
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              if (i0 + q < N) z[(size_t)(i0 + q) * kMaxN] = zb[q] * sc;
+        __syncthreads();
+        if (act) sc = pscl[j];
+      }
+      if (act) pvec[j] = (T)sc;   // normalisation folded into the back-transform
+    }
+    // Rayleigh-Ritz inside the (rare) clusters that straddle a rule discontinuity:
+    // H = Z_c^T T Z_c (fp64), cyclic Jacobi on H, Z_c <- Z_c Q (eigenvalues descending).
+    for (int r = 0; r < s_nrr; ++r) {
+      const int c = cid[r];
+      const int j0 = cstart[c], nc = clen[c];
+      if (nc > 181) continue;           // H and Q (nc x nc each) must fit the LF scratch
+      double* H = LF;                   // nc x nc (ld nc)
+      double* Q = LF + (size_t)nc * nc;
+      double* Zc = RD;                  // copy of Z_c (element-major, ld kMaxN)
+      for (int x = tid; x < nc * nc; x += blockDim.x) {
+        const int a = x / nc, b = x % nc;
+        const double* za = Zs + j0 + a;
+        const double* zb = Zs + j0 + b;
+        double h = 0.0;
+        for (int i = 0; i < N; ++i) {
+          double tz = (double)dd[i] * zb[(size_t)i * kMaxN];
+          if (i > 0) tz += (double)ee[i - 1] * zb[(size_t)(i - 1) * kMaxN];
+          if (i < N - 1) tz += (double)ee[i] * zb[(size_t)(i + 1) * kMaxN];
+          h = fma(za[(size_t)i * kMaxN], tz, h);
+        }
+        H[a * nc + b] = h;
+        Q[a * nc + b] = (a == b) ? 1.0 : 0.0;
+      }
+      for (int x = tid; x < N * nc; x += blockDim.x) {
+        const int i = x / nc, a = x % nc;
+        Zc[(size_t)i * nc + a] = Zs[(size_t)i * kMaxN + j0 + a];
+      }
+      __syncthreads();
+      if (warp == 0) {
+        for (int sweep = 0; sweep < 30; ++sweep) {
+          int rot = 0;
+          for (int a = 0; a < nc - 1; ++a)
+            for (int b = a + 1; b < nc; ++b) {
+              const double hab = H[a * nc + b], haa = H[a * nc + a], hbb = H[b * nc + b];
+              if (fabs(hab) <= 1e-15 * sqrt(fabs(haa * hbb)) + 1e-300) continue;
+              ++rot;
+              const double th = (hbb - haa) / (2.0 * hab);
+              const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+              const double cs = 1.0 / sqrt(t * t + 1.0), sn = t * cs;
+              __syncwarp();
+              for (int k = lane; k < nc; k += 32) {
+                if (k == a || k == b) continue;
+                const double hka = H[k * nc + a], hkb = H[k * nc + b];
+                const double na = cs * hka - sn * hkb, nb = sn * hka + cs * hkb;
+                H[k * nc + a] = na; H[a * nc + k] = na;
+                H[k * nc + b] = nb; H[b * nc + k] = nb;
+              }
+              for (int k = lane; k < nc; k += 32) {
+                const double qa = Q[k * nc + a], qb = Q[k * nc + b];
+                Q[k * nc + a] = cs * qa - sn * qb;
+                Q[k * nc + b] = sn * qa + cs * qb;
+              }
+              __syncwarp();
+              if (lane == 0) {
+                H[a * nc + a] = haa - t * hab;
+                H[b * nc + b] = hbb + t * hab;
+                H[a * nc + b] = 0.0;
+                H[b * nc + a] = 0.0;
+              }
+              __syncwarp();
+            }
+          if (rot == 0) break;
+        }
+        // order of the Ritz vectors: descending Ritz value (stable)
+        if (lane == 0) {
+          for (int a = 0; a < nc; ++a) ord[a] = a;
+          for (int a = 1; a < nc; ++a) {
+            const int x = ord[a];
+            int b = a - 1;
+            while (b >= 0 && H[ord[b] * (nc + 1)] < H[x * (nc + 1)]) {
+              ord[b + 1] = ord[b];
+              --b;
+            }
+            ord[b + 1] = x;
           }
-          pvec[j] = T(1);
-        } else {
-          pvec[j] = (T)sc;
         }
       }
+      __syncthreads();
+      for (int x = tid; x < N * nc; x += blockDim.x) {
+        const int i = x / nc, k = x % nc;
+        const int col = ord[k];
+        double s = 0.0;
+        for (int a = 0; a < nc; ++a) s = fma(Zc[(size_t)i * nc + a], Q[a * nc + col], s);
+        Zs[(size_t)i * kMaxN + j0 + k] = s;
+      }
+      __syncthreads();
     }
     __syncthreads();
     if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[5] += t_ - t_ph0; t_ph0 = t_; }
