@@ -118,13 +118,14 @@ class Sketcher:
     def profile(self, enable=True):
         check(lib().fd_profile(self.h, 1 if enable else 0))
 
-    KERNELS = ("ingest", "gram", "eig", "recon")
+    KERNELS = ("ingest", "gram", "eig", "recon", "trd")
 
     def profile_read(self):
         """{kernel: (total_ms, launches)} since the last read (synchronises)."""
-        ms = (ctypes.c_double * 4)()
-        n = (ctypes.c_int64 * 4)()
-        lib().fd_profile_read(self.h, ms, n, 4)
+        k = len(self.KERNELS)
+        ms = (ctypes.c_double * k)()
+        n = (ctypes.c_int64 * k)()
+        lib().fd_profile_read(self.h, ms, n, k)
         return {k: (ms[i], n[i]) for i, k in enumerate(self.KERNELS)}
 
     def close(self):

@@ -137,6 +137,7 @@ struct fd_handle {
   std::vector<int> occ, cur;
   int64_t rows_seen;
   bool dead;
+  bool legacy_trd;    // FD_LEGACY_TRD set: tridiagonalise inside eig_kernel (A/B checks)
   // live profiling: event pairs around launches
   bool prof;
   struct Rec { int kind; cudaEvent_t a, b; };
@@ -172,7 +173,7 @@ fd_status push_desc(fd_handle* h, const std::vector<T>& v, const T** out) {
   return FD_OK;
 }
 
-enum { K_INGEST = 0, K_GRAM = 1, K_EIG = 2, K_RECON = 3, K_COUNT = 4 };
+enum { K_INGEST = 0, K_GRAM = 1, K_EIG = 2, K_RECON = 3, K_TRD = 4, K_COUNT = 5 };
 
 cudaEvent_t get_event(fd_handle* h) {
   if (!h->pool.empty()) {
@@ -207,9 +208,13 @@ fd_status run_reduce(fd_handle* h, const std::vector<Prob>& probs) {
   const int n = (int)probs.size();
   Params prm = h->prm;
   prm.f64 = use_f64(h->D, nmax) ? 1 : 0;
+  prm.pretrd = (!h->legacy_trd && fdk::trd_supported(nmax, prm)) ? 1 : 0;
   cudaError_t e;
   if ((e = timed(h, K_GRAM, [&] { return fdk::launch_gram(dp, n, nmax, prm, h->stream); })) != cudaSuccess)
     return cuda_fail(e, "gram");
+  if (prm.pretrd &&
+      (e = timed(h, K_TRD, [&] { return fdk::launch_trd(dp, n, nmax, prm, h->stream); })) != cudaSuccess)
+    return cuda_fail(e, "trd");
   if ((e = timed(h, K_EIG, [&] { return fdk::launch_eig(dp, n, prm, h->eig, h->stream); })) != cudaSuccess)
     return cuda_fail(e, "eig");
   if ((e = timed(h, K_RECON, [&] { return fdk::launch_recon(dp, n, nmax, prm, h->stream); })) != cudaSuccess)
@@ -346,6 +351,8 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
   h->device = cfg->device;
   h->prm.d = D.d; h->prm.ldb = D.ldb; h->prm.ldg = D.ldg; h->prm.ell = D.ell; h->prm.rule = D.rule; h->prm.m = D.m;
   h->prm.f64 = 0;
+  h->prm.pretrd = 0;
+  h->legacy_trd = getenv("FD_LEGACY_TRD") != nullptr;
   h->prm.dbg = nullptr;
   if (getenv("FD_DEBUG_EIG")) {
     void* dbgp = nullptr;
@@ -520,8 +527,8 @@ fd_status fd_profile(fd_handle* h, int32_t enable) {
 int32_t fd_profile_read(fd_handle* h, double* ms, int64_t* launches, int32_t max_kernels) {
   if (!h) return 0;
   cudaStreamSynchronize(h->stream);
-  double acc[K_COUNT] = {0, 0, 0, 0};
-  int64_t cnt[K_COUNT] = {0, 0, 0, 0};
+  double acc[K_COUNT] = {0, 0, 0, 0, 0};
+  int64_t cnt[K_COUNT] = {0, 0, 0, 0, 0};
   for (auto& r : h->recs) {
     float t = 0.f;
     if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) acc[r.kind] += t;

@@ -54,6 +54,7 @@ struct Params {
   int rule;
   int m;         // alpha-FD: number of trailing values that shrink
   int f64;       // 1: Gram / eigen / reconstruct accumulate in fp64 (per-row chains)
+  int pretrd;    // 1: the Gram scratch already holds the tridiagonal form (trd_kernel)
   long long* dbg;  // optional phase clock trace of problem 0 (FD_DEBUG_EIG), else null
 };
 
@@ -63,6 +64,10 @@ cudaError_t launch_gram(const Prob* dev_probs, int count, int nmax, const Params
 cudaError_t launch_eig(const Prob* dev_probs, int count, const Params& p, double* scratch, cudaStream_t s);
 cudaError_t launch_recon(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s);
 size_t eig_scratch_bytes();   // device scratch the eig kernel needs (all CTA slots)
+// Register-resident Householder tridiagonalisation (fd_trd.cu): overwrites each
+// problem's Gram scratch with the packed reflectors + d / e / tau.
+bool trd_supported(int nmax, const Params& p);
+cudaError_t launch_trd(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s);
 
 // Evaluator.
 cudaError_t launch_syrk_f64(const float* A, int64_t n, int64_t ld, int64_t d, double* AtA, cudaStream_t s);

@@ -355,6 +355,21 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
     long long t_ph0 = clock64();
     const T* G = static_cast<const T*>(P.G);
     T* Wt = static_cast<T*>(P.Wt);
+    if (p.pretrd) {
+      // ---------------- tridiagonal form from trd_kernel (fd_trd.cu) ----------------
+      // packed Householder vectors, then d / e / tau at round_up(N(N+1)/2, 4)
+      const float* V = reinterpret_cast<const float*>(P.G);
+      const int npk = N * (N + 1) / 2;
+      const int offd = (npk + 3) / 4 * 4;
+      for (int k = tid; k < npk; k += blockDim.x) Apk[k] = (T)V[k];
+      for (int r = tid; r < N; r += blockDim.x) {
+        dd[r] = (T)V[offd + r];
+        ee[r] = (T)V[offd + N + r];
+        tau[r] = (T)V[offd + 2 * N + r];
+      }
+      __syncthreads();
+      if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[1] += t_ - t_ph0; t_ph0 = t_; }
+    } else {
     // ---------------- load lower triangle (packed, column-major) ----------------
     for (int c = warp; c < N; c += kNW) {
       const int oc = pk_off(c, N);
@@ -506,6 +521,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
       if (N >= 1) { ee[N - 1] = T(0); tau[N - 1] = T(0); }
     }
     __syncthreads();
+    }  // !p.pretrd
     if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[2] += t_ - t_ph0; t_ph0 = t_; }
     // ---------------- eigenvalues: multisection bisection ----------------
     const int K = min(ell, N);        // top-K eigenvalues needed (lambda_ell = delta)
