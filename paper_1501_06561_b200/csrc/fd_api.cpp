@@ -138,6 +138,7 @@ struct fd_handle {
   int64_t rows_seen;
   bool dead;
   bool legacy_trd;    // FD_LEGACY_TRD set: tridiagonalise inside eig_kernel (A/B checks)
+  bool simt_gemm;     // FD_SIMT_GEMM set: FP32 SIMT Gram / reconstruct instead of tcgen05 (A/B checks)
   // live profiling: event pairs around launches
   bool prof;
   struct Rec { int kind; cudaEvent_t a, b; };
@@ -210,7 +211,10 @@ fd_status run_reduce(fd_handle* h, const std::vector<Prob>& probs) {
   prm.f64 = use_f64(h->D, nmax) ? 1 : 0;
   prm.pretrd = (!h->legacy_trd && fdk::trd_supported(nmax, prm)) ? 1 : 0;
   cudaError_t e;
-  if ((e = timed(h, K_GRAM, [&] { return fdk::launch_gram(dp, n, nmax, prm, h->stream); })) != cudaSuccess)
+  const bool tc_gram = !h->simt_gemm && fdk::gram_tc_supported(nmax, prm);
+  if ((e = timed(h, K_GRAM, [&] {
+         return tc_gram ? fdk::launch_gram_tc(dp, n, nmax, prm, h->stream) : fdk::launch_gram(dp, n, nmax, prm, h->stream);
+       })) != cudaSuccess)
     return cuda_fail(e, "gram");
   if (prm.pretrd &&
       (e = timed(h, K_TRD, [&] { return fdk::launch_trd(dp, n, nmax, prm, h->stream); })) != cudaSuccess)
@@ -353,6 +357,7 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
   h->prm.f64 = 0;
   h->prm.pretrd = 0;
   h->legacy_trd = getenv("FD_LEGACY_TRD") != nullptr;
+  h->simt_gemm = getenv("FD_SIMT_GEMM") != nullptr;
   h->prm.dbg = nullptr;
   if (getenv("FD_DEBUG_EIG")) {
     void* dbgp = nullptr;

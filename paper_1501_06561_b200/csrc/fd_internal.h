@@ -67,6 +67,9 @@ size_t eig_scratch_bytes();   // device scratch the eig kernel needs (all CTA sl
 // Register-resident Householder tridiagonalisation (fd_trd.cu): overwrites each
 // problem's Gram scratch with the packed reflectors + d / e / tau.
 bool trd_supported(int nmax, const Params& p);
+// tcgen05 3xTF32 GEMMs (fd_tc.cu)
+bool gram_tc_supported(int nmax, const Params& p);
+cudaError_t launch_gram_tc(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s);
 cudaError_t launch_trd(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s);
 
 // Evaluator.

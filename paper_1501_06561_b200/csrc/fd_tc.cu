@@ -1,0 +1,191 @@
+// fd_tc.cu — tensor-core (tcgen05, kind::tf32) GEMMs of one ReduceRank with an
+// FP32-accurate 3xTF32 split (x = hi + lo, hi = tf32(x); a.b ~ hi.hi + hi.lo + lo.hi,
+// fp32 accumulation in TMEM).  SURVEY §8(a) rows a2 / a5:
+//   gram:  G = Bf Bf^T                (buffer Gram; "svd(B_[i])", Alg. 1)
+//   recon: B' = Wt Bf, Wt = diag(w) U^T  ("B_[i] <- S'V^T")
+//
+// One CTA per problem (persistent over the launch's problems), 256 threads:
+// all threads stream 32-column K-chunks of the operands from global memory into
+// registers, split them into hi / lo and store them into double-buffered,
+// 128-byte-swizzled shared-memory tiles; one elected thread issues the MMAs and
+// commits them to an mbarrier that releases the buffer; warps 0-3 read the
+// accumulators back with tcgen05.ld for the epilogue.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fd_internal.h"
+#include "fd_tc.cuh"
+
+namespace fdk {
+
+namespace {
+
+constexpr int kTcThreads = 256;
+constexpr int kTile = 256 * 128;   // bytes of one 256-row x 32-value SW128 tile
+
+__device__ __forceinline__ const float* row_ptr(const Prob& P, int r, int64_t ldb) {
+  if (r < P.rows0) return P.src0 + (int64_t)r * ldb;
+  r -= P.rows0;
+  return P.src1 + (int64_t)r * ldb;
+}
+
+// load 32-column K-chunk kc of rows [0, NP) of Bf (zero outside N / ldb) into registers
+template <int NP>
+__device__ __forceinline__ void gram_load(const Prob& P, int N, int64_t ldb, int kc, float4 (&x)[NP * 8 / kTcThreads]) {
+  constexpr int NI = NP * 8 / kTcThreads;
+#pragma unroll
+  for (int j = 0; j < NI; ++j) {
+    const int it = threadIdx.x + kTcThreads * j;
+    const int r = it >> 3, c4 = it & 7;
+    const int64_t col = (int64_t)kc * 32 + 4 * c4;
+    x[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r < N && col < ldb) x[j] = __ldg(reinterpret_cast<const float4*>(row_ptr(P, r, ldb) + col));
+  }
+}
+
+template <int NP>
+__device__ __forceinline__ void gram_store(unsigned char* hi, unsigned char* lo, const float4 (&x)[NP * 8 / kTcThreads]) {
+  constexpr int NI = NP * 8 / kTcThreads;
+#pragma unroll
+  for (int j = 0; j < NI; ++j) {
+    const int it = threadIdx.x + kTcThreads * j;
+    const int r = it >> 3, c4 = it & 7;
+    const uint32_t off = tc::sw128_off(r, 4 * c4);
+    float4 h, l;
+    tc::split_tf32(x[j].x, h.x, l.x);
+    tc::split_tf32(x[j].y, h.y, l.y);
+    tc::split_tf32(x[j].z, h.z, l.z);
+    tc::split_tf32(x[j].w, h.w, l.w);
+    *reinterpret_cast<float4*>(hi + off) = h;
+    *reinterpret_cast<float4*>(lo + off) = l;
+  }
+}
+
+}  // namespace
+
+// G (fp32, ldg) = Bf Bf^T for every problem, N <= NP (NP = 128: one 128x128 tile;
+// NP = 256: tiles rows [0,128) x cols [0,128) and rows [128,256) x cols [0,256)).
+// Written: the lower block triangle (rows >= 128 x all cols, rows < 128 x cols < 128);
+// entries are symmetric up to accumulation order (readers use the lower triangle).
+template <int NP>
+__global__ void __launch_bounds__(kTcThreads, 1) gram_tc_kernel(const Prob* __restrict__ probs, int count, Params p) {
+  extern __shared__ unsigned char smraw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ uint32_t s_tmem;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) tc::tmem_alloc(&s_tmem, 512);
+  if (tid == 0) {
+    tc::mbar_init(&mbar[0], 1);
+    tc::mbar_init(&mbar[1], 1);
+    tc::fence_mbar_init();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = s_tmem;
+  uint32_t uses[2] = {0, 0};   // completed commits per buffer (phase tracking)
+  const uint32_t id0 = tc::idesc_tf32(128, 128, 0, 0);
+  const uint32_t id1 = tc::idesc_tf32(128, 256, 0, 0);
+  constexpr int NI = NP * 8 / kTcThreads;
+
+  for (int pi = blockIdx.x; pi < count; pi += gridDim.x) {
+    const Prob P = probs[pi];
+    const int N = P.rows0 + P.rows1;
+    const int nk = (int)((p.ldb + 31) / 32);
+    float4 x[NI];
+    gram_load<NP>(P, N, p.ldb, 0, x);
+    gram_store<NP>(sm, sm + kTile, x);
+    tc::fence_async_smem();
+    __syncthreads();
+    for (int kc = 0; kc < nk; ++kc) {
+      const int b = kc & 1;
+      if (tid == 0) {
+        tc::fence_after_sync();
+        const uint32_t hi = tc::smem_u32(sm + (2 * b) * kTile), lo = tc::smem_u32(sm + (2 * b + 1) * kTile);
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const uint32_t acc = (kc > 0 || ks > 0) ? 1u : 0u;
+          const uint32_t ko = ks * 32;  // 8 tf32 = 32 bytes along K
+          // tile 0: rows [0,128) x cols [0,128)
+          tc::mma_tf32(tbase, tc::desc_k_sw128(hi + ko), tc::desc_k_sw128(hi + ko), id0, acc);
+          tc::mma_tf32(tbase, tc::desc_k_sw128(hi + ko), tc::desc_k_sw128(lo + ko), id0, 1u);
+          tc::mma_tf32(tbase, tc::desc_k_sw128(lo + ko), tc::desc_k_sw128(hi + ko), id0, 1u);
+          if (NP == 256) {  // tile 1: rows [128,256) x cols [0,256), TMEM columns [128, 384)
+            tc::mma_tf32(tbase + 128, tc::desc_k_sw128(hi + 16384 + ko), tc::desc_k_sw128(hi + ko), id1, acc);
+            tc::mma_tf32(tbase + 128, tc::desc_k_sw128(hi + 16384 + ko), tc::desc_k_sw128(lo + ko), id1, 1u);
+            tc::mma_tf32(tbase + 128, tc::desc_k_sw128(lo + 16384 + ko), tc::desc_k_sw128(hi + ko), id1, 1u);
+          }
+        }
+        tc::commit(&mbar[b]);
+      }
+      if (kc + 1 < nk) {
+        gram_load<NP>(P, N, p.ldb, kc + 1, x);
+        const int nb = b ^ 1;
+        if (kc >= 1) {  // buffer nb was read by the MMAs of chunk kc-1
+          tc::mbar_wait(&mbar[nb], uses[nb] & 1);
+          ++uses[nb];
+        }
+        gram_store<NP>(sm + (2 * nb) * kTile, sm + (2 * nb + 1) * kTile, x);
+        tc::fence_async_smem();
+      }
+      __syncthreads();
+    }
+    // all MMAs of this problem: the last commit (and, if nk > 1, the one before it)
+    {
+      const int bl = (nk - 1) & 1;
+      if (nk >= 2) { tc::mbar_wait(&mbar[bl ^ 1], uses[bl ^ 1] & 1); ++uses[bl ^ 1]; }
+      tc::mbar_wait(&mbar[bl], uses[bl] & 1);
+      ++uses[bl];
+    }
+    tc::fence_after_sync();
+    // epilogue: warps 0-3 hold TMEM lanes 0-127 (= tile rows)
+    if (warp < 4) {
+      float* G = static_cast<float*>(P.G);
+      const int m = 32 * warp + lane;
+      const uint32_t lanebase = tbase + ((uint32_t)(32 * warp) << 16);
+#pragma unroll 1
+      for (int t = 0; t < (NP == 256 ? 2 : 1); ++t) {
+        const int row = 128 * t + m;
+        const int ncols = (t == 0) ? 128 : 256;
+        for (int c0 = 0; c0 < ncols; c0 += 16) {
+          float v[16];
+          tc::tmem_ld16(lanebase + (t == 0 ? 0 : 128) + c0, v);
+          if (row < N) {
+            float* dst = G + (int64_t)row * p.ldg + c0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (c0 + 4 * q + 4 <= p.ldg) *reinterpret_cast<float4*>(dst + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          }
+        }
+      }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+  }
+  if (warp == 0) tc::tmem_dealloc(tbase, 512);
+}
+
+template <int NP>
+static cudaError_t launch_gram_tc_t(const Prob* dev_probs, int count, const Params& p, cudaStream_t s) {
+  constexpr int dyn = 4 * kTile + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gram_tc_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int grid = count < kNumSMs ? count : kNumSMs;
+  gram_tc_kernel<NP><<<grid, kTcThreads, dyn, s>>>(dev_probs, count, p);
+  return cudaGetLastError();
+}
+
+bool gram_tc_supported(int nmax, const Params& p) { return !p.f64 && nmax >= 1 && nmax <= 256 && (p.ldg % 4) == 0; }
+
+cudaError_t launch_gram_tc(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  if (nmax <= 128) return launch_gram_tc_t<128>(dev_probs, count, p, s);
+  return launch_gram_tc_t<256>(dev_probs, count, p, s);
+}
+
+}  // namespace fdk

@@ -198,6 +198,16 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
     if (tid < NB) s_apart[tid] = 0.f;
     if (tid == 0) s_tprev = 0.f;
     __syncthreads();  // G fully read before V overwrites it
+    // diagonal tiles: mirror the lower triangle (the tensor-core Gram is symmetric
+    // only up to accumulation order; the symmetric update needs exact symmetry)
+    for (int q = 0; q < nd; ++q) {
+      const int D = dT[q];
+      for (int e = lane; e < 32 * 32; e += 32) {
+        const int r = e >> 5, c = e & 31;
+        if (r < c) s_dg[D][r][c] = s_dg[D][c][r];
+      }
+    }
+    __syncthreads();
     float* Vout = G;
     const int offd = (N * (N + 1) / 2 + 3) / 4 * 4;
 
