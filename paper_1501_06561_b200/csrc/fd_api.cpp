@@ -104,6 +104,7 @@ Layout layout(const Derived& D) {
   Lo.nodes = take((size_t)Lo.nnodes * D.ell * D.ldb * sizeof(float));
   Lo.G = take((size_t)Lo.nslots * D.ldg * D.ldg * D.gbytes);
   Lo.Wt = take((size_t)Lo.nslots * D.ell * D.ldg * D.gbytes);
+
   Lo.stats = take((size_t)(D.P + Lo.nnodes) * sizeof(Stats));
   Lo.flag = take(sizeof(int) * 4);
   Lo.eig = take(fdk::eig_scratch_bytes());
@@ -139,6 +140,7 @@ struct fd_handle {
   bool dead;
   bool legacy_trd;    // FD_LEGACY_TRD set: tridiagonalise inside eig_kernel (A/B checks)
   bool simt_gemm;     // FD_SIMT_GEMM set: FP32 SIMT Gram / reconstruct instead of tcgen05 (A/B checks)
+  bool simt_gram, simt_recon;  // per-GEMM variants (FD_SIMT_GRAM; FD_TC_RECON opts into the TC reconstruct)
   // live profiling: event pairs around launches
   bool prof;
   struct Rec { int kind; cudaEvent_t a, b; };
@@ -211,7 +213,7 @@ fd_status run_reduce(fd_handle* h, const std::vector<Prob>& probs) {
   prm.f64 = use_f64(h->D, nmax) ? 1 : 0;
   prm.pretrd = (!h->legacy_trd && fdk::trd_supported(nmax, prm)) ? 1 : 0;
   cudaError_t e;
-  const bool tc_gram = !h->simt_gemm && fdk::gram_tc_supported(nmax, prm);
+  const bool tc_gram = !h->simt_gram && fdk::gram_tc_supported(nmax, prm);
   if ((e = timed(h, K_GRAM, [&] {
          return tc_gram ? fdk::launch_gram_tc(dp, n, nmax, prm, h->stream) : fdk::launch_gram(dp, n, nmax, prm, h->stream);
        })) != cudaSuccess)
@@ -221,7 +223,10 @@ fd_status run_reduce(fd_handle* h, const std::vector<Prob>& probs) {
     return cuda_fail(e, "trd");
   if ((e = timed(h, K_EIG, [&] { return fdk::launch_eig(dp, n, prm, h->eig, h->stream); })) != cudaSuccess)
     return cuda_fail(e, "eig");
-  if ((e = timed(h, K_RECON, [&] { return fdk::launch_recon(dp, n, nmax, prm, h->stream); })) != cudaSuccess)
+  const bool tc_recon = !h->simt_recon && fdk::recon_tc_supported(nmax, prm);
+  if ((e = timed(h, K_RECON, [&] {
+         return tc_recon ? fdk::launch_recon_tc(dp, n, nmax, prm, h->stream) : fdk::launch_recon(dp, n, nmax, prm, h->stream);
+       })) != cudaSuccess)
     return cuda_fail(e, "recon");
   return FD_OK;
 }
@@ -234,6 +239,7 @@ Prob make_prob(fd_handle* h, int slot, const float* s0, int r0, const float* s1,
   p.dst = dst;
   p.G = h->G + (size_t)slot * h->D.ldg * h->D.ldg * h->D.gbytes;
   p.Wt = h->Wt + (size_t)slot * h->D.ell * h->D.ldg * h->D.gbytes;
+
   p.stats = st;
   p.child0 = c0; p.child1 = c1;
   return p;
@@ -358,6 +364,9 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
   h->prm.pretrd = 0;
   h->legacy_trd = getenv("FD_LEGACY_TRD") != nullptr;
   h->simt_gemm = getenv("FD_SIMT_GEMM") != nullptr;
+  h->simt_gram = h->simt_gemm || getenv("FD_SIMT_GRAM") != nullptr;
+  // the tensor-core reconstruct is opt-in (accumulation bias, fd_tc.cu)
+  h->simt_recon = h->simt_gemm || getenv("FD_TC_RECON") == nullptr;
   h->prm.dbg = nullptr;
   if (getenv("FD_DEBUG_EIG")) {
     void* dbgp = nullptr;
@@ -371,6 +380,7 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
   h->nodes = reinterpret_cast<float*>(h->ws + Lo.nodes);
   h->G = h->ws + Lo.G;
   h->Wt = h->ws + Lo.Wt;
+
   h->stats = reinterpret_cast<Stats*>(h->ws + Lo.stats);
   h->flag = reinterpret_cast<int*>(h->ws + Lo.flag);
   h->eig = reinterpret_cast<double*>(h->ws + Lo.eig);

@@ -70,6 +70,8 @@ bool trd_supported(int nmax, const Params& p);
 // tcgen05 3xTF32 GEMMs (fd_tc.cu)
 bool gram_tc_supported(int nmax, const Params& p);
 cudaError_t launch_gram_tc(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s);
+bool recon_tc_supported(int nmax, const Params& p);
+cudaError_t launch_recon_tc(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s);
 cudaError_t launch_trd(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s);
 
 // Evaluator.

@@ -180,6 +180,211 @@ static cudaError_t launch_gram_tc_t(const Prob* dev_probs, int count, const Para
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// EXPERIMENTAL (opt-in, FD_TC_RECON=1): the tensor core's fp32 accumulation
+// truncates, which shrinks the reconstructed rows by ~1e-6 per ReduceRank; fed
+// back through the retained rows this compounds (cov-err bias ~2e-3 relative on
+// c2 after ~100 rounds), so the default reconstruct is FP32 SIMT.
+// Reconstruct B' = Wt Bf (rows 0..ell-2; row ell-1 = 0), Wt: (ell-1) x N (ldg),
+// Bf: N x d rows of the problem (ldb).  M = 128 (ell-1 <= 127), N-tiles of 256
+// columns of d, K = N in 32-row chunks.  Both operands K-major SW128: A = Wt rows;
+// B = Bf^T, transposed while staging (each thread loads an 8 (k) x 4 (n) block of
+// Bf with four coalesced 16-B loads per k-row and stores, per column n, the 8
+// k-values as two 16-B chunks).
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int kRA = 128 * 128;      // A tile bytes (128 rows x 32 values)
+constexpr int kRB = 256 * 128;      // B tile bytes (256 rows (n) x 32 values (k))
+constexpr int kRStage = 2 * kRA + 2 * kRB;
+
+struct ReconRegs {
+  float4 a[4];   // A: 128 rows x 8 float4 = 1024 items / 256 threads
+  float4 b[8];   // B: k-rows 8g..8g+7 of columns n0 + 4q .. +3 (q = tid & 63, g = tid >> 6)
+};
+
+__device__ __forceinline__ void recon_load(const Prob& P, const Params& p, int N, int jrows, int kc, int n0,
+                                           ReconRegs& R) {
+  const float* Wt = static_cast<const float*>(P.Wt);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int it = threadIdx.x + kTcThreads * j;
+    const int r = it >> 3, c4 = it & 7;
+    const int k = kc * 32 + 4 * c4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r < jrows && k < N) {
+      v = *reinterpret_cast<const float4*>(Wt + (int64_t)r * p.ldg + k);
+      if (k + 1 >= N) v.y = 0.f;
+      if (k + 2 >= N) v.z = 0.f;
+      if (k + 3 >= N) v.w = 0.f;
+    }
+    R.a[j] = v;
+  }
+  const int q = threadIdx.x & 63, g = threadIdx.x >> 6;
+  const int64_t n = n0 + 4 * q;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const int k = kc * 32 + 8 * g + kk;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (k < N && n < p.ldb) v = __ldg(reinterpret_cast<const float4*>(row_ptr(P, k, p.ldb) + n));
+    R.b[kk] = v;
+  }
+}
+
+__device__ __forceinline__ void st_split(unsigned char* hi, unsigned char* lo, uint32_t off, float4 x) {
+  float4 h, l;
+  tc::split_tf32(x.x, h.x, l.x);
+  tc::split_tf32(x.y, h.y, l.y);
+  tc::split_tf32(x.z, h.z, l.z);
+  tc::split_tf32(x.w, h.w, l.w);
+  *reinterpret_cast<float4*>(hi + off) = h;
+  *reinterpret_cast<float4*>(lo + off) = l;
+}
+
+__device__ __forceinline__ float comp(const float4& v, int e) {
+  return e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w));
+}
+
+__device__ __forceinline__ void recon_store(unsigned char* st, const ReconRegs& R) {
+  unsigned char* ahi = st;
+  unsigned char* alo = st + kRA;
+  unsigned char* bhi = st + 2 * kRA;
+  unsigned char* blo = st + 2 * kRA + kRB;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int it = threadIdx.x + kTcThreads * j;
+    const int r = it >> 3, c4 = it & 7;
+    st_split(ahi, alo, tc::sw128_off(r, 4 * c4), R.a[j]);
+  }
+  const int q = threadIdx.x & 63, g = threadIdx.x >> 6;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int n = 4 * q + e;
+    const float4 v0 = make_float4(comp(R.b[0], e), comp(R.b[1], e), comp(R.b[2], e), comp(R.b[3], e));
+    const float4 v1 = make_float4(comp(R.b[4], e), comp(R.b[5], e), comp(R.b[6], e), comp(R.b[7], e));
+    st_split(bhi, blo, tc::sw128_off(n, 8 * g), v0);
+    st_split(bhi, blo, tc::sw128_off(n, 8 * g + 4), v1);
+  }
+}
+}  // namespace
+
+__global__ void __launch_bounds__(kTcThreads, 1) recon_tc_kernel(const Prob* __restrict__ probs, int count, Params p) {
+  extern __shared__ unsigned char smraw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ uint32_t s_tmem;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) tc::tmem_alloc(&s_tmem, 512);
+  if (tid == 0) {
+    tc::mbar_init(&mbar[0], 1);
+    tc::mbar_init(&mbar[1], 1);
+    tc::fence_mbar_init();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = s_tmem;
+  uint32_t uses[2] = {0, 0};
+  const uint32_t idesc = tc::idesc_tf32(128, 256, 0, 0);
+  const int ell = p.ell, jrows = ell - 1;
+
+  for (int pi = blockIdx.x; pi < count; pi += gridDim.x) {
+    const Prob P = probs[pi];
+    const int N = P.rows0 + P.rows1;
+    const int nk = (N + 31) / 32;
+    for (int n0 = 0; n0 < p.ldb; n0 += 256) {
+      ReconRegs R;
+      recon_load(P, p, N, jrows, 0, n0, R);
+      recon_store(sm, R);
+      tc::fence_async_smem();
+      __syncthreads();
+      for (int kc = 0; kc < nk; ++kc) {
+        const int b = kc & 1;
+        if (tid == 0) {
+          tc::fence_after_sync();
+          unsigned char* st = sm + b * kRStage;
+          const uint32_t ahi = tc::smem_u32(st), alo = tc::smem_u32(st + kRA);
+          const uint32_t bhi = tc::smem_u32(st + 2 * kRA), blo = tc::smem_u32(st + 2 * kRA + kRB);
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            const uint32_t acc = (kc > 0 || ks > 0) ? 1u : 0u;
+            const uint32_t ka = ks * 32;
+            // hi.hi and the small cross terms go to separate accumulators: the tensor
+            // core's fp32 accumulation truncates, so fewer steps on the large one
+            // means less bias (summed with round-to-nearest in the epilogue)
+            tc::mma_tf32(tbase, tc::desc_k_sw128(ahi + ka), tc::desc_k_sw128(bhi + ka), idesc, acc);
+            tc::mma_tf32(tbase + 256, tc::desc_k_sw128(ahi + ka), tc::desc_k_sw128(blo + ka), idesc, acc);
+            tc::mma_tf32(tbase + 256, tc::desc_k_sw128(alo + ka), tc::desc_k_sw128(bhi + ka), idesc, 1u);
+          }
+          tc::commit(&mbar[b]);
+        }
+        if (kc + 1 < nk) {
+          recon_load(P, p, N, jrows, kc + 1, n0, R);
+          const int nb = b ^ 1;
+          if (kc >= 1) {
+            tc::mbar_wait(&mbar[nb], uses[nb] & 1);
+            ++uses[nb];
+          }
+          recon_store(sm + nb * kRStage, R);
+          tc::fence_async_smem();
+        }
+        __syncthreads();
+      }
+      {
+        const int bl = (nk - 1) & 1;
+        if (nk >= 2) { tc::mbar_wait(&mbar[bl ^ 1], uses[bl ^ 1] & 1); ++uses[bl ^ 1]; }
+        tc::mbar_wait(&mbar[bl], uses[bl] & 1);
+        ++uses[bl];
+      }
+      tc::fence_after_sync();
+      if (warp < 4) {
+        const int m = 32 * warp + lane;
+        const uint32_t lanebase = tbase + ((uint32_t)(32 * warp) << 16);
+        for (int c0 = 0; c0 < 256; c0 += 16) {
+          float v[16], vs[16];
+          tc::tmem_ld16(lanebase + c0, v);
+          tc::tmem_ld16(lanebase + 256 + c0, vs);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) v[q] += vs[q];
+          if (m < ell) {
+            float* dst = P.dst + (int64_t)m * p.ldb + n0 + c0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (n0 + c0 + 4 * q + 4 <= p.ldb) {
+                const float4 o = (m < jrows) ? make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3])
+                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+                *reinterpret_cast<float4*>(dst + 4 * q) = o;
+              }
+            }
+          }
+        }
+      }
+      tc::fence_before_sync();
+      __syncthreads();
+    }
+    __syncthreads();
+  }
+  if (warp == 0) tc::tmem_dealloc(tbase, 512);
+}
+
+bool recon_tc_supported(int nmax, const Params& p) {
+  return !p.f64 && p.ell - 1 <= 128 && nmax >= 1 && nmax <= 1024 && (p.ldg % 4) == 0;
+}
+
+cudaError_t launch_recon_tc(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s) {
+  (void)nmax;
+  if (count <= 0) return cudaSuccess;
+  constexpr int dyn = 2 * kRStage + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(recon_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int grid = count < kNumSMs ? count : kNumSMs;
+  recon_tc_kernel<<<grid, kTcThreads, dyn, s>>>(dev_probs, count, p);
+  return cudaGetLastError();
+}
+
 bool gram_tc_supported(int nmax, const Params& p) { return !p.f64 && nmax >= 1 && nmax <= 256 && (p.ldg % 4) == 0; }
 
 cudaError_t launch_gram_tc(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s) {
