@@ -142,8 +142,8 @@ fd_status fd_reset(fd_handle* h);
 /* Live per-kernel timing (for the bench's roofline).  enable != 0 records a
  * CUDA event pair (on the handle's stream) around every kernel launch.
  * fd_profile_read synchronises, writes per-kernel totals
- * {ingest, gram, eig, recon, trd} (ms[k], launches[k], k < max_kernels) since
- * the last read, and returns the number of kernel kinds (5). */
+ * {ingest, gram, eig, recon, trd, bt} (ms[k], launches[k], k < max_kernels)
+ * since the last read, and returns the number of kernel kinds (6). */
 fd_status fd_profile(fd_handle* h, int32_t enable);
 int32_t fd_profile_read(fd_handle* h, double* ms, int64_t* launches, int32_t max_kernels);
 

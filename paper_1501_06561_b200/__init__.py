@@ -118,7 +118,7 @@ class Sketcher:
     def profile(self, enable=True):
         check(lib().fd_profile(self.h, 1 if enable else 0))
 
-    KERNELS = ("ingest", "gram", "eig", "recon", "trd")
+    KERNELS = ("ingest", "gram", "eig", "recon", "trd", "bt")
 
     def profile_read(self):
         """{kernel: (total_ms, launches)} since the last read (synchronises)."""

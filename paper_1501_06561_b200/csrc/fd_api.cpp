@@ -92,6 +92,10 @@ bool derive(const fd_config* c, Derived* D, std::string* why) {
   return true;
 }
 
+// rows of a Wt slot: ell-1 weight rows (+1), or the N x 128 eigenvector block
+// eig_kernel hands to bt_kernel (fd_bt.cu) in the tridiagonal-kernel path
+size_t wt_rows(const Derived& D) { return (size_t)std::max(D.ell, 128); }
+
 Layout layout(const Derived& D) {
   Layout Lo;
   size_t off = 0;
@@ -103,7 +107,7 @@ Layout layout(const Derived& D) {
   Lo.buf1 = take(bufb);
   Lo.nodes = take((size_t)Lo.nnodes * D.ell * D.ldb * sizeof(float));
   Lo.G = take((size_t)Lo.nslots * D.ldg * D.ldg * D.gbytes);
-  Lo.Wt = take((size_t)Lo.nslots * D.ell * D.ldg * D.gbytes);
+  Lo.Wt = take((size_t)Lo.nslots * wt_rows(D) * D.ldg * D.gbytes);
 
   Lo.stats = take((size_t)(D.P + Lo.nnodes) * sizeof(Stats));
   Lo.flag = take(sizeof(int) * 4);
@@ -176,7 +180,7 @@ fd_status push_desc(fd_handle* h, const std::vector<T>& v, const T** out) {
   return FD_OK;
 }
 
-enum { K_INGEST = 0, K_GRAM = 1, K_EIG = 2, K_RECON = 3, K_TRD = 4, K_COUNT = 5 };
+enum { K_INGEST = 0, K_GRAM = 1, K_EIG = 2, K_RECON = 3, K_TRD = 4, K_BT = 5, K_COUNT = 6 };
 
 cudaEvent_t get_event(fd_handle* h) {
   if (!h->pool.empty()) {
@@ -223,6 +227,8 @@ fd_status run_reduce(fd_handle* h, const std::vector<Prob>& probs) {
     return cuda_fail(e, "trd");
   if ((e = timed(h, K_EIG, [&] { return fdk::launch_eig(dp, n, prm, h->eig, h->stream); })) != cudaSuccess)
     return cuda_fail(e, "eig");
+  if (prm.pretrd && (e = timed(h, K_BT, [&] { return fdk::launch_bt(dp, n, prm, h->stream); })) != cudaSuccess)
+    return cuda_fail(e, "bt");
   const bool tc_recon = !h->simt_recon && fdk::recon_tc_supported(nmax, prm);
   if ((e = timed(h, K_RECON, [&] {
          return tc_recon ? fdk::launch_recon_tc(dp, n, nmax, prm, h->stream) : fdk::launch_recon(dp, n, nmax, prm, h->stream);
@@ -238,7 +244,7 @@ Prob make_prob(fd_handle* h, int slot, const float* s0, int r0, const float* s1,
   p.src1 = s1; p.rows1 = r1;
   p.dst = dst;
   p.G = h->G + (size_t)slot * h->D.ldg * h->D.ldg * h->D.gbytes;
-  p.Wt = h->Wt + (size_t)slot * h->D.ell * h->D.ldg * h->D.gbytes;
+  p.Wt = h->Wt + (size_t)slot * wt_rows(h->D) * h->D.ldg * h->D.gbytes;
 
   p.stats = st;
   p.child0 = c0; p.child1 = c1;
@@ -542,8 +548,8 @@ fd_status fd_profile(fd_handle* h, int32_t enable) {
 int32_t fd_profile_read(fd_handle* h, double* ms, int64_t* launches, int32_t max_kernels) {
   if (!h) return 0;
   cudaStreamSynchronize(h->stream);
-  double acc[K_COUNT] = {0, 0, 0, 0, 0};
-  int64_t cnt[K_COUNT] = {0, 0, 0, 0, 0};
+  double acc[K_COUNT] = {};
+  int64_t cnt[K_COUNT] = {};
   for (auto& r : h->recs) {
     float t = 0.f;
     if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) acc[r.kind] += t;

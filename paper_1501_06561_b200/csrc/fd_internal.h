@@ -73,6 +73,8 @@ cudaError_t launch_gram_tc(const Prob* dev_probs, int count, int nmax, const Par
 bool recon_tc_supported(int nmax, const Params& p);
 cudaError_t launch_recon_tc(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s);
 cudaError_t launch_trd(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s);
+// Blocked (compact WY) back-transform + Wt = diag(w) U^T (fd_bt.cu), after eig when p.pretrd.
+cudaError_t launch_bt(const Prob* dev_probs, int count, const Params& p, cudaStream_t s);
 
 // Evaluator.
 cudaError_t launch_syrk_f64(const float* A, int64_t n, int64_t ld, int64_t d, double* AtA, cudaStream_t s);

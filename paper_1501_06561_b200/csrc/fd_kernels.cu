@@ -361,7 +361,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
       const float* V = reinterpret_cast<const float*>(P.G);
       const int npk = N * (N + 1) / 2;
       const int offd = (npk + 3) / 4 * 4;
-      for (int k = tid; k < npk; k += blockDim.x) Apk[k] = (T)V[k];
+      (void)npk;  // the reflectors stay in global memory for bt_kernel (fd_bt.cu)
       for (int r = tid; r < N; r += blockDim.x) {
         dd[r] = (T)V[offd + r];
         ee[r] = (T)V[offd + N + r];
@@ -874,6 +874,20 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
     }
     __syncthreads();
     if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[5] += t_ - t_ph0; t_ph0 = t_; }
+    if (p.pretrd) {
+      // ---------------- hand Z to bt_kernel (fd_bt.cu) ----------------
+      // Wt scratch <- Z row-major [r][j] (ld 128; normalised, fp32; 0 for unused j);
+      // w_j after the tridiagonal data in the Gram scratch
+      for (int x = tid; x < N * 128; x += blockDim.x) {
+        const int r = x >> 7, j = x & 127;
+        const bool a = (j < J) && (wgt[j] != T(0));
+        Wt[x] = a ? (T)(Zs[(size_t)r * kMaxN + j] * (double)pvec[j]) : T(0);
+      }
+      {
+        float* wout = reinterpret_cast<float*>(P.G) + (N * (N + 1) / 2 + 3) / 4 * 4 + 3 * N;
+        for (int j = tid; j < J; j += blockDim.x) wout[j] = (float)wgt[j];
+      }
+    } else
     // ---------------- back-transform U = H_0 ... H_{N-3} Z ; Wt = diag(w) U^T ----------------
     // warp-owned vectors held in registers (lane <-> rows 32t + lane), 4 per warp per chunk
     for (int c0 = 0; c0 < J; c0 += 4 * kNW) {
