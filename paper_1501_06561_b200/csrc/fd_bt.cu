@@ -25,9 +25,10 @@ namespace fdk {
 
 namespace {
 
-constexpr int kBtThreads = 256;
+constexpr int kBtThreads = 512;    // two groups of 8 warps split the row range of each product
 constexpr int kNbBt = 32;          // reflectors per block
 constexpr int kZld = 132;          // Z row stride (floats): J <= 128, padded
+constexpr int kVld = kMaxN + 1;    // V_b column stride (column-major, odd: conflict-free)
 
 __device__ __forceinline__ int pk_off_b(int c, int N) { return c * N - (c * (c - 1)) / 2; }
 
@@ -36,13 +37,14 @@ __device__ __forceinline__ int pk_off_b(int c, int N) { return c * N - (c * (c -
 __global__ void __launch_bounds__(kBtThreads, 1) bt_kernel(const Prob* __restrict__ probs, int count, Params p) {
   extern __shared__ __align__(16) float sm[];
   float* Zs = sm;                                  // [kMaxN][kZld]
-  float* Vb = Zs + kMaxN * kZld;                   // [kMaxN][32]   Vb[r][c] = v_{i0+c}[r]
-  float* W1 = Vb + kMaxN * kNbBt;                  // [32][128]
-  float* W2 = W1 + kNbBt * 128;                    // [32][128]
+  float* Vb = Zs + kMaxN * kZld;                   // [32][kVld]   Vb[c][r] = v_{i0+c}[r]
+  float* W1 = Vb + kNbBt * kVld;                   // [32][128]
+  float* W2 = W1 + kNbBt * 128;                    // [32][128]  (also group 1's partial W1)
   float* S = W2 + kNbBt * 128;                     // [32][33]  V^T V
   float* Tm = S + kNbBt * 33;                      // [32][33]  T
   float* tau = Tm + kNbBt * 33;                    // [32]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = warp >> 3, wg8 = warp & 7;       // row-range group, warp within group
   const int ell = p.ell;
 
   for (int pi = blockIdx.x; pi < count; pi += gridDim.x) {
@@ -69,25 +71,31 @@ __global__ void __launch_bounds__(kBtThreads, 1) bt_kernel(const Prob* __restric
       for (int x = tid; x < kNbBt * (N - r0); x += kBtThreads) {
         const int c = x / (N - r0), r = r0 + (x - c * (N - r0));
         float v = 0.f;
-        if (c < nb) {
+        if (c < nb && taug[i0 + c] != 0.f) {   // tau = 0: identity reflector -> zero column
           const int i = i0 + c;
           v = (r == i + 1) ? 1.f : ((r > i + 1) ? V[pk_off_b(i, N) + r - i] : 0.f);
         }
-        Vb[r * kNbBt + c] = v;
+        Vb[c * kVld + r] = v;
       }
-      if (tid < kNbBt) tau[tid] = (tid < nb) ? taug[i0 + tid] : 0.f;
+      if (tid < kNbBt) {
+        const float t = (tid < nb) ? taug[i0 + tid] : 0.f;
+        tau[tid] = (t != 0.f) ? t : 1.f;   // zero columns of V_b: any nonzero tau (no effect)
+      }
       __syncthreads();
-      // ---- W1 = V_b^T Z and S = V_b^T V_b (one pass over the rows) ----
+      // ---- W1 = V_b^T Z and S = V_b^T V_b (one pass over the rows; group g takes
+      //      rows r0 + g, r0 + g + 2, ...; group 1's partials go to W2 / Tm) ----
       {
-        // thread: 4 reflectors (c-block = warp) x {4 columns of Z (lane), 1 column of V_b (lane)}
-        const int cb = 4 * warp, jb = 4 * lane;
+        const int cb = 4 * wg8, jb = 4 * lane;
         float acc[4][4] = {};
         float sacc[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int r = r0; r < N; ++r) {
-          const float4 vv = *reinterpret_cast<const float4*>(&Vb[r * kNbBt + cb]);
+#pragma unroll 2
+        for (int r = r0 + grp; r < N; r += 2) {
           const float4 zz = *reinterpret_cast<const float4*>(&Zs[r * kZld + jb]);
-          const float vl = Vb[r * kNbBt + lane];
-          const float va[4] = {vv.x, vv.y, vv.z, vv.w}, za[4] = {zz.x, zz.y, zz.z, zz.w};
+          const float vl = Vb[lane * kVld + r];
+          float va[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) va[a] = Vb[(cb + a) * kVld + r];
+          const float za[4] = {zz.x, zz.y, zz.z, zz.w};
 #pragma unroll
           for (int a = 0; a < 4; ++a) {
 #pragma unroll
@@ -95,34 +103,54 @@ __global__ void __launch_bounds__(kBtThreads, 1) bt_kernel(const Prob* __restric
             sacc[a] = fmaf(va[a], vl, sacc[a]);
           }
         }
+        float* Wd = grp ? W2 : W1;
+        float* Sd = grp ? Tm : S;
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
-          *reinterpret_cast<float4*>(&W1[(cb + a) * 128 + jb]) = make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
-          S[(cb + a) * 33 + lane] = sacc[a];
+          *reinterpret_cast<float4*>(&Wd[(cb + a) * 128 + jb]) = make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
+          Sd[(cb + a) * 33 + lane] = sacc[a];
         }
       }
       __syncthreads();
-      // ---- T (xLARFT forward, columnwise): T[c][c] = tau_c,
-      //      T[0:c, c] = -tau_c T[0:c, 0:c] S[0:c, c]  (lane = row of T) ----
-      if (warp == 0) {
-        for (int c = 0; c < kNbBt; ++c) {
+      for (int x = tid; x < kNbBt * 128; x += kBtThreads) W1[x] += W2[x];
+      for (int x = tid; x < kNbBt * 32; x += kBtThreads) {
+        const int a = x >> 5, c = x & 31;
+        S[a * 33 + c] += Tm[a * 33 + c];
+      }
+      __syncthreads();
+      // ---- T = U^-1, U = diag(1/tau) + strict_upper(V_b^T V_b): the xLARFT forward
+      //      recurrence T[0:c,c] = -tau_c T[0:c,0:c] S[0:c,c] is exactly this inverse
+      //      (induction on c).  Recursive doubling: for block size h = 1, 2, .., 16 the
+      //      off-diagonal block of each 2h x 2h diagonal block is -T11 U12 T22. ----
+      for (int x = tid; x < kNbBt * 32; x += kBtThreads) {
+        const int a = x >> 5, c = x & 31;
+        Tm[a * 33 + c] = (a == c) ? tau[a] : 0.f;
+      }
+      __syncthreads();
+      for (int h = 1; h < kNbBt; h <<= 1) {
+        const int npair = kNbBt / (2 * h), nent = npair * h * h;
+        // Y = U12 T22 (U12 = S block, rows 2mh.., cols (2m+1)h..)
+        for (int x = tid; x < nent; x += kBtThreads) {
+          const int m = x / (h * h), e = x - m * h * h, i = e / h, j = e - (e / h) * h;
+          const int r1 = 2 * m * h, c2 = (2 * m + 1) * h;
+          float y = 0.f;
+          for (int k = 0; k < h; ++k) y = fmaf(S[(r1 + i) * 33 + c2 + k], Tm[(c2 + k) * 33 + c2 + j], y);
+          W2[x] = y;
+        }
+        __syncthreads();
+        // X = -T11 Y
+        for (int x = tid; x < nent; x += kBtThreads) {
+          const int m = x / (h * h), e = x - m * h * h, i = e / h, j = e - (e / h) * h;
+          const int r1 = 2 * m * h, c2 = (2 * m + 1) * h;
           float t = 0.f;
-          if (lane < c) {
-            for (int k = lane; k < c; ++k) t = fmaf(Tm[lane * 33 + k], S[k * 33 + c], t);
-            t *= -tau[c];
-          } else if (lane == c) {
-            t = tau[c];
-          }
-          __syncwarp();
-          if (lane <= c) Tm[lane * 33 + c] = t;
-          else Tm[lane * 33 + c] = 0.f;
-          __syncwarp();
+          for (int k = 0; k < h; ++k) t = fmaf(Tm[(r1 + i) * 33 + r1 + k], W2[m * h * h + k * h + j], t);
+          Tm[(r1 + i) * 33 + c2 + j] = -t;
         }
+        __syncthreads();
       }
-      __syncthreads();
-      // ---- W2 = T W1 (T upper triangular) ----
-      {
-        const int cb = 4 * warp, jb = 4 * lane;
+      // ---- W2 = T W1 (T upper triangular; group 0) ----
+      if (grp == 0) {
+        const int cb = 4 * wg8, jb = 4 * lane;
         float acc[4][4] = {};
         {
           for (int k = cb; k < kNbBt; ++k) {
@@ -143,7 +171,7 @@ __global__ void __launch_bounds__(kBtThreads, 1) bt_kernel(const Prob* __restric
       __syncthreads();
       // ---- Z[r0:N, :] -= V_b W2 : thread = 4 rows x 4 columns per 32-row group ----
       {
-        const int rq = warp, jb = 4 * lane;
+        const int rq = warp, jb = 4 * lane;   // 16 warps x 4 rows per 64-row sweep
         if (jb < Jp) {  // columns >= Jp of Z are zero
           for (int rbase = r0 + 4 * rq; rbase < N; rbase += 4 * (kBtThreads / 32)) {
             float acc[4][4] = {};
@@ -154,7 +182,7 @@ __global__ void __launch_bounds__(kBtThreads, 1) bt_kernel(const Prob* __restric
 #pragma unroll
               for (int a = 0; a < 4; ++a) {
                 const int r = rbase + a;
-                const float v = (r < N) ? Vb[r * kNbBt + k] : 0.f;
+                const float v = (r < N) ? Vb[k * kVld + r] : 0.f;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) acc[a][q] = fmaf(v, wa[q], acc[a][q]);
               }
@@ -175,7 +203,7 @@ __global__ void __launch_bounds__(kBtThreads, 1) bt_kernel(const Prob* __restric
     }
     // ---- Wt[j][r] = w_j U[r][j], transposed through per-warp 32 x 33 smem tiles ----
     {
-      float* tile = Vb + warp * 32 * 33;   // V_b / W1 are free now (8 x 4.1 KB)
+      float* tile = Vb + warp * 32 * 33;   // V_b / W1 / W2 are free now (16 x 4.1 KB)
       const int ntr = (N + 31) / 32, ntj = (J + 31) / 32;
       for (int t = warp; t < ntr * ntj; t += kBtThreads / 32) {
         const int rt = t / ntj, jt = t - rt * ntj;
@@ -197,7 +225,7 @@ __global__ void __launch_bounds__(kBtThreads, 1) bt_kernel(const Prob* __restric
 }
 
 size_t bt_smem_bytes() {
-  return sizeof(float) * ((size_t)kMaxN * kZld + (size_t)kMaxN * kNbBt + 2 * kNbBt * 128 + 2 * kNbBt * 33 + kNbBt);
+  return sizeof(float) * ((size_t)kMaxN * kZld + (size_t)kNbBt * kVld + 2 * kNbBt * 128 + 2 * kNbBt * 33 + kNbBt);
 }
 
 bool bt_supported(int nmax, const Params& p) { return p.pretrd && nmax <= kMaxN && p.ell - 1 <= 128; }
