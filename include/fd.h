@@ -70,7 +70,7 @@ typedef enum {
 } fd_variant;
 
 /* Largest eigen-problem (buffer Gram) size supported by this build. */
-#define FD_MAX_N 256
+#define FD_MAX_N 416
 
 typedef struct {
   int64_t d;        /* row length (columns of A), >= 1                                     */

@@ -111,7 +111,7 @@ Layout layout(const Derived& D) {
 
   Lo.stats = take((size_t)(D.P + Lo.nnodes) * sizeof(Stats));
   Lo.flag = take(sizeof(int) * 4);
-  Lo.eig = take(fdk::eig_scratch_bytes());
+  Lo.eig = take(fdk::eig_scratch_bytes(D.ldg));
   Lo.arena = take(2 * kArenaHalf);
   Lo.total = off;
   return Lo;
@@ -368,6 +368,7 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
   h->prm.d = D.d; h->prm.ldb = D.ldb; h->prm.ldg = D.ldg; h->prm.ell = D.ell; h->prm.rule = D.rule; h->prm.m = D.m;
   h->prm.f64 = 0;
   h->prm.pretrd = 0;
+  h->prm.zld = D.ldg;
   h->legacy_trd = getenv("FD_LEGACY_TRD") != nullptr;
   h->simt_gemm = getenv("FD_SIMT_GEMM") != nullptr;
   h->simt_gram = h->simt_gemm || getenv("FD_SIMT_GRAM") != nullptr;

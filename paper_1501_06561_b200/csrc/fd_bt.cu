@@ -28,7 +28,7 @@ namespace {
 constexpr int kBtThreads = 512;    // two groups of 8 warps split the row range of each product
 constexpr int kNbBt = 32;          // reflectors per block
 constexpr int kZld = 132;          // Z row stride (floats): J <= 128, padded
-constexpr int kVld = kMaxN + 1;    // V_b column stride (column-major, odd: conflict-free)
+constexpr int kVld = kMaxNS + 1;    // V_b column stride (column-major, odd: conflict-free)
 
 __device__ __forceinline__ int pk_off_b(int c, int N) { return c * N - (c * (c - 1)) / 2; }
 
@@ -36,8 +36,8 @@ __device__ __forceinline__ int pk_off_b(int c, int N) { return c * N - (c * (c -
 
 __global__ void __launch_bounds__(kBtThreads, 1) bt_kernel(const Prob* __restrict__ probs, int count, Params p) {
   extern __shared__ __align__(16) float sm[];
-  float* Zs = sm;                                  // [kMaxN][kZld]
-  float* Vb = Zs + kMaxN * kZld;                   // [32][kVld]   Vb[c][r] = v_{i0+c}[r]
+  float* Zs = sm;                                  // [kMaxNS][kZld]
+  float* Vb = Zs + kMaxNS * kZld;                   // [32][kVld]   Vb[c][r] = v_{i0+c}[r]
   float* W1 = Vb + kNbBt * kVld;                   // [32][128]
   float* W2 = W1 + kNbBt * 128;                    // [32][128]  (also group 1's partial W1)
   float* S = W2 + kNbBt * 128;                     // [32][33]  V^T V
@@ -225,10 +225,10 @@ __global__ void __launch_bounds__(kBtThreads, 1) bt_kernel(const Prob* __restric
 }
 
 size_t bt_smem_bytes() {
-  return sizeof(float) * ((size_t)kMaxN * kZld + (size_t)kNbBt * kVld + 2 * kNbBt * 128 + 2 * kNbBt * 33 + kNbBt);
+  return sizeof(float) * ((size_t)kMaxNS * kZld + (size_t)kNbBt * kVld + 2 * kNbBt * 128 + 2 * kNbBt * 33 + kNbBt);
 }
 
-bool bt_supported(int nmax, const Params& p) { return p.pretrd && nmax <= kMaxN && p.ell - 1 <= 128; }
+bool bt_supported(int nmax, const Params& p) { return p.pretrd && nmax <= kMaxNS && p.ell - 1 <= 128; }
 
 cudaError_t launch_bt(const Prob* dev_probs, int count, const Params& p, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;

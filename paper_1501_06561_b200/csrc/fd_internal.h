@@ -7,7 +7,8 @@
 namespace fdk {
 
 constexpr int kNumSMs = 148;
-constexpr int kMaxN = 256;          // largest buffer Gram (eigen-problem) size (fp32 path)
+constexpr int kMaxN = 416;          // largest buffer Gram (eigen-problem) size (fp32 path; c3 ell=200 -> 400)
+constexpr int kMaxNS = 256;         // largest size whose packed matrix / eigenvector block is smem-resident
 constexpr int kMaxN64 = 160;        // largest problem run in fp64 (per-row chains)
 constexpr int kEigThreads = 512;
 
@@ -55,6 +56,7 @@ struct Params {
   int m;         // alpha-FD: number of trailing values that shrink
   int f64;       // 1: Gram / eigen / reconstruct accumulate in fp64 (per-row chains)
   int pretrd;    // 1: the Gram scratch already holds the tridiagonal form (trd_kernel)
+  int zld;       // eig_kernel fp64 scratch stride (>= every problem size of the handle)
   long long* dbg;  // optional phase clock trace of problem 0 (FD_DEBUG_EIG), else null
 };
 
@@ -63,7 +65,7 @@ cudaError_t launch_ingest(const Ingest* dev_desc, int count, const Params& p, in
 cudaError_t launch_gram(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s);
 cudaError_t launch_eig(const Prob* dev_probs, int count, const Params& p, double* scratch, cudaStream_t s);
 cudaError_t launch_recon(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s);
-size_t eig_scratch_bytes();   // device scratch the eig kernel needs (all CTA slots)
+size_t eig_scratch_bytes(int zld);   // device scratch the eig kernel needs (all CTA slots)
 // Register-resident Householder tridiagonalisation (fd_trd.cu): overwrites each
 // problem's Gram scratch with the packed reflectors + d / e / tau.
 bool trd_supported(int nmax, const Params& p);

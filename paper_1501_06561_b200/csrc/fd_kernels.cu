@@ -238,15 +238,19 @@ cudaError_t launch_recon(const Prob* dev_probs, int count, int nmax, const Param
 // problems), precision T, max size NM.
 // ============================================================================
 constexpr int kNW = kEigThreads / 32;  // 16 warps
-// fp64 scratch per CTA slot: LDL^T factors (2N per cluster thread) + Z (N per vector)
-constexpr size_t kSlotDoubles = (size_t)3 * kMaxN * kMaxN;
+// fp64 scratch per CTA slot (stride zld): LDL^T factors and Z (element-major
+// [i][j], zld x zld each), a Rayleigh-Ritz copy region, then, for problems above
+// kMaxNS, the packed matrix (global / L2 instead of shared memory).
+__host__ __device__ inline size_t slot_doubles(int zld) {
+  return (size_t)4 * zld * zld + (zld > kMaxNS ? ((size_t)zld * (zld + 1) / 2 + 1) / 2 : 0);
+}
 
-size_t eig_scratch_bytes() { return (size_t)kNumSMs * kSlotDoubles * sizeof(double); }
+size_t eig_scratch_bytes(int zld) { return (size_t)kNumSMs * slot_doubles(zld) * sizeof(double); }
 
-template <typename T, int NM>
+template <typename T, int NM, bool GAPK>
 struct EigCfg {
   static_assert(NM % 32 == 0, "NM must be a multiple of 32");
-  static constexpr int kPk = NM * (NM + 1) / 2;
+  static constexpr int kPk = GAPK ? 0 : NM * (NM + 1) / 2;   // packed matrix in smem unless GAPK
   static constexpr int kPart = kNW * NM + 32 * (NM + 1);  // ppart[16][NM] + colpart[32][NM+1]
   static constexpr int kVec = 13;                 // vector arrays of NM
   static constexpr size_t kT = (size_t)kPk + kPart + kVec * NM + 64;  // elements of T
@@ -308,16 +312,18 @@ template <> struct Lim<double> {
   static constexpr float bits = 56.f;
 };
 
-template <typename T, int NM>
+template <typename T, int NM, bool GAPK>
 __global__ void __launch_bounds__(kEigThreads, 1)
 eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restrict__ scratch) {
-  using C = EigCfg<T, NM>;
+  using C = EigCfg<T, NM, GAPK>;
   constexpr int NT = NM / 32;   // row blocks (lane <-> row 32t + lane)
   constexpr int NK = NM / kNW;  // columns per warp (warp <-> column warp + 16k)
   extern __shared__ __align__(16) unsigned char smraw[];
   T* sm = reinterpret_cast<T*>(smraw);
-  T* Apk = sm;
-  T* ppart = Apk + C::kPk;        // [kNW][NM]  per-warp row partials of the SYMV
+  const int kMaxN = p.zld;        // scratch stride (runtime)
+  double* slot = scratch + (size_t)blockIdx.x * slot_doubles(kMaxN);
+  T* Apk = GAPK ? reinterpret_cast<T*>(slot + (size_t)4 * kMaxN * kMaxN) : sm;
+  T* ppart = sm + C::kPk;         // [kNW][NM]  per-warp row partials of the SYMV
   T* colpart = ppart + kNW * NM;  // [32][NM+1] per-lane column partials (padded: no bank conflicts)
   T* vbuf0 = colpart + 32 * (NM + 1);   // v / w of the current and previous Householder step
   T* wbuf0 = vbuf0 + NM;
@@ -342,7 +348,6 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
   __shared__ T s_gl, s_gu, s_a1, s_a2;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* slot = scratch + (size_t)blockIdx.x * kSlotDoubles;
   // element-major (coalesced across threads): LF[i][cl], RD[i][cl], Zs[i][j]
   double* LF = slot;
   double* RD = slot + (size_t)kMaxN * kMaxN;
@@ -744,35 +749,35 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
           if (j1 - j0 < 2) continue;
           for (int k = j0; k < j1; ++k) {
             double* zk = Zs + k;
-            double zr[kMaxN / 32];
+            double zr[NM / 32];
             const double s0 = pscl[k];
 #pragma unroll
-            for (int t = 0; t < kMaxN / 32; ++t) {
+            for (int t = 0; t < NM / 32; ++t) {
               const int i = 32 * t + lane;
               zr[t] = (i < N) ? zk[(size_t)i * kMaxN] * s0 : 0.0;
             }
             for (int pass = 0; pass < 2; ++pass)
               for (int q = j0; q < k; ++q) {
                 const double* zq = Zs + q;
-                double zqr[kMaxN / 32];
+                double zqr[NM / 32];
                 double h = 0.0;
 #pragma unroll
-                for (int t = 0; t < kMaxN / 32; ++t) {
+                for (int t = 0; t < NM / 32; ++t) {
                   const int i = 32 * t + lane;
                   zqr[t] = (i < N) ? zq[(size_t)i * kMaxN] : 0.0;
                   h = fma(zqr[t], zr[t], h);
                 }
                 h = warp_sum_d(h);
 #pragma unroll
-                for (int t = 0; t < kMaxN / 32; ++t) zr[t] = fma(-h, zqr[t], zr[t]);
+                for (int t = 0; t < NM / 32; ++t) zr[t] = fma(-h, zqr[t], zr[t]);
               }
             double n2 = 0.0;
 #pragma unroll
-            for (int t = 0; t < kMaxN / 32; ++t) n2 = fma(zr[t], zr[t], n2);
+            for (int t = 0; t < NM / 32; ++t) n2 = fma(zr[t], zr[t], n2);
             n2 = warp_sum_d(n2);
             const double inv = (n2 > 0.0) ? 1.0 / sqrt(n2) : 0.0;
 #pragma unroll
-            for (int t = 0; t < kMaxN / 32; ++t) {
+            for (int t = 0; t < NM / 32; ++t) {
               const int i = 32 * t + lane;
               if (i < N) zk[(size_t)i * kMaxN] = zr[t] * inv;
             }
@@ -790,10 +795,9 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
     for (int r = 0; r < s_nrr; ++r) {
       const int c = cid[r];
       const int j0 = cstart[c], nc = clen[c];
-      if (nc > 181) continue;           // H and Q (nc x nc each) must fit the LF scratch
       double* H = LF;                   // nc x nc (ld nc)
-      double* Q = LF + (size_t)nc * nc;
-      double* Zc = RD;                  // copy of Z_c (element-major, ld kMaxN)
+      double* Q = RD;                   // nc x nc (ld nc)
+      double* Zc = Zs + (size_t)kMaxN * kMaxN;   // copy of Z_c (N x nc), 4th scratch region
       for (int x = tid; x < nc * nc; x += blockDim.x) {
         const int a = x / nc, b = x % nc;
         const double* za = Zs + j0 + a;
@@ -957,24 +961,25 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
   }
 }
 
-template <typename T, int NM>
+template <typename T, int NM, bool GAPK>
 static cudaError_t launch_eig_t(const Prob* dev_probs, int count, const Params& p, double* scratch, cudaStream_t s) {
-  using C = EigCfg<T, NM>;
+  using C = EigCfg<T, NM, GAPK>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(eig_kernel<T, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kBytes);
+    cudaError_t e = cudaFuncSetAttribute(eig_kernel<T, NM, GAPK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kBytes);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int grid = count < kNumSMs ? count : kNumSMs;
-  eig_kernel<T, NM><<<grid, kEigThreads, C::kBytes, s>>>(dev_probs, count, p, scratch);
+  eig_kernel<T, NM, GAPK><<<grid, kEigThreads, C::kBytes, s>>>(dev_probs, count, p, scratch);
   return cudaGetLastError();
 }
 
 cudaError_t launch_eig(const Prob* dev_probs, int count, const Params& p, double* scratch, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
-  if (p.f64) return launch_eig_t<double, kMaxN64>(dev_probs, count, p, scratch, s);
-  return launch_eig_t<float, kMaxN>(dev_probs, count, p, scratch, s);
+  if (p.f64) return launch_eig_t<double, kMaxN64, false>(dev_probs, count, p, scratch, s);
+  if (p.zld <= kMaxNS) return launch_eig_t<float, kMaxNS, false>(dev_probs, count, p, scratch, s);
+  return launch_eig_t<float, kMaxN, true>(dev_probs, count, p, scratch, s);
 }
 
 // ============================================================================

@@ -48,7 +48,7 @@ def test_workspace_bytes_and_validation():
     assert L.fd_workspace_bytes(ctypes.byref(_cfg(n_shards=8))) > L.fd_workspace_bytes(ctypes.byref(_cfg()))
     h = ctypes.c_void_p()
     assert L.fd_create(ctypes.byref(_cfg(ell=1)), None, 0, None, ctypes.byref(h)) == -1
-    assert L.fd_create(ctypes.byref(_cfg(ell=200, variant=1)), ctypes.c_void_p(1), 1 << 40, None,
+    assert L.fd_create(ctypes.byref(_cfg(ell=209, variant=1)), ctypes.c_void_p(1), 1 << 40, None,
                        ctypes.byref(h)) == -8
     assert L.fd_create(ctypes.byref(_cfg()), None, 0, None, ctypes.byref(h)) == -4
     assert L.fd_cov_workspace_bytes(0) == 0 and L.fd_cov_workspace_bytes(64) > 64 * 64 * 8

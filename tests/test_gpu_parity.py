@@ -139,6 +139,29 @@ def test_parity_c2_perrow_ell40(variant):
     check_parity(_c2(), 40, variant)
 
 
+_C3 = {}
+
+
+def _c3(n):
+    if n not in _C3:
+        w = fdgen.config("c3", n=n)
+        w.xminmax = fdgen.host_minmax(w)
+        _C3[n] = fdgen.host_rows(w)
+    return _C3[n]
+
+
+@pytest.mark.parametrize("ell,variant", [(50, "fast_fd"), (100, "fast_alpha_fd")])
+def test_parity_c3_prefix(ell, variant):
+    """Config 3's image-like generator (d = 3072), first 3000 rows, 2 shards + merge."""
+    check_parity(_c3(3000), ell, variant, n_shards=2)
+
+
+def test_parity_c3_ell200_large_gram():
+    """c3 at ell = 200: buffer Gram N = 2 ell = 400 > 256 (global-memory eigensolver
+    variant), merge Gram 2 ell - 2 = 398."""
+    check_parity(_c3(2000), 200, "fast_fd", n_shards=2)
+
+
 def test_parity_c5_scaled_perrow():
     """Config 5's generator with 1000-row blocks (20 subspaces in 20000 rows, rank
     ~161 > ell): the drifting-subspace structure at a size the per-row oracle runs fast."""
@@ -242,7 +265,7 @@ def test_max_perrow_size():
 def test_unsupported_and_invalid():
     m = fd()
     with pytest.raises(m.FdError) as e:
-        m.Sketcher(64, 129, "fast_fd")
+        m.Sketcher(64, 209, "fast_fd")   # buffer Gram 418 > FD_MAX_N = 416
     assert "UNSUPPORTED" in str(e.value)
     with pytest.raises(m.FdError):
         m.Sketcher(64, 8, "alpha_fd", alpha=1.5)
