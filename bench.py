@@ -49,15 +49,21 @@ def peaks():
     return p
 
 
-def algorithmic_flops_per_shrink(ell, d, N):
-    """Per-ReduceRank algorithmic flops:
-    gram  = [2(ell^2-1) + (ell+1)(ell+2)] d   (cross + new blocks; the retained block is diag(sigma'^2))
-    recon = 4 ell (ell-1) d                    (Wt (ell-1 x 2ell) . Bf (2ell x d))
-    eig   = 4/3 N^3 + 2 N^2 (ell-1)            (Householder tridiagonalisation + back-transform)"""
+def algorithmic_work(ell, d, N):
+    """Algorithmic work of one ReduceRank:
+    gram  = [2(ell^2-1) + (ell+1)(ell+2)] d flops (cross + new blocks; the retained
+            block is diag(sigma'^2))
+    recon = 4 ell (ell-1) d flops           (Wt (ell-1 x 2ell) . Bf (2ell x d))
+    trd   = (4/3) N^3 flops                 (Householder tridiagonalisation)
+    bt    = 2 N^2 (ell-1) flops             (back-transform of ell-1 eigenvectors)
+    eig   = 0                               (bisection + inverse iteration: O(N^2), latency-bound)
+    ingest= 2 (ell+1) d 4 bytes             (read the rows, write the buffer)"""
     return {
         "gram": (2 * (ell * ell - 1) + (ell + 1) * (ell + 2)) * d,
         "recon": 4 * ell * (ell - 1) * d,
-        "eig": (4.0 / 3.0) * N ** 3 + 2.0 * N * N * (ell - 1),
+        "trd": (4.0 / 3.0) * N ** 3,
+        "bt": 2.0 * N * N * (ell - 1),
+        "eig": 0.0,
     }
 
 
@@ -272,45 +278,59 @@ def run_ours(args):
     # ---- roofline of the dominant kernel (live CUDA-event times of this run) ----
     pk = peaks()
     N = 2 * ell if fd.is_batched(variant) else ell
-    fl = algorithmic_flops_per_shrink(ell, w.d, N)
-    shrinks_per_step = sk_stats_shrinks = None
-    dom = max(("ingest", "gram", "eig", "recon"), key=lambda k: kern[k][0])
-    # shrinks per step on this rank: every ReduceRank launch processes a batch of problems
+    work = algorithmic_work(ell, w.d, N)
     sk.reset()
     sk.append(A)
     Bst, st = sk.sketch(stats=True)
     shrinks_per_step = st["n_shrinks"]
-    mhz = clk["sm_mhz"] or pk.get("sm_max_mhz", 1965.0)
     simt_peak = fp32_simt_peak_tflops(pk.get("sm_max_mhz", 1965.0))
+    tf32_peak = pk["bf16_tflops"] / 2.0          # nominal tf32 = bf16 / 2 (B200_PROFILING.md)
+    dom = max(kern, key=lambda k: kern[k][0])
     dom_ms = kern[dom][0] / args.steps
     if dom == "ingest":
         bytes_step = 2.0 * nloc * w.d * 4
-        achieved = bytes_step / (dom_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s"}
+        roof = {"bound": "hbm", "achieved": bytes_step / (dom_ms / 1e3) / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s"}
+    elif dom == "gram":
+        flops_step = work["gram"] * shrinks_per_step
+        roof = {"bound": "tensor", "achieved": flops_step / (dom_ms / 1e3) / 1e12, "peak": tf32_peak / 3.0,
+                "unit": "TFLOP/s"}
     else:
-        flops_step = fl[dom] * shrinks_per_step
-        achieved = flops_step / (dom_ms / 1e3) / 1e12
-        roof = {"bound": "alu", "achieved": achieved, "peak": simt_peak, "unit": "TFLOP/s"}
+        flops_step = work[dom] * shrinks_per_step
+        roof = {"bound": "alu", "achieved": flops_step / (dom_ms / 1e3) / 1e12, "peak": simt_peak, "unit": "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["kernel"] = f"{dom}_kernel"
     roof["kernel_share_of_step"] = kern[dom][0] / ms_total
     roof["per_kernel_ms_per_step"] = {k: v[0] / args.steps for k, v in kern.items()}
     roof["launches_per_step"] = {k: v[1] / args.steps for k, v in kern.items()}
-    roof["peak_source"] = (f"FP32 SIMT 148 SM x 128 lanes x 2 x {pk.get('sm_max_mhz', 1965.0):.0f} MHz (derived)"
-                           if roof["bound"] == "alu" else f"hbm_gbs {pk['source']}")
+    roof["problems_per_step"] = shrinks_per_step
+    roof["peak_source"] = {
+        "alu": f"FP32 SIMT: 148 SM x 128 lanes x 2 flop x {pk.get('sm_max_mhz', 1965.0):.0f} MHz (derived, DESIGN.md §5)",
+        "tensor": f"3xTF32 = (bf16_tflops {pk['bf16_tflops']} / 2) / 3, {pk['source']}",
+        "hbm": f"hbm_gbs {pk['source']}"}[roof["bound"]]
     traffic_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     roof["traffic"] = None
     if os.path.exists(traffic_file):
         with open(traffic_file) as f:
-            roof["traffic"] = json.load(f).get(roof["kernel"])
-    # end-to-end north_star roofline (GEMM pipe + HBM) for context
-    gemm_flops_row = (7 * ell * ell - ell) * w.d / (ell + 1)
-    gemm_peak = simt_peak * 1e12
-    roof["step_vs_north_star_roofline"] = {
-        "R_roof_rows_per_s_per_gpu": min(pk["hbm_gbs"] * 1e9 / (4 * w.d), gemm_peak / gemm_flops_row),
-        "pipe": "FP32 SIMT (v1 kernels)",
-    }
-    roof["step_vs_north_star_roofline"]["frac"] = (value / world) / roof["step_vs_north_star_roofline"]["R_roof_rows_per_s_per_gpu"]
+            tr = json.load(f).get(roof["kernel"])
+        if tr:
+            # bytes per problem from the committed capture x problems per launch of this run
+            roof["traffic"] = tr["bytes_per_problem"] * shrinks_per_step / max(kern[dom][1], 1) * args.steps
+            roof["traffic_source"] = tr["source"]
+    # north_star roofline: slower of HBM (4d bytes/row) and the Gram + reconstruct flops
+    # on the pipes this build uses (Gram: tcgen05 3xTF32; reconstruct: FP32 SIMT)
+    n_rows = w.n / world
+    gram_s = work["gram"] * shrinks_per_step / (tf32_peak / 3.0 * 1e12)
+    recon_s = work["recon"] * shrinks_per_step / (simt_peak * 1e12)
+    hbm_s = n_rows * 4 * w.d / (pk["hbm_gbs"] * 1e9)
+    t_roof = max(hbm_s, gram_s + recon_s)
+    roof["north_star"] = {
+        "R_roof_rows_per_s_per_gpu": n_rows / t_roof, "t_roof_ms": t_roof * 1e3,
+        "pipes": "Gram tcgen05 3xTF32 (bf16/6), reconstruct FP32 SIMT", "hbm_ms": hbm_s * 1e3,
+        "frac": (value / world) / (n_rows / t_roof)}
+    eig_flops = (work["trd"] + work["bt"]) * shrinks_per_step
+    roof["eigensolver_inclusive"] = {
+        "t_roof_ms": (t_roof + eig_flops / (simt_peak * 1e12)) * 1e3,
+        "frac": (ms_step / 1e3) and ((t_roof + eig_flops / (simt_peak * 1e12)) / (ms_step / 1e3))}
 
     gpu_launches = int(sum(v[1] for v in kern.values()))
 
@@ -356,7 +376,8 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded fdgen, generated on device)",
+        "vs_baseline": None, "dtype": "f32 (Gram: 3xTF32 tensor cores, fp32-accurate)",
+        "data": "synthetic (seeded fdgen, generated on device)",
         "config": config_dict(wl, variant, P, world),
         "roofline": roof,
         "gpu_launches": gpu_launches,

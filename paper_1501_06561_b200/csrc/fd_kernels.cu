@@ -238,6 +238,7 @@ cudaError_t launch_recon(const Prob* dev_probs, int count, int nmax, const Param
 // problems), precision T, max size NM.
 // ============================================================================
 constexpr int kNW = kEigThreads / 32;  // 16 warps
+constexpr int kEigPreCtasPerSM = 3;     // resident CTAs of the lean (tridiagonal-input) variant
 // fp64 scratch per CTA slot (stride zld): LDL^T factors and Z (element-major
 // [i][j], zld x zld each), a Rayleigh-Ritz copy region, then, for problems above
 // kMaxNS, the packed matrix (global / L2 instead of shared memory).
@@ -245,13 +246,17 @@ __host__ __device__ inline size_t slot_doubles(int zld) {
   return (size_t)4 * zld * zld + (zld > kMaxNS ? ((size_t)zld * (zld + 1) / 2 + 1) / 2 : 0);
 }
 
-size_t eig_scratch_bytes(int zld) { return (size_t)kNumSMs * slot_doubles(zld) * sizeof(double); }
+size_t eig_scratch_bytes(int zld) {
+  return (size_t)kNumSMs * kEigPreCtasPerSM * slot_doubles(zld) * sizeof(double);
+}
 
-template <typename T, int NM, bool GAPK>
+template <typename T, int NM, bool GAPK, bool PRE = false>
 struct EigCfg {
   static_assert(NM % 32 == 0, "NM must be a multiple of 32");
-  static constexpr int kPk = GAPK ? 0 : NM * (NM + 1) / 2;   // packed matrix in smem unless GAPK
-  static constexpr int kPart = kNW * NM + 32 * (NM + 1);  // ppart[16][NM] + colpart[32][NM+1]
+  // packed matrix in smem unless GAPK (global) or PRE (tridiagonal form precomputed by
+  // trd_kernel: neither the packed matrix nor the Householder workspaces are needed)
+  static constexpr int kPk = (GAPK || PRE) ? 0 : NM * (NM + 1) / 2;
+  static constexpr int kPart = PRE ? 0 : kNW * NM + 32 * (NM + 1);  // ppart[16][NM] + colpart[32][NM+1]
   static constexpr int kVec = 13;                 // vector arrays of NM
   static constexpr size_t kT = (size_t)kPk + kPart + kVec * NM + 64;  // elements of T
   static constexpr size_t kBytes = kT * sizeof(T) + 4 * NM * sizeof(int) + NM * sizeof(double) + 16;
@@ -312,20 +317,24 @@ template <> struct Lim<double> {
   static constexpr float bits = 56.f;
 };
 
-template <typename T, int NM, bool GAPK>
-__global__ void __launch_bounds__(kEigThreads, 1)
+// PRE = true: the lean variant for the tridiagonal-kernel path (p.pretrd): 256
+// threads, small shared memory, several CTAs (problems) per SM.
+template <typename T, int NM, bool GAPK, bool PRE = false>
+__global__ void __launch_bounds__(PRE ? 256 : kEigThreads, PRE ? 3 : 1)
 eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restrict__ scratch) {
-  using C = EigCfg<T, NM, GAPK>;
+  using C = EigCfg<T, NM, GAPK, PRE>;
+  constexpr int kNT = PRE ? 256 : kEigThreads;   // threads
+  constexpr int kNW = kNT / 32;                  // warps
   constexpr int NT = NM / 32;   // row blocks (lane <-> row 32t + lane)
   constexpr int NK = NM / kNW;  // columns per warp (warp <-> column warp + 16k)
   extern __shared__ __align__(16) unsigned char smraw[];
   T* sm = reinterpret_cast<T*>(smraw);
   const int kMaxN = p.zld;        // scratch stride (runtime)
-  double* slot = scratch + (size_t)blockIdx.x * slot_doubles(kMaxN);
+  double* slot = scratch + (size_t)blockIdx.x * slot_doubles(kMaxN);   // one slot per resident CTA
   T* Apk = GAPK ? reinterpret_cast<T*>(slot + (size_t)4 * kMaxN * kMaxN) : sm;
   T* ppart = sm + C::kPk;         // [kNW][NM]  per-warp row partials of the SYMV
   T* colpart = ppart + kNW * NM;  // [32][NM+1] per-lane column partials (padded: no bank conflicts)
-  T* vbuf0 = colpart + 32 * (NM + 1);   // v / w of the current and previous Householder step
+  T* vbuf0 = sm + C::kPk + C::kPart;    // v / w of the current and previous Householder step
   T* wbuf0 = vbuf0 + NM;
   T* vbuf1 = wbuf0 + NM;
   T* wbuf1 = vbuf1 + NM;
@@ -360,7 +369,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
     long long t_ph0 = clock64();
     const T* G = static_cast<const T*>(P.G);
     T* Wt = static_cast<T*>(P.Wt);
-    if (p.pretrd) {
+    if (PRE || p.pretrd) {
       // ---------------- tridiagonal form from trd_kernel (fd_trd.cu) ----------------
       // packed Householder vectors, then d / e / tau at round_up(N(N+1)/2, 4)
       const float* V = reinterpret_cast<const float*>(P.G);
@@ -374,7 +383,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
       }
       __syncthreads();
       if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[1] += t_ - t_ph0; t_ph0 = t_; }
-    } else {
+    } else if constexpr (!PRE) {
     // ---------------- load lower triangle (packed, column-major) ----------------
     for (int c = warp; c < N; c += kNW) {
       const int oc = pk_off(c, N);
@@ -566,7 +575,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
     if (N > 0) {
       int kp = 1;
       while (kp < KC) kp <<= 1;
-      int g = kEigThreads / kp;  // threads per eigenvalue (power of two)
+      int g = kNT / kp;  // threads per eigenvalue (power of two)
       if (g > 32) g = 32;
       if (g < 1) g = 1;
       const int j = tid / g, sub = tid % g;
@@ -666,56 +675,47 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
         }
       }
       double* lf = LF + j;   // lf[i * kMaxN]  multipliers of L
-      double* rdp = RD + j;  // rdp[i * kMaxN] reciprocal pivots of D
       double* z = Zs + j;    // z[i * kMaxN]
       double sc = 1.0;
       for (int it = 0; it < 3; ++it) {
         if (act) {
-          double u;
-          if (it == 0) {
-            // L D L^T = T - mu I (tiny pivots perturbed) fused with the forward
-            // solve L u = b, v = D^-1 u of the start vector b.
-            const double mu = (double)lam[j];
-            double dpi = (double)dd[0] - mu;
-            if (fabs(dpi) < tiny) dpi = (dpi < 0.0) ? -tiny : tiny;
-            double rd = 1.0 / dpi;
-            rdp[0] = rd;
-            u = 1.0 + 0.5 * (double)(((1) * 7919 + (j + 3) * 104729) % 211) / 211.0;
-            z[0] = u * rd;
-            for (int i = 0; i < N - 1; ++i) {
-              const double e = (double)ee[i];
-              const double li = e * rd;
-              lf[(size_t)i * kMaxN] = li;
-              dpi = ((double)dd[i + 1] - mu) - li * e;
-              if (fabs(dpi) < tiny) dpi = (dpi < 0.0) ? -tiny : tiny;
-              rd = 1.0 / dpi;
-              rdp[(size_t)(i + 1) * kMaxN] = rd;
-              const double b = 1.0 + 0.5 * (double)(((i + 2) * 7919 + (j + 3) * 104729) % 211) / 211.0;
-              u = b - li * u;
-              z[(size_t)(i + 1) * kMaxN] = u * rd;
+          // L D L^T = T - mu I (tiny pivots perturbed), recomputed every iteration and
+          // fused with the forward solve L u = b, v = D^-1 u (b: start vector, then the
+          // scaled previous iterate); only the multipliers of L are stored (for the
+          // backward solve), so the per-CTA scratch stays L2-resident.
+          const double mu = (double)lam[j];
+          double rd = 0.0, u = 0.0, eprev = 0.0;
+          for (int i0 = 0; i0 < N; i0 += 8) {
+            double zb[8];
+            if (it > 0) {
+#pragma unroll
+              for (int q = 0; q < 8; ++q) zb[q] = (i0 + q < N) ? z[(size_t)(i0 + q) * kMaxN] : 0.0;
             }
-          } else {  // forward solve of the (scaled) previous iterate, 8-element load batches
-            u = 0.0;
-            double lprev = 0.0;
-            for (int i0 = 0; i0 < N; i0 += 8) {
-              double zb[8], lb[8], rb[8];
 #pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                const int i = i0 + q;
-                zb[q] = (i < N) ? z[(size_t)i * kMaxN] : 0.0;
-                lb[q] = (i < N) ? lf[(size_t)i * kMaxN] : 0.0;
-                rb[q] = (i < N) ? rdp[(size_t)i * kMaxN] : 0.0;
+            for (int q = 0; q < 8; ++q) {
+              const int i = i0 + q;
+              if (i < N) {
+                const double bi = (it == 0) ? 1.0 + 0.5 * (double)(((i + 1) * 7919 + (j + 3) * 104729) % 211) / 211.0
+                                            : zb[q] * sc;
+                double dpi;
+                if (i == 0) {
+                  dpi = (double)dd[0] - mu;
+                  u = bi;
+                } else {
+                  const double li = eprev * rd;
+                  lf[(size_t)(i - 1) * kMaxN] = li;
+                  dpi = ((double)dd[i] - mu) - li * eprev;
+                  u = bi - li * u;
+                }
+                if (fabs(dpi) < tiny) dpi = (dpi < 0.0) ? -tiny : tiny;
+                rd = 1.0 / dpi;
+                zb[q] = u * rd;
+                eprev = (double)ee[i];
               }
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                u = zb[q] * sc - lprev * u;
-                lprev = lb[q];
-                zb[q] = u * rb[q];
-              }
-#pragma unroll
-              for (int q = 0; q < 8; ++q)
-                if (i0 + q < N) z[(size_t)(i0 + q) * kMaxN] = zb[q];
             }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (i0 + q < N) z[(size_t)(i0 + q) * kMaxN] = zb[q];
           }
           // backward solve L^T y = v, with the norm (8-element load batches)
           double next = 0.0, nr = 0.0;
@@ -878,7 +878,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
     }
     __syncthreads();
     if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[5] += t_ - t_ph0; t_ph0 = t_; }
-    if (p.pretrd) {
+    if (PRE || p.pretrd) {
       // ---------------- hand Z to bt_kernel (fd_bt.cu) ----------------
       // Wt scratch <- Z row-major [r][j] (ld 128; normalised, fp32; 0 for unused j);
       // w_j after the tridiagonal data in the Gram scratch
@@ -891,7 +891,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
         float* wout = reinterpret_cast<float*>(P.G) + (N * (N + 1) / 2 + 3) / 4 * 4 + 3 * N;
         for (int j = tid; j < J; j += blockDim.x) wout[j] = (float)wgt[j];
       }
-    } else
+    } else if constexpr (!PRE)
     // ---------------- back-transform U = H_0 ... H_{N-3} Z ; Wt = diag(w) U^T ----------------
     // warp-owned vectors held in registers (lane <-> rows 32t + lane), 4 per warp per chunk
     for (int c0 = 0; c0 < J; c0 += 4 * kNW) {
@@ -961,23 +961,25 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
   }
 }
 
-template <typename T, int NM, bool GAPK>
+template <typename T, int NM, bool GAPK, bool PRE = false>
 static cudaError_t launch_eig_t(const Prob* dev_probs, int count, const Params& p, double* scratch, cudaStream_t s) {
-  using C = EigCfg<T, NM, GAPK>;
+  using C = EigCfg<T, NM, GAPK, PRE>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(eig_kernel<T, NM, GAPK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kBytes);
+    cudaError_t e = cudaFuncSetAttribute(eig_kernel<T, NM, GAPK, PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kBytes);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int grid = count < kNumSMs ? count : kNumSMs;
-  eig_kernel<T, NM, GAPK><<<grid, kEigThreads, C::kBytes, s>>>(dev_probs, count, p, scratch);
+  const int slots = kNumSMs * (PRE ? kEigPreCtasPerSM : 1);
+  const int grid = count < slots ? count : slots;
+  eig_kernel<T, NM, GAPK, PRE><<<grid, PRE ? 256 : kEigThreads, C::kBytes, s>>>(dev_probs, count, p, scratch);
   return cudaGetLastError();
 }
 
 cudaError_t launch_eig(const Prob* dev_probs, int count, const Params& p, double* scratch, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
   if (p.f64) return launch_eig_t<double, kMaxN64, false>(dev_probs, count, p, scratch, s);
+  if (p.pretrd) return launch_eig_t<float, kMaxNS, false, true>(dev_probs, count, p, scratch, s);
   if (p.zld <= kMaxNS) return launch_eig_t<float, kMaxNS, false>(dev_probs, count, p, scratch, s);
   return launch_eig_t<float, kMaxN, true>(dev_probs, count, p, scratch, s);
 }
