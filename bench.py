@@ -56,14 +56,23 @@ def algorithmic_work(ell, d, N):
     recon = 4 ell (ell-1) d flops           (Wt (ell-1 x 2ell) . Bf (2ell x d))
     trd   = (4/3) N^3 flops                 (Householder tridiagonalisation)
     bt    = 2 N^2 (ell-1) flops             (back-transform of ell-1 eigenvectors)
-    eig   = 0                               (bisection + inverse iteration: O(N^2), latency-bound)
+    eig   = bisection K g iters N 5 + inverse iteration 3 J 13 N   (Sturm counts of the top K = ell
+            eigenvalues, g points each per multisection iteration; 3 fp64 LDL^T solves per
+            retained vector; latency-bound)
     ingest= 2 (ell+1) d 4 bytes             (read the rows, write the buffer)"""
+    import math
+    K = min(ell, N)
+    J = min(ell - 1, N)
+    kp = 1 << max(0, (K - 1).bit_length())
+    lean = 32 < N <= 256 and ell - 1 <= 128
+    g = max(1, min(32, (256 if lean else 512) // kp))
+    iters = math.ceil(27.0 / math.log2(g + 1))
     return {
         "gram": (2 * (ell * ell - 1) + (ell + 1) * (ell + 2)) * d,
         "recon": 4 * ell * (ell - 1) * d,
         "trd": (4.0 / 3.0) * N ** 3,
         "bt": 2.0 * N * N * (ell - 1),
-        "eig": 0.0,
+        "eig": K * g * iters * N * 5.0 + 3.0 * J * 13.0 * N,
     }
 
 
