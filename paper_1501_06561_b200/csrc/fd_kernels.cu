@@ -239,6 +239,7 @@ cudaError_t launch_recon(const Prob* dev_probs, int count, int nmax, const Param
 // ============================================================================
 constexpr int kNW = kEigThreads / 32;  // 16 warps
 constexpr int kEigPreCtasPerSM = 3;     // resident CTAs of the lean (tridiagonal-input) variant
+constexpr int kSmallCl = 8;             // clusters up to this size: warp MGS; larger: block CGS2
 // fp64 scratch per CTA slot (stride zld): LDL^T factors and Z (element-major
 // [i][j], zld x zld each), a Rayleigh-Ritz copy region, then, for problems above
 // kMaxNS, the packed matrix (global / L2 instead of shared memory).
@@ -259,7 +260,12 @@ struct EigCfg {
   static constexpr int kPart = PRE ? 0 : kNW * NM + 32 * (NM + 1);  // ppart[16][NM] + colpart[32][NM+1]
   static constexpr int kVec = 13;                 // vector arrays of NM
   static constexpr size_t kT = (size_t)kPk + kPart + kVec * NM + 64;  // elements of T
-  static constexpr size_t kBytes = kT * sizeof(T) + 4 * NM * sizeof(int) + NM * sizeof(double) + 16;
+  // block-CGS scratch (cpart [warps][NM+1] + chq [NM], doubles): aliases the Householder
+  // workspaces (ppart / colpart, idle during the eigenvectors) unless PRE has none
+  static constexpr int kNWc = (PRE ? 256 : kEigThreads) / 32;
+  static constexpr size_t kCgs = (size_t)(kNWc * (NM + 1) + NM) * sizeof(double);
+  static_assert(PRE || (size_t)kPart * sizeof(T) >= kCgs, "CGS scratch must fit the SYMV workspaces");
+  static constexpr size_t kBytes = kT * sizeof(T) + 4 * NM * sizeof(int) + NM * sizeof(double) + 16 + (PRE ? kCgs : 0);
 };
 
 __device__ __forceinline__ int pk_off(int c, int N) { return c * N - (c * (c - 1)) / 2; }
@@ -325,6 +331,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
   using C = EigCfg<T, NM, GAPK, PRE>;
   constexpr int kNT = PRE ? 256 : kEigThreads;   // threads
   constexpr int kNW = kNT / 32;                  // warps
+  constexpr int kCpStride = NM + 1;
   constexpr int NT = NM / 32;   // row blocks (lane <-> row 32t + lane)
   constexpr int NK = NM / kNW;  // columns per warp (warp <-> column warp + 16k)
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -353,6 +360,8 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
   int* ord = cid + NM;                        // Ritz-vector order
   constexpr size_t kOffD = C::kT * sizeof(T) + 4 * NM * sizeof(int);
   double* pscl = reinterpret_cast<double*>(smraw + kOffD + 8 - (kOffD & 7));  // per-vector scale (fp64)
+  double* cpart = PRE ? pscl + NM : reinterpret_cast<double*>(ppart);  // [kNW][kCpStride] block-CGS dots
+  double* chq = cpart + kNW * kCpStride; // [NM] projection coefficients
   __shared__ int s_ncl, s_jx, s_nrr;
   __shared__ T s_gl, s_gu, s_a1, s_a2;
 
@@ -743,10 +752,11 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
           pscl[j] = sc;
         }
         __syncthreads();
-        // multi-member clusters: warp-parallel MGS (normalise, orthogonalise twice, renormalise)
+        // clusters of 2..kSmallCl members: one warp each, modified Gram-Schmidt
+        // (normalise, orthogonalise twice, renormalise)
         for (int c = warp; c < ncl; c += kNW) {
           const int j0 = cstart[c], j1 = cstart[c] + clen[c];
-          if (j1 - j0 < 2) continue;
+          if (j1 - j0 < 2 || j1 - j0 > kSmallCl) continue;
           for (int k = j0; k < j1; ++k) {
             double* zk = Zs + k;
             double zr[NM / 32];
@@ -783,6 +793,58 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
             }
             __syncwarp();
             if (lane == 0) pscl[k] = 1.0;
+          }
+        }
+        // larger clusters (wide-spread Grams put many small eigenvalues within ctol,
+        // e.g. at merge levels): the whole CTA, one cluster at a time, classical
+        // Gram-Schmidt twice per member.  Dots: warp w sweeps its rows, lane = earlier
+        // member (row segments of a cluster are contiguous in the element-major
+        // scratch -> coalesced); update: thread per row.
+        for (int c = 0; c < ncl; ++c) {
+          const int j0 = cstart[c], nc = clen[c];
+          if (nc <= kSmallCl) continue;
+          const int rpw = (N + kNW - 1) / kNW;   // rows per warp
+          for (int k = j0; k < j0 + nc; ++k) {
+            double* zk = Zs + k;
+            const double s0 = pscl[k];
+            __syncthreads();   // previous member finished; pscl stable
+            for (int i = tid; i < N; i += kNT) zk[(size_t)i * kMaxN] *= s0;
+            for (int pass = 0; pass < 2 && k > j0; ++pass) {
+              __syncthreads();
+              for (int q0 = 0; q0 < k - j0; q0 += 32) {
+                const int q = j0 + q0 + lane;
+                double h = 0.0;
+                if (q < k) {
+                  const int ia = warp * rpw, ib = min(N, ia + rpw);
+                  for (int i = ia; i < ib; ++i) h = fma(Zs[(size_t)i * kMaxN + q], zk[(size_t)i * kMaxN], h);
+                }
+                cpart[warp * kCpStride + q0 + lane] = h;
+              }
+              __syncthreads();
+              for (int q = tid; q < k - j0; q += kNT) {
+                double h = 0.0;
+                for (int w = 0; w < kNW; ++w) h += cpart[w * kCpStride + q];
+                chq[q] = h;
+              }
+              __syncthreads();
+              for (int i = tid; i < N; i += kNT) {
+                double zi = zk[(size_t)i * kMaxN];
+                const double* zrow = Zs + (size_t)i * kMaxN + j0;
+                for (int q = 0; q < k - j0; ++q) zi = fma(-chq[q], zrow[q], zi);
+                zk[(size_t)i * kMaxN] = zi;
+              }
+            }
+            __syncthreads();
+            double n2 = 0.0;
+            for (int i = tid; i < N; i += kNT) { const double x = zk[(size_t)i * kMaxN]; n2 = fma(x, x, n2); }
+            n2 = warp_sum_d(n2);
+            if (lane == 0) cpart[warp] = n2;
+            __syncthreads();
+            double tot = 0.0;
+            for (int w = 0; w < kNW; ++w) tot += cpart[w];
+            const double inv = (tot > 0.0) ? 1.0 / sqrt(tot) : 0.0;
+            for (int i = tid; i < N; i += kNT) zk[(size_t)i * kMaxN] *= inv;
+            if (tid == 0) pscl[k] = 1.0;
           }
         }
         __syncthreads();
