@@ -224,9 +224,94 @@ __global__ void __launch_bounds__(256) recon_kernel(const Prob* __restrict__ pro
   }
 }
 
+// fp32 reconstruct, register-blocked SGEMM: one CTA per (128-column tile of d,
+// 128-row block of Wt, problem); 256 threads, 8 x 8 outputs each; K (= buffer rows)
+// in steps of 8, double-buffered through registers.  A = Wt (rows j, contiguous
+// k) is transposed into As[k][j] on the store; B = Bf rows (contiguous n).
+__global__ void __launch_bounds__(256, 2) recon128_kernel(const Prob* __restrict__ probs, Params p) {
+  const Prob P = probs[blockIdx.z];
+  const int N = P.rows0 + P.rows1;
+  const int n0 = blockIdx.x * 128, j0 = blockIdx.y * 128;
+  const int jrows = p.ell - 1;
+  if (j0 >= p.ell) return;
+  __shared__ __align__(16) float As[2][8][128 + 4];
+  __shared__ __align__(16) float Bs[2][8][128 + 4];
+  const float* Wt = static_cast<const float*>(P.Wt);
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  // loaders: A: row j0 + (tid >> 1), k-quad 4 * (tid & 1); B: k-row tid >> 5, columns 4 * (tid & 31)
+  const int aj = tid >> 1, ak = 4 * (tid & 1);
+  const int bk = tid >> 5, bn = 4 * (tid & 31);
+  const int ja = j0 + aj;
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+  auto load = [&](int k0, float4& av, float4& bv) {
+    av = make_float4(0.f, 0.f, 0.f, 0.f);
+    bv = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int ka = k0 + ak;
+    if (ja < jrows && ka < N) {
+      av = *reinterpret_cast<const float4*>(Wt + (int64_t)ja * p.ldg + ka);
+      if (ka + 1 >= N) av.y = 0.f;
+      if (ka + 2 >= N) av.z = 0.f;
+      if (ka + 3 >= N) av.w = 0.f;
+    }
+    const int kb = k0 + bk, nb = n0 + bn;
+    if (kb < N && nb < p.ldb) bv = __ldg(reinterpret_cast<const float4*>(prob_row(P, kb, p.ldb) + nb));
+  };
+  auto store = [&](int b, const float4& av, const float4& bv) {
+    As[b][ak + 0][aj] = av.x; As[b][ak + 1][aj] = av.y; As[b][ak + 2][aj] = av.z; As[b][ak + 3][aj] = av.w;
+    *reinterpret_cast<float4*>(&Bs[b][bk][bn]) = bv;
+  };
+  float4 av, bv;
+  load(0, av, bv);
+  store(0, av, bv);
+  __syncthreads();
+  const int nk = (N + 7) / 8;
+  for (int kt = 0; kt < nk; ++kt) {
+    const int b = kt & 1;
+    if (kt + 1 < nk) load(8 * (kt + 1), av, bv);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[b][k][8 * ty]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[b][k][8 * ty + 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[b][k][8 * tx]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[b][k][8 * tx + 4]);
+      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], bb[j], acc[i][j]);
+    }
+    if (kt + 1 < nk) store(b ^ 1, av, bv);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int j = j0 + 8 * ty + i;
+    if (j >= p.ell) continue;
+    const int c = n0 + 8 * tx;
+    float* dst = P.dst + (int64_t)j * p.ldb + c;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (c + 4 * h >= p.ldb) continue;
+      const float4 o = (j < jrows) ? make_float4(acc[i][4 * h], acc[i][4 * h + 1], acc[i][4 * h + 2], acc[i][4 * h + 3])
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(dst + 4 * h) = o;
+    }
+  }
+}
+
 cudaError_t launch_recon(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
   (void)nmax;
+  if (!p.f64 && (p.ldg % 4) == 0) {
+    dim3 grid((unsigned)((p.ldb + 127) / 128), (unsigned)((p.ell + 127) / 128), count);
+    recon128_kernel<<<grid, 256, 0, s>>>(dev_probs, p);
+    return cudaGetLastError();
+  }
   dim3 grid((unsigned)((p.ldb + 63) / 64), (unsigned)((p.ell + 63) / 64), count);
   if (p.f64) recon_kernel<double><<<grid, 256, 0, s>>>(dev_probs, p);
   else recon_kernel<float><<<grid, 256, 0, s>>>(dev_probs, p);
