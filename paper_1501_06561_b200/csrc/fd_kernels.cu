@@ -350,7 +350,8 @@ struct EigCfg {
   static constexpr int kNWc = (PRE ? 256 : kEigThreads) / 32;
   static constexpr size_t kCgs = (size_t)(kNWc * (NM + 1) + NM) * sizeof(double);
   static_assert(PRE || (size_t)kPart * sizeof(T) >= kCgs, "CGS scratch must fit the SYMV workspaces");
-  static constexpr size_t kBytes = kT * sizeof(T) + 4 * NM * sizeof(int) + NM * sizeof(double) + 16 + (PRE ? kCgs : 0);
+  static constexpr size_t kBytes = kT * sizeof(T) + (4 * NM + kNWc * 32) * sizeof(int) + NM * sizeof(double) + 16 +
+                                   (PRE ? kCgs : 0);
 };
 
 __device__ __forceinline__ int pk_off(int c, int N) { return c * N - (c * (c - 1)) / 2; }
@@ -400,13 +401,62 @@ template <> struct Lim<float> {
   static __device__ float tiny() { return FLT_MIN; }
   static __device__ float big() { return FLT_MAX; }
   static constexpr float bits = 27.f;
+  static constexpr float btol = 4e-9f;    // bisection: absolute width / (gu - gl)
+  static constexpr float gspan = 30.f;    // coarse geometric points down to gu 2^-gspan
+  using V2 = float2;
 };
 template <> struct Lim<double> {
   static __device__ double eps() { return DBL_EPSILON; }
   static __device__ double tiny() { return DBL_MIN; }
   static __device__ double big() { return DBL_MAX; }
   static constexpr float bits = 56.f;
+  static constexpr double btol = 1e-17;
+  static constexpr double gspan = 60.0;
+  using V2 = double2;
 };
+
+// Sturm counts (number of eigenvalues < x) of the tridiagonal packed as
+// de[i] = (d_i, e_{i-1}^2): one point, or two interleaved points sharing the loads.
+template <typename T, typename V2>
+__device__ __forceinline__ int sturm1(const V2* __restrict__ de, int N, T x, T pivmin) {
+  T q = de[0].x - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  int cnt = q < T(0);
+#pragma unroll 4
+  for (int i = 1; i < N; ++i) {
+    const V2 v = de[i];
+    q = (v.x - x) - fast_div(v.y, q);
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < T(0);
+  }
+  return cnt;
+}
+template <typename T, typename V2>
+__device__ __forceinline__ void sturm2(const V2* __restrict__ de, int N, T x0, T x1, T pivmin, int& c0, int& c1) {
+  T q0 = de[0].x - x0, q1 = de[0].x - x1;
+  if (fabs(q0) < pivmin) q0 = -pivmin;
+  if (fabs(q1) < pivmin) q1 = -pivmin;
+  int n0 = q0 < T(0), n1 = q1 < T(0);
+#pragma unroll 4
+  for (int i = 1; i < N; ++i) {
+    const V2 v = de[i];
+    q0 = (v.x - x0) - fast_div(v.y, q0);
+    q1 = (v.x - x1) - fast_div(v.y, q1);
+    if (fabs(q0) < pivmin) q0 = -pivmin;
+    if (fabs(q1) < pivmin) q1 = -pivmin;
+    n0 += q0 < T(0);
+    n1 += q1 < T(0);
+  }
+  c0 = n0;
+  c1 = n1;
+}
+
+// coarse bisection points: family 0 linear over (gl, gu), family 1 geometric below gu
+template <typename T>
+__device__ __forceinline__ T coarse_pt(int t, int fam, int H, T gl, T gu) {
+  if (fam == 0) return gl + (gu - gl) * (T)(t + 1) / (T)(H + 1);
+  return gu * (T)exp2((double)(-Lim<T>::gspan * (double)(H - t) / (double)H));
+}
 
 // PRE = true: the lean variant for the tridiagonal-kernel path (p.pretrd): 256
 // threads, small shared memory, several CTAs (problems) per SM.
@@ -443,7 +493,8 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
   int* clen = cstart + NM;
   int* cid = clen + NM;                       // Rayleigh-Ritz cluster list
   int* ord = cid + NM;                        // Ritz-vector order
-  constexpr size_t kOffD = C::kT * sizeof(T) + 4 * NM * sizeof(int);
+  int* ccnt = ord + NM;                       // [kNT] coarse bisection counts
+  constexpr size_t kOffD = C::kT * sizeof(T) + (4 * NM + kNT) * sizeof(int);
   double* pscl = reinterpret_cast<double*>(smraw + kOffD + 8 - (kOffD & 7));  // per-vector scale (fp64)
   double* cpart = PRE ? pscl + NM : reinterpret_cast<double*>(ppart);  // [kNW][kCpStride] block-CGS dots
   double* chq = cpart + kNW * kCpStride; // [NM] projection coefficients
@@ -667,26 +718,62 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
     const T pivmin = red[48];
     const T bnorm = red[49];
     if (N > 0) {
+      using V2 = typename Lim<T>::V2;
+      V2* de = reinterpret_cast<V2*>(vbuf0);   // (d_i, e_{i-1}^2): Householder buffers are idle here
+      for (int i = tid; i < N; i += kNT) {
+        V2 v;
+        v.x = dd[i];
+        v.y = (i > 0) ? e2[i - 1] : T(0);
+        de[i] = v;
+      }
+      __syncthreads();
+      // coarse pass: one Sturm count per thread, kNT/2 linear and kNT/2 geometric points
+      constexpr int H = kNT / 2;
+      const T gl = s_gl, gu = s_gu;
+      ccnt[tid] = sturm1<T, V2>(de, N, coarse_pt<T>(tid % H, tid / H, H, gl, gu), pivmin);
+      __syncthreads();
       int kp = 1;
       while (kp < KC) kp <<= 1;
-      int g = kNT / kp;  // threads per eigenvalue (power of two)
+      int g = kNT / kp;  // threads per eigenvalue (power of two), 2 points each
       if (g > 32) g = 32;
       if (g < 1) g = 1;
       const int j = tid / g, sub = tid % g;
       const unsigned gmask = (g == 32) ? 0xffffffffu : (((1u << g) - 1u) << ((lane / g) * g));
-      T lo = s_gl, hi = s_gu;
-      const int niter = (int)ceilf(Lim<T>::bits / log2f((float)g + 1.f));
-      for (int it = 0; it < niter; ++it) {
-        const T step = (hi - lo) / (T)(g + 1);
-        const T x = lo + step * (T)(sub + 1);
-        const bool below = (j < KC) ? (sturm_count(dd, e2, N, x, pivmin) >= N - j) : false;
-        const unsigned b = __ballot_sync(0xffffffffu, below) & gmask;
-        const int base = (lane / g) * g;
-        const int ss = b ? (__ffs(b) - 1 - base) : g;
-        const T nlo = (ss == 0) ? lo : lo + step * (T)ss;
-        const T nhi = (ss == g) ? hi : lo + step * (T)(ss + 1);
-        lo = nlo;
-        hi = fmax(nhi, nlo);
+      const int base = (lane / g) * g;
+      T lo = gl, hi = gu;
+      if (j < KC) {  // initial bracket from the coarse counts (non-decreasing in each family)
+        const int target = N - j;   // lambda_j (descending index j) is the target-th smallest
+        for (int fam = 0; fam < 2; ++fam) {
+          int a0 = -1, b0 = H;
+          while (b0 - a0 > 1) {
+            const int mid = (a0 + b0) >> 1;
+            if (ccnt[fam * H + mid] >= target) b0 = mid; else a0 = mid;
+          }
+          if (a0 >= 0) lo = fmax(lo, coarse_pt<T>(a0, fam, H, gl, gu));
+          if (b0 < H) hi = fmin(hi, coarse_pt<T>(b0, fam, H, gl, gu));
+        }
+        hi = fmax(hi, lo);
+      }
+      const T tol = (gu - gl) * (T)Lim<T>::btol;
+      const int P = 2 * g;
+      for (int it = 0; it < 96; ++it) {
+        // converged: absolute width tol, or a few ulps of the endpoints (fp resolution)
+        const bool need = (j < KC) && (hi - lo > fmax(tol, T(4) * Lim<T>::eps() * fmax(fabs(lo), fabs(hi))));
+        if (!__syncthreads_or(need)) break;
+        const T step = (hi - lo) / (T)(P + 1);
+        int c0 = 0, c1 = 0;
+        if (need) sturm2<T, V2>(de, N, lo + step * (T)(sub + 1), lo + step * (T)(sub + g + 1), pivmin, c0, c1);
+        const unsigned m0 = __ballot_sync(0xffffffffu, need && c0 >= N - j) & gmask;
+        const unsigned m1 = __ballot_sync(0xffffffffu, need && c1 >= N - j) & gmask;
+        int ss = P;   // first point at or above lambda_j (points 0..g-1 = x0 of sub, g..2g-1 = x1)
+        if (m0) ss = __ffs(m0) - 1 - base;
+        else if (m1) ss = __ffs(m1) - 1 - base + g;
+        if (need) {
+          const T nlo = (ss == 0) ? lo : lo + step * (T)ss;
+          const T nhi = (ss == P) ? hi : lo + step * (T)(ss + 1);
+          lo = nlo;
+          hi = fmax(nhi, nlo);
+        }
       }
       if (sub == 0 && j < KC) lam[j] = fmax(T(0.5) * (lo + hi), T(0));  // clamp (reading C8)
     }
