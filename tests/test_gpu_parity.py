@@ -172,6 +172,15 @@ def test_parity_c5_scaled_perrow():
         check_parity(A, 32, v)
 
 
+def test_parity_c5_fullsize_perrow():
+    """Config 5 at full size (n = 200 000, d = 256, drifting subspaces), per-row FD,
+    ell = 32, P = 8 shard streams (25 000 dependent ReduceRanks each) + merge tree:
+    the whole sketch against the oracle run with the same DAG."""
+    w = fdgen.config("c5")
+    A = fdgen.host_rows(w)
+    check_parity(A, 32, "fd", n_shards=8)
+
+
 def test_evaluator_parity_same_B():
     """GPU evaluator vs oracle evaluator on identical (A, B_oracle): relative 1e-6 (C12 iii)."""
     for cfg, ell, v in (("c1", 16, "fd"), ("c2", 20, "fast_fd")):
