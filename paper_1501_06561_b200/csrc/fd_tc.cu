@@ -181,25 +181,27 @@ static cudaError_t launch_gram_tc_t(const Prob* dev_probs, int count, const Para
 }
 
 // ---------------------------------------------------------------------------
-// EXPERIMENTAL (opt-in, FD_TC_RECON=1): the tensor core's fp32 accumulation
-// truncates, which shrinks the reconstructed rows by ~1e-6 per ReduceRank; fed
-// back through the retained rows this compounds (cov-err bias ~2e-3 relative on
-// c2 after ~100 rounds), so the default reconstruct is FP32 SIMT.
-// Reconstruct B' = Wt Bf (rows 0..ell-2; row ell-1 = 0), Wt: (ell-1) x N (ldg),
-// Bf: N x d rows of the problem (ldb).  M = 128 (ell-1 <= 127), N-tiles of 256
-// columns of d, K = N in 32-row chunks.  Both operands K-major SW128: A = Wt rows;
-// B = Bf^T, transposed while staging (each thread loads an 8 (k) x 4 (n) block of
-// Bf with four coalesced 16-B loads per k-row and stores, per column n, the 8
-// k-values as two 16-B chunks).
+// Reconstruct B' = Wt Bf (rows 0..ell-2; row ell-1 = 0) on tcgen05, 3xTF32.
+// Wt: (ell-1) x N (ldg), Bf: N x d rows of the problem (ldb).  M = 128 (ell-1 <=
+// 127), N-tiles of 128 columns of d, K = N in 32-row chunks; both operands K-major
+// SW128 (A = Wt rows; B = Bf^T, transposed while staging).
+//
+// Accuracy: the tensor core's fp32 accumulation truncates (~0.5 ulp per MMA step).
+// Accumulating all K = 256 in TMEM shrinks every reconstructed row by ~1e-6 per
+// ReduceRank, which compounds through the retained rows.  Here each
+// 32-row chunk accumulates into fresh TMEM partials (hi.hi and the small cross
+// terms apart: 4 and 8 steps), double-buffered, and the partials are drained into
+// fp32 register running sums (round-to-nearest adds) while the next chunk's MMAs
+// run.  Warps w and w+4 share TMEM lanes 32 (w % 4).. and split the 128 columns.
 // ---------------------------------------------------------------------------
 namespace {
 constexpr int kRA = 128 * 128;      // A tile bytes (128 rows x 32 values)
-constexpr int kRB = 256 * 128;      // B tile bytes (256 rows (n) x 32 values (k))
+constexpr int kRB = 128 * 128;      // B tile bytes (128 rows (n) x 32 values (k))
 constexpr int kRStage = 2 * kRA + 2 * kRB;
 
 struct ReconRegs {
   float4 a[4];   // A: 128 rows x 8 float4 = 1024 items / 256 threads
-  float4 b[8];   // B: k-rows 8g..8g+7 of columns n0 + 4q .. +3 (q = tid & 63, g = tid >> 6)
+  float4 b[4];   // B: k-rows 4g..4g+3 of columns n0 + 4q .. +3 (q = tid & 31, g = tid >> 5)
 };
 
 __device__ __forceinline__ void recon_load(const Prob& P, const Params& p, int N, int jrows, int kc, int n0,
@@ -219,11 +221,11 @@ __device__ __forceinline__ void recon_load(const Prob& P, const Params& p, int N
     }
     R.a[j] = v;
   }
-  const int q = threadIdx.x & 63, g = threadIdx.x >> 6;
+  const int q = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int64_t n = n0 + 4 * q;
 #pragma unroll
-  for (int kk = 0; kk < 8; ++kk) {
-    const int k = kc * 32 + 8 * g + kk;
+  for (int kk = 0; kk < 4; ++kk) {
+    const int k = kc * 32 + 4 * g + kk;
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     if (k < N && n < p.ldb) v = __ldg(reinterpret_cast<const float4*>(row_ptr(P, k, p.ldb) + n));
     R.b[kk] = v;
@@ -255,14 +257,11 @@ __device__ __forceinline__ void recon_store(unsigned char* st, const ReconRegs& 
     const int r = it >> 3, c4 = it & 7;
     st_split(ahi, alo, tc::sw128_off(r, 4 * c4), R.a[j]);
   }
-  const int q = threadIdx.x & 63, g = threadIdx.x >> 6;
+  const int q = threadIdx.x & 31, g = threadIdx.x >> 5;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    const int n = 4 * q + e;
-    const float4 v0 = make_float4(comp(R.b[0], e), comp(R.b[1], e), comp(R.b[2], e), comp(R.b[3], e));
-    const float4 v1 = make_float4(comp(R.b[4], e), comp(R.b[5], e), comp(R.b[6], e), comp(R.b[7], e));
-    st_split(bhi, blo, tc::sw128_off(n, 8 * g), v0);
-    st_split(bhi, blo, tc::sw128_off(n, 8 * g + 4), v1);
+    const float4 v = make_float4(comp(R.b[0], e), comp(R.b[1], e), comp(R.b[2], e), comp(R.b[3], e));
+    st_split(bhi, blo, tc::sw128_off(4 * q + e, 4 * g), v);
   }
 }
 }  // namespace
@@ -284,90 +283,86 @@ __global__ void __launch_bounds__(kTcThreads, 1) recon_tc_kernel(const Prob* __r
   tc::fence_after_sync();
   const uint32_t tbase = s_tmem;
   uint32_t uses[2] = {0, 0};
-  const uint32_t idesc = tc::idesc_tf32(128, 256, 0, 0);
+  const uint32_t idesc = tc::idesc_tf32(128, 128, 0, 0);
   const int ell = p.ell, jrows = ell - 1;
+  // TMEM: partials of chunk parity b: hi.hi at 128 b, cross terms at 256 + 128 b
+  const uint32_t lanebase = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
+  const int half = warp >> 2;                    // columns 64 half .. 64 half + 63 of the tile
+  const int m = 32 * (warp & 3) + lane;          // tile row (= TMEM lane)
 
   for (int pi = blockIdx.x; pi < count; pi += gridDim.x) {
     const Prob P = probs[pi];
     const int N = P.rows0 + P.rows1;
     const int nk = (N + 31) / 32;
-    for (int n0 = 0; n0 < p.ldb; n0 += 256) {
+    for (int n0 = 0; n0 < p.ldb; n0 += 128) {
+      float acc[64];
+#pragma unroll
+      for (int c = 0; c < 64; ++c) acc[c] = 0.f;
       ReconRegs R;
       recon_load(P, p, N, jrows, 0, n0, R);
       recon_store(sm, R);
       tc::fence_async_smem();
       __syncthreads();
-      for (int kc = 0; kc < nk; ++kc) {
+      for (int kc = 0; kc <= nk; ++kc) {
         const int b = kc & 1;
-        if (tid == 0) {
+        if (kc < nk && tid == 0) {
           tc::fence_after_sync();
           unsigned char* st = sm + b * kRStage;
           const uint32_t ahi = tc::smem_u32(st), alo = tc::smem_u32(st + kRA);
           const uint32_t bhi = tc::smem_u32(st + 2 * kRA), blo = tc::smem_u32(st + 2 * kRA + kRB);
+          const uint32_t thh = tbase + 128 * b, tx = tbase + 256 + 128 * b;
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
-            const uint32_t acc = (kc > 0 || ks > 0) ? 1u : 0u;
             const uint32_t ka = ks * 32;
-            // hi.hi and the small cross terms go to separate accumulators: the tensor
-            // core's fp32 accumulation truncates, so fewer steps on the large one
-            // means less bias (summed with round-to-nearest in the epilogue)
-            tc::mma_tf32(tbase, tc::desc_k_sw128(ahi + ka), tc::desc_k_sw128(bhi + ka), idesc, acc);
-            tc::mma_tf32(tbase + 256, tc::desc_k_sw128(ahi + ka), tc::desc_k_sw128(blo + ka), idesc, acc);
-            tc::mma_tf32(tbase + 256, tc::desc_k_sw128(alo + ka), tc::desc_k_sw128(bhi + ka), idesc, 1u);
+            tc::mma_tf32(thh, tc::desc_k_sw128(ahi + ka), tc::desc_k_sw128(bhi + ka), idesc, ks > 0 ? 1u : 0u);
+            tc::mma_tf32(tx, tc::desc_k_sw128(ahi + ka), tc::desc_k_sw128(blo + ka), idesc, ks > 0 ? 1u : 0u);
+            tc::mma_tf32(tx, tc::desc_k_sw128(alo + ka), tc::desc_k_sw128(bhi + ka), idesc, 1u);
           }
           tc::commit(&mbar[b]);
         }
-        if (kc + 1 < nk) {
-          recon_load(P, p, N, jrows, kc + 1, n0, R);
-          const int nb = b ^ 1;
-          if (kc >= 1) {
-            tc::mbar_wait(&mbar[nb], uses[nb] & 1);
-            ++uses[nb];
+        if (kc + 1 < nk) recon_load(P, p, N, jrows, kc + 1, n0, R);
+        if (kc >= 1) {
+          // chunk kc-1: MMAs complete -> drain its partials, its smem stage is free
+          const int pb = b ^ 1;
+          tc::mbar_wait(&mbar[pb], uses[pb] & 1);
+          ++uses[pb];
+          tc::fence_after_sync();
+#pragma unroll
+          for (int c0 = 0; c0 < 64; c0 += 16) {
+            float vh[16], vx[16];
+            tc::tmem_ld16(lanebase + 128 * pb + 64 * half + c0, vh);
+            tc::tmem_ld16(lanebase + 256 + 128 * pb + 64 * half + c0, vx);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) acc[c0 + q] += vh[q] + vx[q];
           }
-          recon_store(sm + nb * kRStage, R);
+        }
+        if (kc + 1 < nk) {
+          recon_store(sm + (b ^ 1) * kRStage, R);
           tc::fence_async_smem();
         }
+        tc::fence_before_sync();
         __syncthreads();
       }
-      {
-        const int bl = (nk - 1) & 1;
-        if (nk >= 2) { tc::mbar_wait(&mbar[bl ^ 1], uses[bl ^ 1] & 1); ++uses[bl ^ 1]; }
-        tc::mbar_wait(&mbar[bl], uses[bl] & 1);
-        ++uses[bl];
-      }
-      tc::fence_after_sync();
-      if (warp < 4) {
-        const int m = 32 * warp + lane;
-        const uint32_t lanebase = tbase + ((uint32_t)(32 * warp) << 16);
-        for (int c0 = 0; c0 < 256; c0 += 16) {
-          float v[16], vs[16];
-          tc::tmem_ld16(lanebase + c0, v);
-          tc::tmem_ld16(lanebase + 256 + c0, vs);
+      // epilogue: row m, columns n0 + 64 half .. +63
+      if (m < ell) {
+        float* dst = P.dst + (int64_t)m * p.ldb + n0 + 64 * half;
 #pragma unroll
-          for (int q = 0; q < 16; ++q) v[q] += vs[q];
-          if (m < ell) {
-            float* dst = P.dst + (int64_t)m * p.ldb + n0 + c0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              if (n0 + c0 + 4 * q + 4 <= p.ldb) {
-                const float4 o = (m < jrows) ? make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3])
-                                             : make_float4(0.f, 0.f, 0.f, 0.f);
-                *reinterpret_cast<float4*>(dst + 4 * q) = o;
-              }
-            }
+        for (int q = 0; q < 16; ++q) {
+          if (n0 + 64 * half + 4 * q + 4 <= p.ldb) {
+            const float4 o = (m < jrows) ? make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3])
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+            *reinterpret_cast<float4*>(dst + 4 * q) = o;
           }
         }
       }
-      tc::fence_before_sync();
-      __syncthreads();
     }
-    __syncthreads();
   }
+  __syncthreads();
   if (warp == 0) tc::tmem_dealloc(tbase, 512);
 }
 
 bool recon_tc_supported(int nmax, const Params& p) {
-  return !p.f64 && p.ell - 1 <= 128 && nmax >= 1 && nmax <= 1024 && (p.ldg % 4) == 0;
+  return !p.f64 && p.ell - 1 <= 128 && nmax >= 1 && nmax <= 1024 && (p.ldg % 4) == 0 && (p.ldb % 4) == 0;
 }
 
 cudaError_t launch_recon_tc(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s) {
