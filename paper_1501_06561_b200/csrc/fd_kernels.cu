@@ -323,7 +323,7 @@ cudaError_t launch_recon(const Prob* dev_probs, int count, int nmax, const Param
 // problems), precision T, max size NM.
 // ============================================================================
 constexpr int kNW = kEigThreads / 32;  // 16 warps
-constexpr int kEigPreCtasPerSM = 3;     // resident CTAs of the lean (tridiagonal-input) variant
+constexpr int kEigPreCtasPerSM = 4;     // resident CTAs of the lean (tridiagonal-input) variant
 constexpr int kSmallCl = 8;             // clusters up to this size: warp MGS; larger: block CGS2
 // fp64 scratch per CTA slot (stride zld): LDL^T factors and Z (element-major
 // [i][j], zld x zld each), a Rayleigh-Ritz copy region, then, for problems above
@@ -461,7 +461,7 @@ __device__ __forceinline__ T coarse_pt(int t, int fam, int H, T gl, T gu) {
 // PRE = true: the lean variant for the tridiagonal-kernel path (p.pretrd): 256
 // threads, small shared memory, several CTAs (problems) per SM.
 template <typename T, int NM, bool GAPK, bool PRE = false>
-__global__ void __launch_bounds__(PRE ? 256 : kEigThreads, PRE ? 3 : 1)
+__global__ void __launch_bounds__(PRE ? 256 : kEigThreads, PRE ? kEigPreCtasPerSM : 1)
 eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restrict__ scratch) {
   using C = EigCfg<T, NM, GAPK, PRE>;
   constexpr int kNT = PRE ? 256 : kEigThreads;   // threads
