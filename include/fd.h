@@ -114,6 +114,19 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
  * STATE, CUDA. */
 fd_status fd_append_rows(fd_handle* h, const float* rows, int64_t n_rows, int64_t ld);
 
+/* Append n_rows rows that live in HOST memory (row stride ld elements;
+ * host_rows should be page-locked for the copies to overlap).  Same semantics
+ * and shard split as fd_append_rows (Alg. 1 row loop; reading
+ * C10): each lockstep round's rows are copied host -> device into `stage`
+ * [device] (one 2-D copy per run of equally sized shard chunks, on an internal
+ * copy stream) while the previous round computes.  stage_bytes >=
+ * fd_host_stage_bytes(cfg, ld).  host_rows must stay valid and unmodified until
+ * the handle's stream passes this call.  Errors: as fd_append_rows, plus
+ * WORKSPACE (stage too small). */
+size_t fd_host_stage_bytes(const fd_config* cfg, int64_t ld);
+fd_status fd_append_rows_host(fd_handle* h, const float* host_rows, int64_t n_rows, int64_t ld, void* stage,
+                              size_t stage_bytes);
+
 /* Snapshot sketch (non-destructive; appends may continue, reading C9): every
  * shard's buffer gets one more ReduceRank (Alg. 1 "return B = B_[n]" with the
  * final shrink of C9), then the P shard sketches are merged pairwise

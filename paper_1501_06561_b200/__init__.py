@@ -64,21 +64,28 @@ class Sketcher:
         check(lib().fd_create(ctypes.byref(self.cfg), self.ws.data_ptr(), nbytes, self.stream.cuda_stream,
                               ctypes.byref(h)))
         self.h = h
-        self._keep = []  # host->device staging copies kept alive until the next sync point
+        self._keep = []  # host inputs kept alive until the next sync point
+        self._stage = None  # device staging buffer of fd_append_rows_host
 
     # -- streaming ---------------------------------------------------------
     def append(self, rows):
-        """Append rows (n x d fp32).  Device tensors are read in place (async);
-        host tensors are copied to the device first (pinned -> async H2D)."""
+        """Append rows (n x d fp32).  Device tensors are read in place (async).
+        Host tensors go through fd_append_rows_host: each lockstep round's rows
+        are copied host -> device into a staging buffer while the previous round
+        computes (pin the host tensor for the copies to overlap)."""
         torch = _torch()
         rows = _as_rows(rows, self.d)
         if rows.shape[0] == 0:
             return self
         if not rows.is_cuda:
-            with torch.cuda.stream(self.stream):
-                dev = rows.to(self.device, non_blocking=True)
-            self._keep.append(dev)
-            rows = dev
+            ld = rows.stride(0)
+            nbytes = lib().fd_host_stage_bytes(ctypes.byref(self.cfg), ld)
+            if self._stage is None or self._stage.numel() < nbytes:
+                self._stage = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            self._keep.append(rows)   # must outlive the asynchronous copies
+            check(lib().fd_append_rows_host(self.h, rows.data_ptr(), rows.shape[0], ld, self._stage.data_ptr(),
+                                            self._stage.numel()))
+            return self
         check(lib().fd_append_rows(self.h, rows.data_ptr(), rows.shape[0], rows.stride(0)))
         return self
 
@@ -133,6 +140,7 @@ class Sketcher:
             lib().fd_destroy(self.h)
             self.h = None
             self.ws = None
+            self._stage = None
 
     def __del__(self):
         try:

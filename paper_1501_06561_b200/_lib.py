@@ -22,7 +22,7 @@ FD_MAX_N = 416
 
 # every symbol include/fd.h declares (checked by tests/test_abi.py)
 EXPORTS = [
-    "fd_workspace_bytes", "fd_create", "fd_append_rows", "fd_sketch", "fd_merge", "fd_shard_sketch",
+    "fd_workspace_bytes", "fd_create", "fd_append_rows", "fd_host_stage_bytes", "fd_append_rows_host", "fd_sketch", "fd_merge", "fd_shard_sketch",
     "fd_destroy", "fd_reset", "fd_profile", "fd_profile_read", "fd_cov_workspace_bytes", "fd_cov_gram_partial", "fd_cov_err_from_gram", "fd_cov_err",
     "fd_last_error", "fd_version",
 ]
@@ -62,6 +62,9 @@ def lib():
         L.fd_workspace_bytes.restype = sz
         L.fd_create.argtypes = [ctypes.POINTER(FdConfig), vp, sz, vp, ctypes.POINTER(vp)]
         L.fd_append_rows.argtypes = [vp, vp, i64, i64]
+        L.fd_host_stage_bytes.argtypes = [ctypes.POINTER(FdConfig), i64]
+        L.fd_host_stage_bytes.restype = sz
+        L.fd_append_rows_host.argtypes = [vp, vp, i64, i64, vp, sz]
         L.fd_sketch.argtypes = [vp, vp, ctypes.POINTER(FdStats)]
         L.fd_merge.argtypes = [vp, vp, i32, vp, ctypes.POINTER(FdStats)]
         L.fd_shard_sketch.argtypes = [vp, i32, vp]
@@ -75,7 +78,7 @@ def lib():
         L.fd_cov_gram_partial.argtypes = [vp, i64, i64, i64, vp, vp, sz, vp]
         L.fd_cov_err_from_gram.argtypes = [vp, vp, i32, i64, dbl, dp, dp, dp, vp, sz, vp]
         L.fd_cov_err.argtypes = [vp, i64, i64, vp, i32, i64, dp, dp, dp, vp, sz, vp]
-        for f in ("fd_create", "fd_append_rows", "fd_sketch", "fd_merge", "fd_shard_sketch", "fd_destroy",
+        for f in ("fd_create", "fd_append_rows", "fd_append_rows_host", "fd_sketch", "fd_merge", "fd_shard_sketch", "fd_destroy",
                   "fd_reset", "fd_profile",
                   "fd_cov_gram_partial", "fd_cov_err_from_gram", "fd_cov_err"):
             getattr(L, f).restype = ctypes.c_int

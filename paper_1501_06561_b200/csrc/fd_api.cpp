@@ -137,6 +137,8 @@ struct fd_handle {
   char* arena;        // device descriptor arena (2 halves)
   char* host_arena;   // pinned host mirror
   cudaEvent_t ev[2];
+  cudaStream_t copy_stream;     // host-input staging (fd_append_rows_host)
+  cudaEvent_t ev_copied[2], ev_consumed[2];
   int half;
   size_t half_used;
   std::vector<int> occ, cur;
@@ -403,6 +405,12 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
   if (e == cudaSuccess) e = cudaMallocHost(&h->host_arena, 2 * kArenaHalf);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev[0], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev[1], cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking);
+  for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+    e = cudaEventCreateWithFlags(&h->ev_copied[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_consumed[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(h->ev_consumed[k], h->stream);
+  }
   if (e == cudaSuccess) e = cudaEventRecord(h->ev[0], h->stream);
   if (e == cudaSuccess) e = cudaEventRecord(h->ev[1], h->stream);
   // zero the shard buffers' statistics and the flag
@@ -417,7 +425,14 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
   return FD_OK;
 }
 
-fd_status fd_append_rows(fd_handle* h, const float* rows, int64_t n_rows, int64_t ld) {
+// Round loop shared by the device- and host-input appends.  Every call's rows are
+// split into P contiguous ranges (reading C10); each round ingests the next
+// min(L - occ, remaining) rows of every shard, then runs one batched ReduceRank
+// over the shards whose buffer filled.  For host input the rows of round k are
+// staged to the device (one 2-D copy per run of equally sized, equally spaced
+// shard chunks) on the copy stream while round k-1 computes.
+static fd_status append_impl(fd_handle* h, const float* rows, int64_t n_rows, int64_t ld, bool host, float* stage,
+                             size_t stage_bytes) {
   if (!h) return fail(FD_ERR_INVALID_ARG, "handle is NULL");
   if (h->dead) return fail(FD_ERR_STATE, "handle refuses work after a sticky error");
   if (n_rows < 0) return fail(FD_ERR_INVALID_ARG, "n_rows < 0");
@@ -425,7 +440,9 @@ fd_status fd_append_rows(fd_handle* h, const float* rows, int64_t n_rows, int64_
   if (!rows) return fail(FD_ERR_INVALID_ARG, "rows is NULL");
   if (ld < h->D.d) return fail(FD_ERR_SHAPE, "ld < d");
   const int P = h->D.P, L = h->D.L, ell = h->D.ell;
-  // contiguous ranges of this call (reading C10)
+  const size_t slot_floats = (size_t)P * L * ld;
+  if (host && (!stage || stage_bytes < 2 * slot_floats * sizeof(float)))
+    return fail(FD_ERR_WORKSPACE, "host staging buffer smaller than fd_host_stage_bytes()");
   const int64_t q = n_rows / P, r = n_rows % P;
   std::vector<int64_t> start(P), rem(P);
   int64_t off = 0;
@@ -434,6 +451,50 @@ fd_status fd_append_rows(fd_handle* h, const float* rows, int64_t n_rows, int64_
     rem[s] = q + (s < r ? 1 : 0);
     off += rem[s];
   }
+  // plan of one round: (shard, first row, count)
+  struct Chunk { int s; int64_t row; int c; };
+  auto plan_round = [&](std::vector<int>& occ, std::vector<int64_t>& st, std::vector<int64_t>& rm,
+                        std::vector<Chunk>& out) {
+    out.clear();
+    for (int s = 0; s < P; ++s) {
+      if (rm[s] == 0) continue;
+      const int c = (int)std::min<int64_t>(L - occ[s], rm[s]);
+      out.push_back({s, st[s], c});
+      st[s] += c;
+      rm[s] -= c;
+      occ[s] += c;
+      if (occ[s] == L) occ[s] = ell - 1;
+    }
+  };
+  // host staging: copy the chunks of a round into stage slot k (chunk i at i * maxc * ld)
+  auto stage_round = [&](const std::vector<Chunk>& ch, int slot) -> fd_status {
+    int maxc = 0;
+    for (const Chunk& c : ch) maxc = std::max(maxc, c.c);
+    float* base = stage + (size_t)slot * slot_floats;
+    FD_CUDA(cudaStreamWaitEvent(h->copy_stream, h->ev_consumed[slot], 0));
+    size_t i = 0;
+    while (i < ch.size()) {
+      size_t j = i + 1;
+      const int64_t delta = (j < ch.size()) ? ch[j].row - ch[i].row : 0;
+      while (j < ch.size() && ch[j].c == ch[i].c && ch[j].row - ch[j - 1].row == delta) ++j;
+      const size_t cnt = j - i;
+      const size_t width = (size_t)ch[i].c * ld * sizeof(float);
+      const size_t spitch = (cnt > 1) ? (size_t)delta * ld * sizeof(float) : width;
+      FD_CUDA(cudaMemcpy2DAsync(base + i * (size_t)maxc * ld, (size_t)maxc * ld * sizeof(float), rows + ch[i].row * ld,
+                                spitch, width, cnt, cudaMemcpyHostToDevice, h->copy_stream));
+      i = j;
+    }
+    FD_CUDA(cudaEventRecord(h->ev_copied[slot], h->copy_stream));
+    return FD_OK;
+  };
+  std::vector<int> pocc = h->occ;   // planning copies (host staging runs one round ahead)
+  std::vector<int64_t> pst = start, prm = rem;
+  std::vector<Chunk> cur_ch, next_ch;
+  int round = 0;
+  if (host) {
+    plan_round(pocc, pst, prm, cur_ch);
+    if (!cur_ch.empty()) { fd_status e0 = stage_round(cur_ch, 0); if (e0 != FD_OK) return e0; }
+  }
   std::vector<Ingest> ing;
   std::vector<Prob> probs;
   ing.reserve(P);
@@ -441,17 +502,21 @@ fd_status fd_append_rows(fd_handle* h, const float* rows, int64_t n_rows, int64_
   for (;;) {
     ing.clear();
     probs.clear();
+    int maxc = 0;
+    if (host) for (const Chunk& c : cur_ch) maxc = std::max(maxc, c.c);
+    int ci = 0;
     for (int s = 0; s < P; ++s) {
       if (rem[s] == 0) continue;
       const int c = (int)std::min<int64_t>(L - h->occ[s], rem[s]);
       Ingest g;
-      g.src = rows + start[s] * ld;
+      g.src = host ? stage + (size_t)(round & 1) * slot_floats + (size_t)ci * maxc * ld : rows + start[s] * ld;
       g.ld = ld;
       g.dst = shard_buf(h, s, h->cur[s]) + (size_t)h->occ[s] * h->D.ldb;
       g.nrows = c;
       g.pad = 0;
       g.stats = h->stats + s;
       ing.push_back(g);
+      ++ci;
       start[s] += c;
       rem[s] -= c;
       h->occ[s] += c;
@@ -464,17 +529,42 @@ fd_status fd_append_rows(fd_handle* h, const float* rows, int64_t n_rows, int64_
       }
     }
     if (ing.empty()) break;
+    if (host) {
+      // stage the next round while this one computes
+      plan_round(pocc, pst, prm, next_ch);
+      if (!next_ch.empty()) { fd_status e1 = stage_round(next_ch, (round + 1) & 1); if (e1 != FD_OK) return e1; }
+      FD_CUDA(cudaStreamWaitEvent(h->stream, h->ev_copied[round & 1], 0));
+    }
     const Ingest* di = nullptr;
     fd_status st = push_desc(h, ing, &di);
     if (st != FD_OK) return st;
     const int ni = (int)ing.size();
     cudaError_t e = timed(h, K_INGEST, [&] { return fdk::launch_ingest(di, ni, h->prm, h->flag, h->stream); });
     if (e != cudaSuccess) return cuda_fail(e, "ingest");
+    if (host) FD_CUDA(cudaEventRecord(h->ev_consumed[round & 1], h->stream));
     st = run_reduce(h, probs);
     if (st != FD_OK) return st;
+    if (host) cur_ch.swap(next_ch);
+    ++round;
   }
   h->rows_seen += n_rows;
   return FD_OK;
+}
+
+fd_status fd_append_rows(fd_handle* h, const float* rows, int64_t n_rows, int64_t ld) {
+  return append_impl(h, rows, n_rows, ld, false, nullptr, 0);
+}
+
+size_t fd_host_stage_bytes(const fd_config* cfg, int64_t ld) {
+  Derived D;
+  std::string why;
+  if (!derive(cfg, &D, &why) || ld < D.d) return 0;
+  return 2 * (size_t)D.P * D.L * ld * sizeof(float);
+}
+
+fd_status fd_append_rows_host(fd_handle* h, const float* host_rows, int64_t n_rows, int64_t ld, void* stage,
+                              size_t stage_bytes) {
+  return append_impl(h, host_rows, n_rows, ld, true, static_cast<float*>(stage), stage_bytes);
 }
 
 fd_status fd_sketch(fd_handle* h, float* B_out, fd_stats* st) {
@@ -573,6 +663,8 @@ fd_status fd_destroy(fd_handle* h) {
   for (auto e : h->pool) cudaEventDestroy(e);
   cudaEventDestroy(h->ev[0]);
   cudaEventDestroy(h->ev[1]);
+  for (int k = 0; k < 2; ++k) { cudaEventDestroy(h->ev_copied[k]); cudaEventDestroy(h->ev_consumed[k]); }
+  cudaStreamDestroy(h->copy_stream);
   cudaFreeHost(h->host_arena);
   delete h;
   return FD_OK;

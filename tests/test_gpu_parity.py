@@ -308,6 +308,27 @@ def test_snapshot_is_non_destructive():
     assert spec_norm(Bn.T @ Bn - r.B.T @ r.B) <= SKETCH_TOL * r.frob_sq
 
 
+def test_host_input_append_matches_device_input():
+    """fd_append_rows_host (staged, copy/compute overlapped) computes the same DAG as
+    fd_append_rows on device rows: identical sketches and statistics."""
+    m = fd()
+    A = _c2()
+    for variant, P, apps in (("fast_fd", 7, [3001, 6999]), ("alpha_fd", 2, [10000]), ("fast_isvd", 1, [5, 9995])):
+        outs = []
+        for host in (False, True):
+            sk = m.Sketcher(A.shape[1], 40, variant, n_shards=P)
+            src = torch.from_numpy(A).pin_memory() if host else torch.from_numpy(A).cuda()
+            o = 0
+            for a in apps:
+                sk.append(src[o:o + a])
+                o += a
+            B, st = sk.sketch()
+            outs.append((B.cpu().numpy(), st))
+            sk.close()
+        assert np.array_equal(outs[0][0], outs[1][0]), variant
+        assert outs[0][1] == outs[1][1], variant
+
+
 def test_merge_api_matches_oracle_tree():
     A = fdgen.host_rows(fdgen.config("c1"))
     r = oracle.sketch(A, 16, "fast_fd", n_shards=5, want_shards=True)
