@@ -4,7 +4,7 @@
 Workload (BASELINE.json config 4, the largest single-GPU configuration and the
 one north_star's >=60% roofline / >=75% scaling targets are read on):
     noisy low-rank stream n = 8,388,608 rows, d = 1024, k = 64, zeta = 10 (32 GiB fp32),
-    ell = 128, Fast FD (2*ell buffer), P_total = 1184 shard streams (8 x 148),
+    ell = 128, Fast FD (2*ell buffer), P_total = 2368 shard streams (16 x 148; 296 per GPU at 8 GPUs),
     rows split evenly across the N GPUs (strong scaling; the shard DAG depends on
     P_total only, so every N computes the same sketch), per-GPU sketches
     all-gathered (NCCL) and tree-merged.
@@ -32,7 +32,7 @@ sys.path.insert(0, ROOT)
 METRIC = "rows/sec sketched (fp32, ell given) at 1/2/4/8 B200 + % roofline; cov err"
 WORKLOADS = {
     # name: (fdgen config, ell, default variant, P_total)
-    "c4": ("c4", 128, "fast_fd", 1184),
+    "c4": ("c4", 128, "fast_fd", 2368),
     "c2": ("c2", 100, "fast_fd", 8),
     "c1": ("c1", 16, "fast_fd", 8),
 }
@@ -232,6 +232,7 @@ def run_ours(args):
     wl = args.workload
     cfgname, ell, variant, P = WORKLOADS[wl]
     variant = args.variant or variant
+    P = args.shards or P
     if P % world:
         raise SystemExit(f"P_total={P} not divisible by world={world}")
     w = fdgen.config(cfgname)
@@ -412,6 +413,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--variant", default=None)
+    ap.add_argument("--shards", type=int, default=None, help="P_total shard streams (default: the workload's)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

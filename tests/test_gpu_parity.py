@@ -345,7 +345,7 @@ def test_merge_api_matches_oracle_tree():
 # ---------------------------------------------------------------------------
 # full-size c4 at the bench launch configuration: properties + sampled shards
 # ---------------------------------------------------------------------------
-C4_SHARDS = 1184
+C4_SHARDS = 2368
 
 
 def test_c4_fullsize_bench_config():
@@ -360,7 +360,7 @@ def test_c4_fullsize_bench_config():
     B, st = sk.sketch()
     # sampled shard parity: shard s's rows through the oracle (one by one)
     q, rr = divmod(w.n, C4_SHARDS)
-    picks = [0, 593, C4_SHARDS - 1]
+    picks = [0, 1187, C4_SHARDS - 1]
 
     def one(s):
         start = s * q + min(s, rr)

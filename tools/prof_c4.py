@@ -10,7 +10,7 @@ w = fdgen.config("c4")
 gen = fdgen.DeviceGenerator(w)
 A = torch.empty((w.n, w.d), dtype=torch.float32, device="cuda")
 gen.fill(A)
-sk = m.Sketcher(w.d, 128, "fast_fd", n_shards=1184)
+sk = m.Sketcher(w.d, 128, "fast_fd", n_shards=2368)
 sk.append(A)
 B, st = sk.sketch()
 torch.cuda.synchronize()
