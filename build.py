@@ -66,9 +66,10 @@ def build_libfd(force=False):
     if not cu:
         return None
     if force or _stale(out, srcs):
+        extra = os.environ.get("FD_NVCC_EXTRA", "").split()   # e.g. -DFD_INV_ITERS=2 (A/B builds)
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
               "-Xptxas", "-v" if os.environ.get("FD_PTXAS_V") else "-O3",
-              "-I", os.path.join(ROOT, "include"), "-I", os.path.join(pkg, "csrc"),
+              "-I", os.path.join(ROOT, "include"), "-I", os.path.join(pkg, "csrc"), *extra,
               "-o", out, *cu])
     return out
 

@@ -325,6 +325,20 @@ cudaError_t launch_recon(const Prob* dev_probs, int count, int nmax, const Param
 constexpr int kNW = kEigThreads / 32;  // 16 warps
 constexpr int kEigPreCtasPerSM = 4;     // resident CTAs of the lean (tridiagonal-input) variant
 constexpr int kSmallCl = 8;             // clusters up to this size: warp MGS; larger: block CGS2
+#ifndef FD_INV_ITERS
+#define FD_INV_ITERS 2
+#endif
+constexpr int kInvIters = FD_INV_ITERS;  // inverse-iteration sweeps (2: same parity as 3)
+
+// fp64 reciprocal: fp32 estimate + two Newton steps (each squares the ~6e-8
+// relative error of the estimate), cheaper than the IEEE division.
+__device__ __forceinline__ double rcp_d(double x) {
+  if (!(fabs(x) > 1e-30 && fabs(x) < 1e30)) return 1.0 / x;   // outside the fp32 estimate's range
+  double r = (double)__frcp_rn((float)x);
+  r = r * fma(-x, r, 2.0);
+  r = r * fma(-x, r, 2.0);
+  return r;
+}
 // fp64 scratch per CTA slot (stride zld): LDL^T factors and Z (element-major
 // [i][j], zld x zld each), a Rayleigh-Ritz copy region, then, for problems above
 // kMaxNS, the packed matrix (global / L2 instead of shared memory).
@@ -858,7 +872,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
       double* lf = LF + j;   // lf[i * kMaxN]  multipliers of L
       double* z = Zs + j;    // z[i * kMaxN]
       double sc = 1.0;
-      for (int it = 0; it < 3; ++it) {
+      for (int it = 0; it < kInvIters; ++it) {
         if (act) {
           // L D L^T = T - mu I (tiny pivots perturbed), recomputed every iteration and
           // fused with the forward solve L u = b, v = D^-1 u (b: start vector, then the
@@ -889,7 +903,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
                   u = bi - li * u;
                 }
                 if (fabs(dpi) < tiny) dpi = (dpi < 0.0) ? -tiny : tiny;
-                rd = 1.0 / dpi;
+                rd = rcp_d(dpi);
                 zb[q] = u * rd;
                 eprev = (double)ee[i];
               }
