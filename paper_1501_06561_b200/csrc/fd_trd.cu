@@ -45,6 +45,7 @@ struct TrdCfg {
   static_assert(2 * kWarps >= kOff, "not enough register slots");
   static_assert(2 * kFree >= NB, "not enough diagonal slots");
   static_assert(kThreads >= NM, "P4 needs a thread per row");
+  static_assert(NB <= 8, "the alpha / sigma reductions assume at most 8 row blocks");
 };
 
 // sub-column cc (0..3) of a lane block row
@@ -210,6 +211,7 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
     __syncthreads();
     float* Vout = G;
     const int offd = (N * (N + 1) / 2 + 3) / 4 * 4;
+    long long t_ph = clock64();
 
     for (int i = 0; i <= N - 2; ++i) {
       const int ci = i >> 5, cc = i & 3, cgi = (i & 31) >> 2;
@@ -219,9 +221,10 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
       {
         float alpha = 0.f;
         if (i > 0) {
-          float x = (lane < NB) ? s_apart[lane] : 0.f;
+          // NB <= 8 partials: every group of 8 lanes reduces its own copy (3 levels)
+          float x = ((lane & 7) < NB) ? s_apart[lane & 7] : 0.f;
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+          for (int o = 4; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
           alpha = 0.5f * s_tprev * x;
         }
         // publication of column i (rows >= i; rows < i -> 0) + partial sum of squares (rows >= i+2)
@@ -273,14 +276,15 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
         }
       }
       __syncthreads();
+      if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[11] += t_ - t_ph; t_ph = t_; }
       if (last) break;
       // ---- P3: the reflector of column i (every warp, identical arithmetic); SYMV of the
       //      unscaled x (x_r = col_r for r >= i+2, x_{i+1} = alpha - beta, v = x * scale) ----
       float tau_i, scale, amb;
       {
-        float x = (lane >= ci && lane < NB) ? s_sig[lane] : 0.f;
+        float x = ((lane & 7) >= ci && (lane & 7) < NB) ? s_sig[lane & 7] : 0.f;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        for (int o = 4; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
         const float sig = x;
         const float al = s_col[i + 1];
         float beta;
@@ -333,6 +337,7 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
         symv(a1, D, D);
       }
       __syncthreads();
+      if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[12] += t_ - t_ph; t_ph = t_; }
       // ---- P4 (warps owning rows): y = scale * (A x), p = tau y (rows > i), v = scale x ----
       if (warp < NB) {
         const int r = tid;
@@ -357,6 +362,7 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
         if (tid == 0) s_tprev = tau_i;
       }
       __syncthreads();
+      if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[13] += t_ - t_ph; t_ph = t_; p.dbg[14] += 1; }
     }
     // ---------------- last entries, outputs ----------------
     if (tid == 0) {
