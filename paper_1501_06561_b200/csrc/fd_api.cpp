@@ -379,8 +379,8 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
   h->prm.dbg = nullptr;
   if (getenv("FD_DEBUG_EIG")) {
     void* dbgp = nullptr;
-    if (cudaMalloc(&dbgp, 16 * sizeof(long long)) == cudaSuccess) {
-      cudaMemset(dbgp, 0, 16 * sizeof(long long));
+    if (cudaMalloc(&dbgp, 32 * sizeof(long long)) == cudaSuccess) {
+      cudaMemset(dbgp, 0, 32 * sizeof(long long));
       h->prm.dbg = static_cast<long long*>(dbgp);
     }
   }
@@ -751,11 +751,11 @@ fd_status fd_cov_err(const float* A, int64_t n, int64_t ld, const float* B, int3
 
 const char* fd_last_error(void) { return g_err.c_str(); }
 
-// debug: copy the eig phase trace (16 x int64) of the last eig launch (FD_DEBUG_EIG set)
+// debug: copy the phase trace (32 x int64, CTA 0 of the eig / trd kernels; FD_DEBUG_EIG set)
 int32_t fd_debug_eig_trace(fd_handle* h, long long* out16) {
   if (!h || !h->prm.dbg) return -1;
   cudaStreamSynchronize(h->stream);
-  cudaMemcpy(out16, h->prm.dbg, 16 * sizeof(long long), cudaMemcpyDeviceToHost);
+  cudaMemcpy(out16, h->prm.dbg, 32 * sizeof(long long), cudaMemcpyDeviceToHost);
   return 0;
 }
 

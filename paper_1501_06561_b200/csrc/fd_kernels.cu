@@ -872,6 +872,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
       double* lf = LF + j;   // lf[i * kMaxN]  multipliers of L
       double* z = Zs + j;    // z[i * kMaxN]
       double sc = 1.0;
+      long long t_iv = clock64();
       for (int it = 0; it < kInvIters; ++it) {
         if (act) {
           // L D L^T = T - mu I (tiny pivots perturbed), recomputed every iteration and
@@ -938,6 +939,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
           pscl[j] = sc;
         }
         __syncthreads();
+        if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[16] += t_ - t_iv; t_iv = t_; }
         // clusters of 2..kSmallCl members: one warp each, modified Gram-Schmidt
         // (normalise, orthogonalise twice, renormalise)
         for (int c = warp; c < ncl; c += kNW) {
@@ -981,6 +983,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
             if (lane == 0) pscl[k] = 1.0;
           }
         }
+        if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[17] += t_ - t_iv; t_iv = t_; }
         // larger clusters (wide-spread Grams put many small eigenvalues within ctol,
         // e.g. at merge levels): the whole CTA, one cluster at a time, classical
         // Gram-Schmidt twice per member.  Dots: warp w sweeps its rows, lane = earlier
@@ -1034,6 +1037,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
           }
         }
         __syncthreads();
+        if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[18] += t_ - t_iv; t_iv = t_; }
         if (act) sc = pscl[j];
       }
       if (act) pvec[j] = (T)sc;   // normalisation folded into the back-transform

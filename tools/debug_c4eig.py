@@ -12,7 +12,7 @@ A = torch.empty((w.n, w.d), dtype=torch.float32, device="cuda"); gen.fill(A)
 sk = m.Sketcher(w.d, 128, "fast_fd", n_shards=P)
 sk.profile(True)
 sk.append(A)
-tr = (ctypes.c_longlong * 16)()
+tr = (ctypes.c_longlong * 32)()
 L.fd_debug_eig_trace(sk.h, tr)
 prof = sk.profile_read()
 t = list(tr)

@@ -11,7 +11,7 @@ for variant, ell, P in [("fast_fd", 128, 148), ("fast_fd", 64, 148), ("fd", 32, 
     sk = m.Sketcher(w.d, ell, variant, n_shards=P)
     sk.profile(True)
     sk.append(A[: P * 2000] if variant == "fd" else A)
-    tr = (ctypes.c_longlong * 16)()
+    tr = (ctypes.c_longlong * 32)()
     L.fd_debug_eig_trace(sk.h, tr)
     prof = sk.profile_read()
     t = list(tr)

@@ -10,7 +10,7 @@ gen = fdgen.DeviceGenerator(w)
 A = torch.empty((w.n, w.d), dtype=torch.float32, device="cuda"); gen.fill(A)
 sk = m.Sketcher(w.d, 128, "fast_fd", n_shards=1184)
 sk.append(A)
-tr = (ctypes.c_longlong * 16)()
+tr = (ctypes.c_longlong * 32)()
 L.fd_debug_eig_trace(sk.h, tr)
 t = list(tr)
 steps = max(t[14], 1)
