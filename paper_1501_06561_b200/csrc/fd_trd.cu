@@ -211,7 +211,7 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
     __syncthreads();
     float* Vout = G;
     const int offd = (N * (N + 1) / 2 + 3) / 4 * 4;
-    long long t_ph = clock64();
+    long long t_ph = clock64(), t_st = t_ph;
 
     for (int i = 0; i <= N - 2; ++i) {
       const int ci = i >> 5, cc = i & 3, cgi = (i & 31) >> 2;
@@ -362,7 +362,11 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
         if (tid == 0) s_tprev = tau_i;
       }
       __syncthreads();
-      if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[13] += t_ - t_ph; t_ph = t_; p.dbg[14] += 1; }
+      if (p.dbg && blockIdx.x == 0 && tid == 0) {
+        const long long t_ = clock64();
+        p.dbg[13] += t_ - t_ph; t_ph = t_; p.dbg[14] += 1;
+        p.dbg[20 + min(3, i / 64)] += t_ - t_st; t_st = t_;
+      }
     }
     // ---------------- last entries, outputs ----------------
     if (tid == 0) {

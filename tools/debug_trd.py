@@ -15,3 +15,5 @@ L.fd_debug_eig_trace(sk.h, tr)
 t = list(tr)
 steps = max(t[14], 1)
 print("steps", steps, {"P1": t[11] / steps, "P3": t[12] / steps, "P4": t[13] / steps}, "cycles per step")
+q = steps / 4
+print("cycles per step by i range [0,64) [64,128) [128,192) [192,254):", [round(t[20 + k] / q) for k in range(4)])
