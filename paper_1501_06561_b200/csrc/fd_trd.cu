@@ -54,8 +54,10 @@ __device__ __forceinline__ float pick4(const float (&x)[4], int cc) {
 }
 
 // SYMV column sums of a lane block: sum over the 8 rows, reduce-scatter over the
-// 4 row groups (lanes ^16, ^8); lane (rg, cg) returns column 4cg + rg.
-__device__ __forceinline__ float col_sums(const float (&a)[8][4], const float (&vr)[8], int lane) {
+// 4 row groups (lanes ^16, ^8); lane (rg, cg) returns column 4cg + rg.  Also the
+// lane-local part of x_I^T T x_J (its 8 x 4 block) in dot.
+__device__ __forceinline__ float col_sums(const float (&a)[8][4], const float (&vr)[8], const float (&vc)[4],
+                                          int lane, float& dot) {
   float cs[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
@@ -63,6 +65,7 @@ __device__ __forceinline__ float col_sums(const float (&a)[8][4], const float (&
 #pragma unroll
     for (int c = 0; c < 4; ++c) cs[c] = fmaf(a[k][c], vk, cs[c]);
   }
+  dot = fmaf(cs[3], vc[3], fmaf(cs[2], vc[2], fmaf(cs[1], vc[1], cs[0] * vc[0])));
   const bool hb = (lane >> 4) & 1;
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
@@ -113,16 +116,18 @@ __device__ __forceinline__ float row_sums(const float (&a)[8][4], const float (&
 size_t trd_out_floats(int N) { return (size_t)((N * (N + 1) / 2 + 3) / 4 * 4) + 3 * (size_t)N; }
 
 // Per-tile helpers (lane block rows r0..r0+7, cols c0..c0+3).
-// rank-2 update A -= v w^T + w v^T with w = p - alpha v (previous step)
+// rank-2 update A -= v w^T + w v^T (pending step)
 template <bool DIAG>
-__device__ __forceinline__ void tile_update(float (&t)[8][4], int r0, int c0, float alpha,
-                                            const float* s_v, const float* s_p) {
-  float vc[4], wc[4];
-#pragma unroll
-  for (int c = 0; c < 4; ++c) { vc[c] = s_v[c0 + c]; wc[c] = fmaf(-alpha, vc[c], s_p[c0 + c]); }
+__device__ __forceinline__ void tile_update(float (&t)[8][4], int r0, int c0, const float* s_v, const float* s_w) {
+  const float4 v4 = *reinterpret_cast<const float4*>(s_v + c0), w4 = *reinterpret_cast<const float4*>(s_w + c0);
+  const float vc[4] = {v4.x, v4.y, v4.z, v4.w}, wc[4] = {w4.x, w4.y, w4.z, w4.w};
+  const float4 va = *reinterpret_cast<const float4*>(s_v + r0), vb = *reinterpret_cast<const float4*>(s_v + r0 + 4);
+  const float4 wa = *reinterpret_cast<const float4*>(s_w + r0), wb = *reinterpret_cast<const float4*>(s_w + r0 + 4);
+  const float vrs[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
+  const float wrs[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const float vr = s_v[r0 + k], wr = fmaf(-alpha, vr, s_p[r0 + k]);
+    const float vr = vrs[k], wr = wrs[k];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       if (DIAG) t[k][c] -= vr * wc[c] + wr * vc[c];   // exactly symmetric
@@ -138,15 +143,15 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
   constexpr int NB = C::NB, W = C::kWarps;
   extern __shared__ __align__(16) float s_dyn[];    // diagonal tiles (full): s_dg[NB][32][32]
   float (*s_dg)[32][32] = reinterpret_cast<float (*)[32][32]>(s_dyn);
-  __shared__ __align__(16) float s_v[NM];      // v of the previous step (materialised in P4)
-  __shared__ __align__(16) float s_p[NM];      // p = tau A v of the previous step
-  __shared__ __align__(16) float s_col[NM];    // column i, rows >= i (rows < i of its blocks: 0)
-  __shared__ __align__(16) float s_col2[NM];   // column N-1 (final step)
+  __shared__ __align__(16) float s_v[NM];      // v of the pending update (step s-1)
+  __shared__ __align__(16) float s_w[NM];      // w = p - alpha v of the pending update
+  __shared__ __align__(16) float s_col[NM];    // column s of A^(s-1), rows >= s (else 0)
+  __shared__ __align__(16) float s_nxt[NM];    // look-ahead: column s+1 of A^(s-1)
   __shared__ __align__(16) float s_ctb[NB][NB][32];  // SYMV contributions [block][slot][row]
-  __shared__ float s_sig[NB];                  // per-block partial sum of squares of column i
-  __shared__ float s_apart[NB];                // per-warp partials of p^T v
+  __shared__ float s_sig[NB];                  // per-block partial sums of squares (rows >= s+2)
+  __shared__ __align__(16) float s_xax[(W + 3) / 4 * 4];  // per-warp partials of x^T A x (zero-padded)
   __shared__ float s_d[NM], s_e[NM], s_tau[NM];
-  __shared__ float s_tprev;                    // tau of the previous step
+  __shared__ float s_corner, s_dlast;          // A[N-1][N-1] (look-ahead / updated)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rg = lane >> 3, cg = lane & 7;     // lane block: rows 8rg..8rg+7, cols 4cg..4cg+3
@@ -163,11 +168,11 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
     oI[q] = J + 1 + (t - base);
   }
   // diagonal tiles on the warps with a free second block: D -> warp W - kFree + D % kFree
-  int dT[2];
-  int nd = 0;
-  for (int D = 0; D < NB; ++D)
-    if (warp == W - C::kFree + D % C::kFree) dT[nd++] = D;
+  const int fw = warp - (W - C::kFree);
+  const int dT[2] = {fw, fw + C::kFree};
+  const int nd = (fw < 0) ? 0 : (fw < NB) + (fw + C::kFree < NB);
 
+  if (tid < (W + 3) / 4 * 4) s_xax[tid] = 0.f;   // padding stays zero
   for (int pi = blockIdx.x; pi < count; pi += gridDim.x) {
     const Prob P = probs[pi];
     const int N = P.rows0 + P.rows1;
@@ -189,19 +194,32 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
     };
     if (ov[0]) load_blk(oI[0], oJ[0], a0);
     if (ov[1]) load_blk(oI[1], oJ[1], a1);
-    for (int q = 0; q < nd; ++q) {
+    _Pragma("unroll") for (int q = 0; q < 2; ++q) {
+      if (q >= nd) break;
       load_blk(dT[q], dT[q], a1);
 #pragma unroll
       for (int k = 0; k < 8; ++k)
         *reinterpret_cast<float4*>(&s_dg[dT[q]][8 * rg + k][4 * cg]) = make_float4(a1[k][0], a1[k][1], a1[k][2], a1[k][3]);
     }
-    for (int r = tid; r < NM; r += blockDim.x) { s_p[r] = 0.f; s_v[r] = 0.f; }
-    if (tid < NB) s_apart[tid] = 0.f;
-    if (tid == 0) s_tprev = 0.f;
+    // column 0 (rows >= 0) straight from G (the lower triangle the tiles hold) and
+    // the partial sums of squares of its rows >= 2, per 32-row block
+    if (warp < NB) {
+      const int r = tid;
+      const float c = (r < N) ? G[(int64_t)r * p.ldg] : 0.f;
+      s_col[r] = c;
+      float sq = (r >= 2 && r < N) ? c * c : 0.f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+      if (lane == 0) s_sig[warp] = sq;
+      s_v[r] = 0.f;
+      s_w[r] = 0.f;
+      if (r == N - 1) s_dlast = G[(int64_t)r * p.ldg + r];
+    }
     __syncthreads();  // G fully read before V overwrites it
     // diagonal tiles: mirror the lower triangle (the tensor-core Gram is symmetric
     // only up to accumulation order; the symmetric update needs exact symmetry)
-    for (int q = 0; q < nd; ++q) {
+    _Pragma("unroll") for (int q = 0; q < 2; ++q) {
+      if (q >= nd) break;
       const int D = dT[q];
       for (int e = lane; e < 32 * 32; e += 32) {
         const int r = e >> 5, c = e & 31;
@@ -212,160 +230,143 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
     float* Vout = G;
     const int offd = (N * (N + 1) / 2 + 3) / 4 * 4;
     long long t_ph = clock64(), t_st = t_ph;
+    const int cn = (N - 1) >> 5, ccn = (N - 1) & 3;
 
-    for (int i = 0; i <= N - 2; ++i) {
-      const int ci = i >> 5, cc = i & 3, cgi = (i & 31) >> 2;
-      const int cn = (N - 1) >> 5, ccn = (N - 1) & 3, cgn = ((N - 1) & 31) >> 2;
-      const bool last = (i == N - 2);
-      // ---- P1: pending rank-2 update of step i-1, publish column i ----
+    // Step s: reflector H_s of column s.  Invariant at the top of phase A(s): the
+    // tiles hold A^(s-2) with the rank-2 update of step s-1 pending (s_v, s_w);
+    // s_col = column s of A^(s-1) (rows >= s, else 0); s_sig = its per-block
+    // partial sums of squares over rows >= s+2.
+    for (int s = 0; s <= N - 3; ++s) {
+      const int cs1 = (s + 1) >> 5, cc1 = (s + 1) & 3, cg1 = ((s + 1) & 31) >> 2;
+      const bool last = (s == N - 3);
+      float tau_s, scale, amb, beta_s;
+      // ---- phase A: pending update (s-1), reflector s, SYMV y = A^(s-1) x_s,
+      //      look-ahead column s+1 of A^(s-1), tile partials of x^T A x ----
       {
-        float alpha = 0.f;
-        if (i > 0) {
-          // NB <= 8 partials: every group of 8 lanes reduces its own copy (3 levels)
-          float x = ((lane & 7) < NB) ? s_apart[lane & 7] : 0.f;
+        if (s > 0) {
+          if (ov[0] && 32 * oJ[0] + 31 > s) tile_update<false>(a0, 32 * oI[0] + 8 * rg, 32 * oJ[0] + 4 * cg, s_v, s_w);
+          if (ov[1] && 32 * oJ[1] + 31 > s) tile_update<false>(a1, 32 * oI[1] + 8 * rg, 32 * oJ[1] + 4 * cg, s_v, s_w);
+        }
+        {  // reflector (every warp, identical arithmetic)
+          float x = ((lane & 7) < NB) ? s_sig[lane & 7] : 0.f;
 #pragma unroll
           for (int o = 4; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-          alpha = 0.5f * s_tprev * x;
+          const float sig = x;
+          const float al = s_col[s + 1];
+          float beta;
+          if (sig == 0.f) {
+            tau_s = 0.f; beta = al; scale = 0.f; amb = 0.f;
+          } else {
+            const float nrm = sqrtf(fmaf(al, al, sig));
+            beta = (al <= 0.f) ? nrm : -nrm;
+            amb = al - beta;
+            tau_s = __fdividef(-amb, beta);
+            scale = __fdividef(1.f, amb);
+          }
+          beta_s = beta;
         }
-        // publication of column i (rows >= i; rows < i -> 0) + partial sum of squares (rows >= i+2)
-        auto publish = [&](const float (&t)[8][4], int TI, int TJ) {
-          const int r0 = 32 * TI + 8 * rg;
-          if (TJ == ci) {
-            float sq = 0.f;
-            if (cg == cgi) {
-#pragma unroll
-              for (int k = 0; k < 8; ++k) {
-                const float x = pick4(t[k], cc);
-                const int r = r0 + k;
-                s_col[r] = (r >= i) ? x : 0.f;
-                if (r >= i + 2) sq = fmaf(x, x, sq);
-              }
-            }
-            sq += __shfl_xor_sync(0xffffffffu, sq, 8);
-            sq += __shfl_xor_sync(0xffffffffu, sq, 16);
-            if (lane == cgi) s_sig[TI] = sq;
+        float xax = 0.f;
+        // x_s (unscaled): x_r = col_r for r >= s+2, x_{s+1} = alpha - beta, 0 above
+        auto xfix = [&](float c, int r) -> float { return (r == s + 1) ? amb : ((r == s) ? 0.f : c); };
+        auto publish_symv = [&](const float (&t)[8][4], int TI, int TJ) {
+          const int r0 = 32 * TI + 8 * rg, c0 = 32 * TJ + 4 * cg;
+          if (TJ == cs1 && cg == cg1) {
+            *reinterpret_cast<float4*>(&s_nxt[r0]) = make_float4(pick4(t[0], cc1), pick4(t[1], cc1), pick4(t[2], cc1), pick4(t[3], cc1));
+            *reinterpret_cast<float4*>(&s_nxt[r0 + 4]) = make_float4(pick4(t[4], cc1), pick4(t[5], cc1), pick4(t[6], cc1), pick4(t[7], cc1));
           }
-          if (last && TJ == cn && cg == cgn) {
+          if (last && TI == cn && TJ == cn && cg == (((N - 1) & 31) >> 2)) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) s_col2[r0 + k] = pick4(t[k], ccn);
+            for (int k = 0; k < 8; ++k)
+              if (r0 + k == N - 1) s_corner = pick4(t[k], ccn);
           }
+          const float4 ra = *reinterpret_cast<const float4*>(&s_col[r0]);
+          const float4 rb = *reinterpret_cast<const float4*>(&s_col[r0 + 4]);
+          const float4 cv = *reinterpret_cast<const float4*>(&s_col[c0]);
+          const float xr[8] = {xfix(ra.x, r0), xfix(ra.y, r0 + 1), xfix(ra.z, r0 + 2), xfix(ra.w, r0 + 3),
+                               xfix(rb.x, r0 + 4), xfix(rb.y, r0 + 5), xfix(rb.z, r0 + 6), xfix(rb.w, r0 + 7)};
+          const float xc[4] = {xfix(cv.x, c0), xfix(cv.y, c0 + 1), xfix(cv.z, c0 + 2), xfix(cv.w, c0 + 3)};
+          float dot;
+          s_ctb[TJ][TI][4 * cg + rg] = col_sums(t, xr, xc, lane, dot);
+          xax = fmaf(TI != TJ ? 2.f : 1.f, dot, xax);
+          if (TI != TJ) s_ctb[TI][TJ][8 * rg + cg] = row_sums(t, xc, lane);
         };
-        if (ov[0] && 32 * oJ[0] + 31 >= i) {
-          if (i > 0) tile_update<false>(a0, 32 * oI[0] + 8 * rg, 32 * oJ[0] + 4 * cg, alpha, s_v, s_p);
-          publish(a0, oI[0], oJ[0]);
-        }
-        if (ov[1] && 32 * oJ[1] + 31 >= i) {
-          if (i > 0) tile_update<false>(a1, 32 * oI[1] + 8 * rg, 32 * oJ[1] + 4 * cg, alpha, s_v, s_p);
-          publish(a1, oI[1], oJ[1]);
-        }
-        for (int q = 0; q < nd; ++q) {
+        if (ov[0] && 32 * oJ[0] + 31 > s) publish_symv(a0, oI[0], oJ[0]);
+        if (ov[1] && 32 * oJ[1] + 31 > s) publish_symv(a1, oI[1], oJ[1]);
+        _Pragma("unroll") for (int q = 0; q < 2; ++q) {
+          if (q >= nd) break;
           const int D = dT[q];
-          if (32 * D + 31 < i) continue;
+          if (32 * D + 31 <= s) continue;
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             const float4 x = *reinterpret_cast<const float4*>(&s_dg[D][8 * rg + k][4 * cg]);
             a1[k][0] = x.x; a1[k][1] = x.y; a1[k][2] = x.z; a1[k][3] = x.w;
           }
-          if (i > 0) {
-            tile_update<true>(a1, 32 * D + 8 * rg, 32 * D + 4 * cg, alpha, s_v, s_p);
+          if (s > 0) {
+            tile_update<true>(a1, 32 * D + 8 * rg, 32 * D + 4 * cg, s_v, s_w);
 #pragma unroll
             for (int k = 0; k < 8; ++k)
               *reinterpret_cast<float4*>(&s_dg[D][8 * rg + k][4 * cg]) = make_float4(a1[k][0], a1[k][1], a1[k][2], a1[k][3]);
           }
-          publish(a1, D, D);
+          publish_symv(a1, D, D);
         }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) xax += __shfl_xor_sync(0xffffffffu, xax, o);
+        if (lane == 0) s_xax[warp] = xax;
       }
       __syncthreads();
       if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[11] += t_ - t_ph; t_ph = t_; }
-      if (last) break;
-      // ---- P3: the reflector of column i (every warp, identical arithmetic); SYMV of the
-      //      unscaled x (x_r = col_r for r >= i+2, x_{i+1} = alpha - beta, v = x * scale) ----
-      float tau_i, scale, amb;
-      {
-        float x = ((lane & 7) >= ci && (lane & 7) < NB) ? s_sig[lane & 7] : 0.f;
-#pragma unroll
-        for (int o = 4; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        const float sig = x;
-        const float al = s_col[i + 1];
-        float beta;
-        if (sig == 0.f) {
-          tau_i = 0.f; beta = al; scale = 0.f; amb = 0.f;
-        } else {
-          const float nrm = sqrtf(fmaf(al, al, sig));
-          beta = (al <= 0.f) ? nrm : -nrm;
-          amb = al - beta;
-          tau_i = __fdividef(-amb, beta);
-          scale = __fdividef(1.f, amb);
-        }
-        if (warp == W - 1) {  // output of the reflector (off the critical path)
-          const int base = pk_off_t(i, N) - i;
-          for (int r = i + 2 + lane; r < N; r += 32) Vout[base + r] = s_col[r] * scale;
-          if (lane == 0) { s_d[i] = s_col[i]; s_e[i] = beta; s_tau[i] = tau_i; }
-        }
-      }
-      auto symv = [&](const float (&t)[8][4], int TI, int TJ) {
-        const int r0 = 32 * TI + 8 * rg, c0 = 32 * TJ + 4 * cg;
-        float xr[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int r = r0 + k;
-          const float x = s_col[r];
-          xr[k] = (r == i + 1) ? amb : ((r == i) ? 0.f : x);
-        }
-        s_ctb[TJ][TI][4 * cg + rg] = col_sums(t, xr, lane);
-        if (TI != TJ) {
-          float xc[4];
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const int r = c0 + c;
-            const float x = s_col[r];
-            xc[c] = (r == i + 1) ? amb : ((r == i) ? 0.f : x);
-          }
-          s_ctb[TI][TJ][8 * rg + cg] = row_sums(t, xc, lane);
-        }
-      };
-      if (ov[0] && 32 * oJ[0] + 31 > i) symv(a0, oI[0], oJ[0]);
-      if (ov[1] && 32 * oJ[1] + 31 > i) symv(a1, oI[1], oJ[1]);
-      for (int q = 0; q < nd; ++q) {
-        const int D = dT[q];
-        if (32 * D + 31 <= i) continue;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float4 x = *reinterpret_cast<const float4*>(&s_dg[D][8 * rg + k][4 * cg]);
-          a1[k][0] = x.x; a1[k][1] = x.y; a1[k][2] = x.z; a1[k][3] = x.w;
-        }
-        symv(a1, D, D);
-      }
-      __syncthreads();
-      if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[12] += t_ - t_ph; t_ph = t_; }
-      // ---- P4 (warps owning rows): y = scale * (A x), p = tau y (rows > i), v = scale x ----
+      // ---- phase B (a thread per row): p = tau A v, w = p - alpha v with
+      //      alpha = (tau/2) p^T v = (tau^2 scale^2 / 2) x^T A x; column s+1 of A^(s) ----
       if (warp < NB) {
-        const int r = tid;
-        float y = 0.f;
-        const int b = r >> 5, rr = r & 31;
-        if (r > i && r < N) {
+        const int r = tid, b = r >> 5, rr = r & 31;
+        float yp[NB], y1p[NB];
 #pragma unroll
-          for (int sl = 0; sl < NB; ++sl) {
-            const int tc = sl < b ? sl : b;
-            if (32 * tc + 31 > i) y += s_ctb[b][sl][rr];
-          }
+        for (int sl = 0; sl < NB; ++sl) {
+          const int tc = sl < b ? sl : b;
+          yp[sl] = (r > s && r < N && 32 * tc + 31 > s) ? s_ctb[b][sl][rr] : 0.f;
+          const int tc1 = sl < cs1 ? sl : cs1;
+          y1p[sl] = (32 * tc1 + 31 > s) ? s_ctb[cs1][sl][(s + 1) & 31] : 0.f;
         }
-        const float x = (b >= ci) ? s_col[r] : 0.f;
-        const float vr = (r == i + 1) ? 1.f : ((r >= i + 2 && r < N) ? x * scale : 0.f);
-        const float pr = tau_i * scale * y;
-        s_p[r] = pr;
-        s_v[r] = vr;
-        float pv = pr * vr;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
-        if (lane == 0) s_apart[warp] = pv;
-        if (tid == 0) s_tprev = tau_i;
+        for (int h = 1; h < NB; h *= 2)
+#pragma unroll
+          for (int sl = 0; sl + h < NB; sl += 2 * h) { yp[sl] += yp[sl + h]; y1p[sl] += y1p[sl + h]; }
+        const float y = yp[0], y1 = y1p[0];
+        float xp[(W + 3) / 4 * 4];
+#pragma unroll
+        for (int q = 0; q < (W + 3) / 4; ++q) {
+          const float4 t4 = *reinterpret_cast<const float4*>(&s_xax[4 * q]);
+          xp[4 * q] = t4.x; xp[4 * q + 1] = t4.y; xp[4 * q + 2] = t4.z; xp[4 * q + 3] = t4.w;
+        }
+        constexpr int XP = (W + 3) / 4 * 4;
+#pragma unroll
+        for (int h = 1; h < XP; h *= 2)
+#pragma unroll
+          for (int q = 0; q + h < XP; q += 2 * h) xp[q] += xp[q + h];
+        const float xax = xp[0];
+        const float alpha = 0.5f * (tau_s * scale) * (tau_s * scale) * xax;
+        const float x = s_col[r];
+        const float vr = (r == s + 1) ? 1.f : ((r >= s + 2 && r < N) ? x * scale : 0.f);
+        const float ts = tau_s * scale;
+        const float wr = fmaf(-alpha, vr, ts * y);
+        const float w1 = fmaf(ts, y1, -alpha);              // w_{s+1} (v_{s+1} = 1)
+        const float col = (r >= s + 1 && r < N) ? s_nxt[r] - vr * w1 - wr : 0.f;
+        s_v[r] = vr;
+        s_w[r] = wr;
+        if (r >= s + 2 && r < N) Vout[pk_off_t(s, N) - s + r] = vr;   // Householder vector s
+        if (r == s) { s_d[s] = x; s_e[s] = beta_s; s_tau[s] = tau_s; }
+        s_col[r] = col;
+        float sq = (r >= s + 3 && r < N) ? col * col : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0) s_sig[warp] = sq;
+        if (last && r == N - 1) s_dlast = s_corner - 2.f * vr * wr;
       }
       __syncthreads();
       if (p.dbg && blockIdx.x == 0 && tid == 0) {
         const long long t_ = clock64();
-        p.dbg[13] += t_ - t_ph; t_ph = t_; p.dbg[14] += 1;
-        p.dbg[20 + min(3, i / 64)] += t_ - t_st; t_st = t_;
+        p.dbg[12] += t_ - t_ph; t_ph = t_; p.dbg[14] += 1;
+        p.dbg[20 + min(3, s / 64)] += t_ - t_st; t_st = t_;
       }
     }
     // ---------------- last entries, outputs ----------------
@@ -373,8 +374,10 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
       if (N >= 2) {
         s_d[N - 2] = s_col[N - 2];
         s_e[N - 2] = s_col[N - 1];
-        s_d[N - 1] = s_col2[N - 1];
+        s_d[N - 1] = s_dlast;
         s_tau[N - 2] = 0.f;
+      } else {
+        s_d[0] = s_col[0];
       }
       s_e[N - 1] = 0.f;
       s_tau[N - 1] = 0.f;
