@@ -145,7 +145,7 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
   float (*s_dg)[32][32] = reinterpret_cast<float (*)[32][32]>(s_dyn);
   __shared__ __align__(16) float s_v[NM];      // v of the pending update (step s-1)
   __shared__ __align__(16) float s_w[NM];      // w = p - alpha v of the pending update
-  __shared__ __align__(16) float s_col[NM];    // column s of A^(s-1), rows >= s (else 0)
+  __shared__ __align__(16) float s_x[NM];      // x~_s: column s of A^(s-1), rows >= s+1 (else 0)
   __shared__ __align__(16) float s_nxt[NM];    // look-ahead: column s+1 of A^(s-1)
   __shared__ __align__(16) float s_ctb[NB][NB][32];  // SYMV contributions [block][slot][row]
   __shared__ float s_sig[NB];                  // per-block partial sums of squares (rows >= s+2)
@@ -201,12 +201,13 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
       for (int k = 0; k < 8; ++k)
         *reinterpret_cast<float4*>(&s_dg[dT[q]][8 * rg + k][4 * cg]) = make_float4(a1[k][0], a1[k][1], a1[k][2], a1[k][3]);
     }
-    // column 0 (rows >= 0) straight from G (the lower triangle the tiles hold) and
-    // the partial sums of squares of its rows >= 2, per 32-row block
+    // column 0 straight from G (the lower triangle the tiles hold): d_0, x~_0 (rows >= 1)
+    // and the partial sums of squares of its rows >= 2, per 32-row block
     if (warp < NB) {
       const int r = tid;
       const float c = (r < N) ? G[(int64_t)r * p.ldg] : 0.f;
-      s_col[r] = c;
+      s_x[r] = (r >= 1) ? c : 0.f;
+      if (r == 0) s_d[0] = c;
       float sq = (r >= 2 && r < N) ? c * c : 0.f;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
@@ -234,12 +235,14 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
 
     // Step s: reflector H_s of column s.  Invariant at the top of phase A(s): the
     // tiles hold A^(s-2) with the rank-2 update of step s-1 pending (s_v, s_w);
-    // s_col = column s of A^(s-1) (rows >= s, else 0); s_sig = its per-block
-    // partial sums of squares over rows >= s+2.
+    // s_x = x~_s = column s of A^(s-1) on rows >= s+1 (else 0); s_sig = its
+    // per-block partial sums of squares over rows >= s+2.  The Householder x_s
+    // differs from x~_s only in row s+1 (alpha - beta instead of alpha): the SYMV
+    // runs on x~_s and phase B adds delta * A[:, s+1] (the look-ahead column).
     for (int s = 0; s <= N - 3; ++s) {
       const int cs1 = (s + 1) >> 5, cc1 = (s + 1) & 3, cg1 = ((s + 1) & 31) >> 2;
       const bool last = (s == N - 3);
-      float tau_s, scale, amb, beta_s;
+      float tau_s, scale, amb, beta_s, al;
       // ---- phase A: pending update (s-1), reflector s, SYMV y = A^(s-1) x_s,
       //      look-ahead column s+1 of A^(s-1), tile partials of x^T A x ----
       {
@@ -252,7 +255,7 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
 #pragma unroll
           for (int o = 4; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
           const float sig = x;
-          const float al = s_col[s + 1];
+          al = s_x[s + 1];
           float beta;
           if (sig == 0.f) {
             tau_s = 0.f; beta = al; scale = 0.f; amb = 0.f;
@@ -266,8 +269,6 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
           beta_s = beta;
         }
         float xax = 0.f;
-        // x_s (unscaled): x_r = col_r for r >= s+2, x_{s+1} = alpha - beta, 0 above
-        auto xfix = [&](float c, int r) -> float { return (r == s + 1) ? amb : ((r == s) ? 0.f : c); };
         auto publish_symv = [&](const float (&t)[8][4], int TI, int TJ) {
           const int r0 = 32 * TI + 8 * rg, c0 = 32 * TJ + 4 * cg;
           if (TJ == cs1 && cg == cg1) {
@@ -279,12 +280,11 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
             for (int k = 0; k < 8; ++k)
               if (r0 + k == N - 1) s_corner = pick4(t[k], ccn);
           }
-          const float4 ra = *reinterpret_cast<const float4*>(&s_col[r0]);
-          const float4 rb = *reinterpret_cast<const float4*>(&s_col[r0 + 4]);
-          const float4 cv = *reinterpret_cast<const float4*>(&s_col[c0]);
-          const float xr[8] = {xfix(ra.x, r0), xfix(ra.y, r0 + 1), xfix(ra.z, r0 + 2), xfix(ra.w, r0 + 3),
-                               xfix(rb.x, r0 + 4), xfix(rb.y, r0 + 5), xfix(rb.z, r0 + 6), xfix(rb.w, r0 + 7)};
-          const float xc[4] = {xfix(cv.x, c0), xfix(cv.y, c0 + 1), xfix(cv.z, c0 + 2), xfix(cv.w, c0 + 3)};
+          const float4 ra = *reinterpret_cast<const float4*>(&s_x[r0]);
+          const float4 rb = *reinterpret_cast<const float4*>(&s_x[r0 + 4]);
+          const float4 cv = *reinterpret_cast<const float4*>(&s_x[c0]);
+          const float xr[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+          const float xc[4] = {cv.x, cv.y, cv.z, cv.w};
           float dot;
           s_ctb[TJ][TI][4 * cg + rg] = col_sums(t, xr, xc, lane, dot);
           xax = fmaf(TI != TJ ? 2.f : 1.f, dot, xax);
@@ -331,7 +331,7 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
         for (int h = 1; h < NB; h *= 2)
 #pragma unroll
           for (int sl = 0; sl + h < NB; sl += 2 * h) { yp[sl] += yp[sl + h]; y1p[sl] += y1p[sl + h]; }
-        const float y = yp[0], y1 = y1p[0];
+        const float yt = yp[0], yt1 = y1p[0];       // (A x~)_r, (A x~)_{s+1}
         float xp[(W + 3) / 4 * 4];
 #pragma unroll
         for (int q = 0; q < (W + 3) / 4; ++q) {
@@ -343,19 +343,25 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
         for (int h = 1; h < XP; h *= 2)
 #pragma unroll
           for (int q = 0; q + h < XP; q += 2 * h) xp[q] += xp[q + h];
-        const float xax = xp[0];
+        // x = x~ + delta e_{s+1}:  A x = A x~ + delta A[:, s+1],
+        // x^T A x = x~^T A x~ + delta (2 (A x~)_{s+1} + delta A[s+1][s+1])
+        const float dl = amb - al;
+        const float nx = s_nxt[r], a11 = s_nxt[s + 1];
+        const float y = fmaf(dl, nx, yt), y1 = fmaf(dl, a11, yt1);
+        const float xax = fmaf(dl, fmaf(dl, a11, 2.f * yt1), xp[0]);
         const float alpha = 0.5f * (tau_s * scale) * (tau_s * scale) * xax;
-        const float x = s_col[r];
-        const float vr = (r == s + 1) ? 1.f : ((r >= s + 2 && r < N) ? x * scale : 0.f);
+        const float xt = s_x[r];
+        const float vr = (r == s + 1) ? 1.f : ((r >= s + 2 && r < N) ? xt * scale : 0.f);
         const float ts = tau_s * scale;
-        const float wr = fmaf(-alpha, vr, ts * y);
+        const float wr = (r > s && r < N) ? fmaf(-alpha, vr, ts * y) : 0.f;
         const float w1 = fmaf(ts, y1, -alpha);              // w_{s+1} (v_{s+1} = 1)
-        const float col = (r >= s + 1 && r < N) ? s_nxt[r] - vr * w1 - wr : 0.f;
+        const float col = (r >= s + 1 && r < N) ? nx - vr * w1 - wr : 0.f;   // column s+1 of A^(s)
         s_v[r] = vr;
         s_w[r] = wr;
+        s_x[r] = (r >= s + 2) ? col : 0.f;
         if (r >= s + 2 && r < N) Vout[pk_off_t(s, N) - s + r] = vr;   // Householder vector s
-        if (r == s) { s_d[s] = x; s_e[s] = beta_s; s_tau[s] = tau_s; }
-        s_col[r] = col;
+        if (r == s) { s_e[s] = beta_s; s_tau[s] = tau_s; }
+        if (r == s + 1) s_d[s + 1] = col;
         float sq = (r >= s + 3 && r < N) ? col * col : 0.f;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
@@ -372,12 +378,9 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
     // ---------------- last entries, outputs ----------------
     if (tid == 0) {
       if (N >= 2) {
-        s_d[N - 2] = s_col[N - 2];
-        s_e[N - 2] = s_col[N - 1];
+        s_e[N - 2] = s_x[N - 1];
         s_d[N - 1] = s_dlast;
         s_tau[N - 2] = 0.f;
-      } else {
-        s_d[0] = s_col[0];
       }
       s_e[N - 1] = 0.f;
       s_tau[N - 1] = 0.f;
