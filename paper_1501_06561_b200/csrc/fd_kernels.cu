@@ -857,75 +857,111 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
     // the per-thread recurrences are coalesced across threads.
     const int ncl = s_ncl;
     const int JX = s_jx;
+    int* vact = ccnt;   // coarse bisection counts are dead here: per-vector "needed" flags
+    for (int j = tid; j < JX; j += blockDim.x) {   // singletons with zero weight are not needed
+      bool a = wgt[j] != T(0);
+      if (!a) {
+        int c = 0;
+        while (c + 1 < ncl && cstart[c + 1] <= j) ++c;
+        a = clen[c] > 1;
+      }
+      vact[j] = a;
+      pscl[j] = 1.0;
+    }
+    __syncthreads();
     {
       const double tiny = 2.3e-16 * (double)bnorm + 1e-300;
-      const int j = tid;
-      bool act = false;
-      if (j < JX) {  // singletons with zero weight are not needed
-        act = wgt[j] != T(0);
-        if (!act) {
-          int c = 0;
-          while (c + 1 < ncl && cstart[c + 1] <= j) ++c;
-          act = clen[c] > 1;
-        }
-      }
-      double* lf = LF + j;   // lf[i * kMaxN]  multipliers of L
-      double* z = Zs + j;    // z[i * kMaxN]
-      double sc = 1.0;
       long long t_iv = clock64();
+      // Twisted solves: vector j is solved by the lane pair (2j', 2j'+1); the even
+      // lane eliminates rows 0..m-1 top-down (T - mu I = L D+ L^T part), the odd lane
+      // rows N-1..m+1 bottom-up (U D- U^T part); they meet at the twist m = N/2
+      // (gamma_m = a_m - l_{m-1} e_{m-1} - u_m e_m) and back-substitute outwards.
+      // Same arithmetic as one LDL^T solve, half the sequential chain.
+      const int side = tid & 1;
+      const unsigned pmask = 3u << (lane & ~1);
+      const int m = N >> 1;
       for (int it = 0; it < kInvIters; ++it) {
-        if (act) {
-          // L D L^T = T - mu I (tiny pivots perturbed), recomputed every iteration and
-          // fused with the forward solve L u = b, v = D^-1 u (b: start vector, then the
-          // scaled previous iterate); only the multipliers of L are stored (for the
-          // backward solve), so the per-CTA scratch stays L2-resident.
+        for (int j = tid >> 1; j < JX; j += blockDim.x >> 1) {
+          if (!vact[j]) continue;
+          double* lf = LF + j;   // lf[i * kMaxN]: l_i (i < m), u_i (i >= m)
+          double* z = Zs + j;    // z[i * kMaxN]
+          const double sc = pscl[j];
           const double mu = (double)lam[j];
-          double rd = 0.0, u = 0.0, eprev = 0.0;
-          for (int i0 = 0; i0 < N; i0 += 8) {
+          auto rhs = [&](int i, double zi) -> double {
+            return (it == 0) ? 1.0 + 0.5 * (double)(((i + 1) * 7919 + (j + 3) * 104729) % 211) / 211.0 : zi * sc;
+          };
+          // Both lanes run ONE instruction stream (no divergence): step k of a side is
+          // row i = i0 + dir k; the coupling to the previous row of its elimination
+          // order is e[ec] with ec = i - 1 (top) / i (bottom), stored multiplier lf[ec].
+          const int cnt = side ? (N - 1 - m) : m;     // rows of this side (<= m)
+          const int dir = side ? -1 : 1, ist = side ? N - 1 : 0;
+          double rd = 0.0, w = 0.0, eprev = 0.0;
+          for (int k0 = 0; k0 < m; k0 += 8) {
             double zb[8];
             if (it > 0) {
 #pragma unroll
-              for (int q = 0; q < 8; ++q) zb[q] = (i0 + q < N) ? z[(size_t)(i0 + q) * kMaxN] : 0.0;
+              for (int q = 0; q < 8; ++q) zb[q] = (k0 + q < cnt) ? z[(size_t)(ist + dir * (k0 + q)) * kMaxN] : 0.0;
             }
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-              const int i = i0 + q;
-              if (i < N) {
-                const double bi = (it == 0) ? 1.0 + 0.5 * (double)(((i + 1) * 7919 + (j + 3) * 104729) % 211) / 211.0
-                                            : zb[q] * sc;
+              const int k = k0 + q;
+              if (k < cnt) {
+                const int i = ist + dir * k;
+                const double bi = rhs(i, zb[q]);
                 double dpi;
-                if (i == 0) {
-                  dpi = (double)dd[0] - mu;
-                  u = bi;
+                if (k == 0) {
+                  dpi = (double)dd[i] - mu;
+                  w = bi;
                 } else {
                   const double li = eprev * rd;
-                  lf[(size_t)(i - 1) * kMaxN] = li;
+                  lf[(size_t)(i - 1 + side) * kMaxN] = li;
                   dpi = ((double)dd[i] - mu) - li * eprev;
-                  u = bi - li * u;
+                  w = bi - li * w;
                 }
                 if (fabs(dpi) < tiny) dpi = (dpi < 0.0) ? -tiny : tiny;
                 rd = rcp_d(dpi);
-                zb[q] = u * rd;
-                eprev = (double)ee[i];
+                zb[q] = w * rd;
+                eprev = (double)ee[i - side];
               }
             }
 #pragma unroll
             for (int q = 0; q < 8; ++q)
-              if (i0 + q < N) z[(size_t)(i0 + q) * kMaxN] = zb[q];
+              if (k0 + q < cnt) z[(size_t)(ist + dir * (k0 + q)) * kMaxN] = zb[q];
           }
-          // backward solve L^T y = v, with the norm (8-element load batches)
-          double next = 0.0, nr = 0.0;
-          for (int i1 = N - 1; i1 >= 0; i1 -= 8) {
+          double tS = 0.0, wS = 0.0;   // this side's term of the twist row
+          if (cnt > 0) {
+            const double l = eprev * rd;   // l_{m-1} (top) / u_m (bottom)
+            lf[(size_t)(m - 1 + side) * kMaxN] = l;
+            tS = l * eprev;
+            wS = l * w;
+          }
+          // twist row m (both lanes, identical arithmetic)
+          const double tO = __shfl_xor_sync(pmask, tS, 1), wO = __shfl_xor_sync(pmask, wS, 1);
+          const double tA = side ? tO : tS, tB = side ? tS : tO;
+          const double wA = side ? wO : wS, wB = side ? wS : wO;
+          double gm = (((double)dd[m] - mu) - tA) - tB;
+          if (fabs(gm) < tiny) gm = (gm < 0.0) ? -tiny : tiny;
+          const double bm = rhs(m, (it > 0) ? z[(size_t)m * kMaxN] : 0.0);
+          const double zm = ((bm - wA) - wB) * rcp_d(gm);
+          __syncwarp(pmask);   // both lanes read z[m] before it is overwritten
+          if (side == 0) z[(size_t)m * kMaxN] = zm;
+          double nr = side ? 0.0 : zm * zm;
+          // back-substitution outwards from m: top i = m-1..0 (l_i = lf[i]),
+          // bottom i = m+1..N-1 (u_{i-1} = lf[i-1])
+          double next = zm;
+          const int bst = side ? m + 1 : m - 1, bdir = side ? 1 : -1;
+          for (int k0 = 0; k0 < m; k0 += 8) {
             double zb[8], lb[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-              const int i = i1 - q;
-              zb[q] = (i >= 0) ? z[(size_t)i * kMaxN] : 0.0;
-              lb[q] = (i >= 0 && i < N - 1) ? lf[(size_t)i * kMaxN] : 0.0;
+              const int i = bst + bdir * (k0 + q);
+              const bool ok = k0 + q < cnt;
+              zb[q] = ok ? z[(size_t)i * kMaxN] : 0.0;
+              lb[q] = ok ? lf[(size_t)(i - side) * kMaxN] : 0.0;
             }
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-              if (i1 - q >= 0) {
+              if (k0 + q < cnt) {
                 next = zb[q] - lb[q] * next;
                 zb[q] = next;
                 nr += next * next;
@@ -933,10 +969,10 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
             }
 #pragma unroll
             for (int q = 0; q < 8; ++q)
-              if (i1 - q >= 0) z[(size_t)(i1 - q) * kMaxN] = zb[q];
+              if (k0 + q < cnt) z[(size_t)(bst + bdir * (k0 + q)) * kMaxN] = zb[q];
           }
-          sc = (nr > 0.0) ? 1.0 / sqrt(nr) : 0.0;
-          pscl[j] = sc;
+          nr += __shfl_xor_sync(pmask, nr, 1);
+          if (side == 0) pscl[j] = (nr > 0.0) ? 1.0 / sqrt(nr) : 0.0;
         }
         __syncthreads();
         if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[16] += t_ - t_iv; t_iv = t_; }
@@ -1005,7 +1041,18 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
                 double h = 0.0;
                 if (q < k) {
                   const int ia = warp * rpw, ib = min(N, ia + rpw);
-                  for (int i = ia; i < ib; ++i) h = fma(Zs[(size_t)i * kMaxN + q], zk[(size_t)i * kMaxN], h);
+                  int i = ia;
+                  for (; i + 8 <= ib; i += 8) {   // 8 independent load pairs in flight
+                    double za[8], zb[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                      za[u] = Zs[(size_t)(i + u) * kMaxN + q];
+                      zb[u] = zk[(size_t)(i + u) * kMaxN];
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) h = fma(za[u], zb[u], h);
+                  }
+                  for (; i < ib; ++i) h = fma(Zs[(size_t)i * kMaxN + q], zk[(size_t)i * kMaxN], h);
                 }
                 cpart[warp * kCpStride + q0 + lane] = h;
               }
@@ -1019,7 +1066,16 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
               for (int i = tid; i < N; i += kNT) {
                 double zi = zk[(size_t)i * kMaxN];
                 const double* zrow = Zs + (size_t)i * kMaxN + j0;
-                for (int q = 0; q < k - j0; ++q) zi = fma(-chq[q], zrow[q], zi);
+                const int nq = k - j0;
+                int q = 0;
+                for (; q + 8 <= nq; q += 8) {   // 8 independent loads in flight
+                  double zr8[8];
+#pragma unroll
+                  for (int u = 0; u < 8; ++u) zr8[u] = zrow[q + u];
+#pragma unroll
+                  for (int u = 0; u < 8; ++u) zi = fma(-chq[q + u], zr8[u], zi);
+                }
+                for (; q < nq; ++q) zi = fma(-chq[q], zrow[q], zi);
                 zk[(size_t)i * kMaxN] = zi;
               }
             }
@@ -1038,9 +1094,9 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
         }
         __syncthreads();
         if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[18] += t_ - t_iv; t_iv = t_; }
-        if (act) sc = pscl[j];
       }
-      if (act) pvec[j] = (T)sc;   // normalisation folded into the back-transform
+      for (int j = tid; j < JX; j += blockDim.x)
+        if (vact[j]) pvec[j] = (T)pscl[j];   // normalisation folded into the back-transform
     }
     // Rayleigh-Ritz inside the (rare) clusters that straddle a rule discontinuity:
     // H = Z_c^T T Z_c (fp64), cyclic Jacobi on H, Z_c <- Z_c Q (eigenvalues descending).
@@ -1134,10 +1190,23 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
       // ---------------- hand Z to bt_kernel (fd_bt.cu) ----------------
       // Wt scratch <- Z row-major [r][j] (ld 128; normalised, fp32; 0 for unused j);
       // w_j after the tridiagonal data in the Gram scratch
-      for (int x = tid; x < N * 128; x += blockDim.x) {
-        const int r = x >> 7, j = x & 127;
+      {  // thread -> fixed column j; 8 independent row loads in flight per batch
+        const int j = tid & 127, rs = blockDim.x >> 7;
         const bool a = (j < J) && (wgt[j] != T(0));
-        Wt[x] = a ? (T)(Zs[(size_t)r * kMaxN + j] * (double)pvec[j]) : T(0);
+        const double sc = a ? (double)pvec[j] : 0.0;
+        for (int r0 = tid >> 7; r0 < N; r0 += 8 * rs) {
+          double v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int r = r0 + q * rs;
+            v[q] = (a && r < N) ? Zs[(size_t)r * kMaxN + j] : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int r = r0 + q * rs;
+            if (r < N) Wt[r * 128 + j] = (T)(v[q] * sc);
+          }
+        }
       }
       {
         float* wout = reinterpret_cast<float*>(P.G) + (N * (N + 1) / 2 + 3) / 4 * 4 + 3 * N;

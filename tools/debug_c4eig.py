@@ -21,3 +21,4 @@ cnt = max(t[10], 1)
 print("P", P, "N", t[9], "problems(block0)", cnt, "avg clusters", t[7] / cnt, "max cluster", t[8],
       {names[i]: f"{t[i + 1] / cnt / 1.965e3:.1f}us" for i in range(6)})
 print("per kernel ms:", {k: (round(v[0], 2), v[1]) for k, v in prof.items()})
+print("invit sub-phases us/problem: solves %.1f warpMGS %.1f blockCGS %.1f" % tuple(t[k] / cnt / 1.965e3 for k in (16, 17, 18)))
