@@ -9,8 +9,9 @@
 // Z <- Q_b Z = Z - V_b (T_b (V_b^T Z)) is two GEMM-shaped products, applied from
 // the last block to the first.  One CTA per problem (persistent), Z resident in
 // shared memory (fp32), V_b streamed from the reflectors trd_kernel left in the
-// problem's Gram scratch; register-blocked FP32 SIMT products (FP32-accurate,
-// like the rest of the eigensolver).
+// problem's Gram scratch (register-prefetched one block ahead); register-blocked
+// FP32 SIMT products (FP32-accurate, like the rest of the eigensolver).  Per block,
+// one warp group forms V_b^T Z while the other forms V_b^T V_b and T.
 //
 // In:  P.G  = packed reflectors (column i rows i+2..N-1 at pk_off(i,N) + r - i),
 //             tau at off = round_up(N(N+1)/2, 4) + 2N, w_j at off + N;
@@ -25,26 +26,49 @@ namespace fdk {
 
 namespace {
 
-constexpr int kBtThreads = 512;    // two groups of 8 warps split the row range of each product
+constexpr int kBtThreads = 512;    // 16 warps: two groups of 8 overlap V^T Z with V^T V -> T
 constexpr int kNbBt = 32;          // reflectors per block
 constexpr int kZld = 132;          // Z row stride (floats): J <= 128, padded
-constexpr int kVld = kMaxNS + 1;    // V_b column stride (column-major, odd: conflict-free)
+constexpr int kVt = 36;            // V_b^T row stride: VbT[r][c] (16-byte aligned rows)
 
 __device__ __forceinline__ int pk_off_b(int c, int N) { return c * N - (c * (c - 1)) / 2; }
+
+__device__ __forceinline__ void bar_group1() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+// the 16 V_b entries one thread stages for block (i0, nb): column c = 2 warp + cc,
+// rows r0 + lane + 32 t (v_{i+1} = 1 implicit, rows above it 0, tau = 0 -> zero column)
+__device__ __forceinline__ void vb_fetch(float (&pf)[16], const float* __restrict__ V, const float* __restrict__ taug,
+                                         int i0, int nb, int N, int warp, int lane) {
+  const int r0 = i0 + 1;
+#pragma unroll
+  for (int cc = 0; cc < 2; ++cc) {
+    const int c = 2 * warp + cc, i = i0 + c;
+    const bool live = (c < nb) && (taug[i] != 0.f);
+    const int base = pk_off_b(i, N) - i;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int r = r0 + lane + 32 * t;
+      float v = 0.f;
+      if (live && r < N) v = (r == i + 1) ? 1.f : ((r > i + 1) ? V[base + r] : 0.f);
+      pf[8 * cc + t] = v;
+    }
+  }
+}
 
 }  // namespace
 
 __global__ void __launch_bounds__(kBtThreads, 1) bt_kernel(const Prob* __restrict__ probs, int count, Params p) {
   extern __shared__ __align__(16) float sm[];
   float* Zs = sm;                                  // [kMaxNS][kZld]
-  float* Vb = Zs + kMaxNS * kZld;                   // [32][kVld]   Vb[c][r] = v_{i0+c}[r]
-  float* W1 = Vb + kNbBt * kVld;                   // [32][128]
-  float* W2 = W1 + kNbBt * 128;                    // [32][128]  (also group 1's partial W1)
-  float* S = W2 + kNbBt * 128;                     // [32][33]  V^T V
-  float* Tm = S + kNbBt * 33;                      // [32][33]  T
-  float* tau = Tm + kNbBt * 33;                    // [32]
+  float* VbT = Zs + kMaxNS * kZld;                 // [kMaxNS][kVt]  VbT[r][c] = v_{i0+c}[r]
+  float* W1 = VbT + kMaxNS * kVt;                  // [32][128]  V^T Z
+  float* W2 = W1 + kNbBt * 128;                    // [32][128]  T V^T Z
+  float* S = W2 + kNbBt * 128;                     // [32][33]   V^T V
+  float* Tm = S + kNbBt * 33;                      // [32][33]   T
+  float* Yb = Tm + kNbBt * 33;                     // [256]      recursive-doubling scratch
+  float* tau = Yb + 256;                           // [32]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int grp = warp >> 3, wg8 = warp & 7;       // row-range group, warp within group
+  const int grp = warp >> 3, wg8 = warp & 7;
   const int ell = p.ell;
 
   for (int pi = blockIdx.x; pi < count; pi += gridDim.x) {
@@ -61,134 +85,129 @@ __global__ void __launch_bounds__(kBtThreads, 1) bt_kernel(const Prob* __restric
       const int r = x >> 5, j4 = 4 * (x & 31);
       *reinterpret_cast<float4*>(&Zs[r * kZld + j4]) = *reinterpret_cast<const float4*>(Wt + (int64_t)r * 128 + j4);
     }
-    __syncthreads();
     const int nref = N - 2;                        // reflectors 0..N-3
-    const int nblk = (nref + kNbBt - 1) / kNbBt;
+    const int nblk = nref > 0 ? (nref + kNbBt - 1) / kNbBt : 0;
+    float pf[16];
+    float tpf = 0.f;
+    if (nblk > 0) {
+      const int i0 = (nblk - 1) * kNbBt;
+      vb_fetch(pf, V, taug, i0, min(kNbBt, nref - i0), N, warp, lane);
+      if (tid < kNbBt) tpf = (tid < nref - i0) ? taug[i0 + tid] : 0.f;
+    }
     for (int b = nblk - 1; b >= 0; --b) {
       const int i0 = b * kNbBt, nb = min(kNbBt, nref - i0);
       const int r0 = i0 + 1;                       // rows < r0 of the block's vectors are 0
-      // ---- V_b (rows r0..N-1) and tau ----
-      for (int x = tid; x < kNbBt * (N - r0); x += kBtThreads) {
-        const int c = x / (N - r0), r = r0 + (x - c * (N - r0));
-        float v = 0.f;
-        if (c < nb && taug[i0 + c] != 0.f) {   // tau = 0: identity reflector -> zero column
-          const int i = i0 + c;
-          v = (r == i + 1) ? 1.f : ((r > i + 1) ? V[pk_off_b(i, N) + r - i] : 0.f);
+      // ---- stage V_b^T and tau (prefetched), then prefetch the next block ----
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int r = r0 + lane + 32 * t;
+          if (r < N) VbT[r * kVt + 2 * warp + cc] = pf[8 * cc + t];
         }
-        Vb[c * kVld + r] = v;
-      }
-      if (tid < kNbBt) {
-        const float t = (tid < nb) ? taug[i0 + tid] : 0.f;
-        tau[tid] = (t != 0.f) ? t : 1.f;   // zero columns of V_b: any nonzero tau (no effect)
-      }
+      if (tid < kNbBt) tau[tid] = (tpf != 0.f) ? tpf : 1.f;   // zero columns: any nonzero tau
       __syncthreads();
-      // ---- W1 = V_b^T Z and S = V_b^T V_b (one pass over the rows; group g takes
-      //      rows r0 + g, r0 + g + 2, ...; group 1's partials go to W2 / Tm) ----
-      {
+      if (b > 0) {
+        const int i0n = (b - 1) * kNbBt;
+        vb_fetch(pf, V, taug, i0n, kNbBt, N, warp, lane);
+        if (tid < kNbBt) tpf = taug[i0n + tid];
+      }
+      if (grp == 0) {
+        // ---- W1 = V_b^T Z (thread: 4 reflectors x 4 columns, all rows) ----
         const int cb = 4 * wg8, jb = 4 * lane;
         float acc[4][4] = {};
-        float sacc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 2
-        for (int r = r0 + grp; r < N; r += 2) {
+#pragma unroll 4
+        for (int r = r0; r < N; ++r) {
           const float4 zz = *reinterpret_cast<const float4*>(&Zs[r * kZld + jb]);
-          const float vl = Vb[lane * kVld + r];
-          float va[4];
+          const float4 vv = *reinterpret_cast<const float4*>(&VbT[r * kVt + cb]);
+          const float za[4] = {zz.x, zz.y, zz.z, zz.w}, va[4] = {vv.x, vv.y, vv.z, vv.w};
 #pragma unroll
-          for (int a = 0; a < 4; ++a) va[a] = Vb[(cb + a) * kVld + r];
-          const float za[4] = {zz.x, zz.y, zz.z, zz.w};
-#pragma unroll
-          for (int a = 0; a < 4; ++a) {
+          for (int a = 0; a < 4; ++a)
 #pragma unroll
             for (int q = 0; q < 4; ++q) acc[a][q] = fmaf(va[a], za[q], acc[a][q]);
-            sacc[a] = fmaf(va[a], vl, sacc[a]);
-          }
-        }
-        float* Wd = grp ? W2 : W1;
-        float* Sd = grp ? Tm : S;
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          *reinterpret_cast<float4*>(&Wd[(cb + a) * 128 + jb]) = make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
-          Sd[(cb + a) * 33 + lane] = sacc[a];
-        }
-      }
-      __syncthreads();
-      for (int x = tid; x < kNbBt * 128; x += kBtThreads) W1[x] += W2[x];
-      for (int x = tid; x < kNbBt * 32; x += kBtThreads) {
-        const int a = x >> 5, c = x & 31;
-        S[a * 33 + c] += Tm[a * 33 + c];
-      }
-      __syncthreads();
-      // ---- T = U^-1, U = diag(1/tau) + strict_upper(V_b^T V_b): the xLARFT forward
-      //      recurrence T[0:c,c] = -tau_c T[0:c,0:c] S[0:c,c] is exactly this inverse
-      //      (induction on c).  Recursive doubling: for block size h = 1, 2, .., 16 the
-      //      off-diagonal block of each 2h x 2h diagonal block is -T11 U12 T22. ----
-      for (int x = tid; x < kNbBt * 32; x += kBtThreads) {
-        const int a = x >> 5, c = x & 31;
-        Tm[a * 33 + c] = (a == c) ? tau[a] : 0.f;
-      }
-      __syncthreads();
-      for (int h = 1; h < kNbBt; h <<= 1) {
-        const int npair = kNbBt / (2 * h), nent = npair * h * h;
-        // Y = U12 T22 (U12 = S block, rows 2mh.., cols (2m+1)h..)
-        for (int x = tid; x < nent; x += kBtThreads) {
-          const int m = x / (h * h), e = x - m * h * h, i = e / h, j = e - (e / h) * h;
-          const int r1 = 2 * m * h, c2 = (2 * m + 1) * h;
-          float y = 0.f;
-          for (int k = 0; k < h; ++k) y = fmaf(S[(r1 + i) * 33 + c2 + k], Tm[(c2 + k) * 33 + c2 + j], y);
-          W2[x] = y;
-        }
-        __syncthreads();
-        // X = -T11 Y
-        for (int x = tid; x < nent; x += kBtThreads) {
-          const int m = x / (h * h), e = x - m * h * h, i = e / h, j = e - (e / h) * h;
-          const int r1 = 2 * m * h, c2 = (2 * m + 1) * h;
-          float t = 0.f;
-          for (int k = 0; k < h; ++k) t = fmaf(Tm[(r1 + i) * 33 + r1 + k], W2[m * h * h + k * h + j], t);
-          Tm[(r1 + i) * 33 + c2 + j] = -t;
-        }
-        __syncthreads();
-      }
-      // ---- W2 = T W1 (T upper triangular; group 0) ----
-      if (grp == 0) {
-        const int cb = 4 * wg8, jb = 4 * lane;
-        float acc[4][4] = {};
-        {
-          for (int k = cb; k < kNbBt; ++k) {
-            const float4 ww = *reinterpret_cast<const float4*>(&W1[k * 128 + jb]);
-            const float wa[4] = {ww.x, ww.y, ww.z, ww.w};
-#pragma unroll
-            for (int a = 0; a < 4; ++a) {
-              const float t = Tm[(cb + a) * 33 + k];
-#pragma unroll
-              for (int q = 0; q < 4; ++q) acc[a][q] = fmaf(t, wa[q], acc[a][q]);
-            }
-          }
         }
 #pragma unroll
         for (int a = 0; a < 4; ++a)
-          *reinterpret_cast<float4*>(&W2[(cb + a) * 128 + jb]) = make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
+          *reinterpret_cast<float4*>(&W1[(cb + a) * 128 + jb]) = make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
+      } else {
+        // ---- S = V_b^T V_b (thread: row a, columns c4..c4+3), then T = U^-1 ----
+        const int t = tid - 256, a = t >> 3, c4 = 4 * (t & 7);
+        float sa[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+        for (int r = r0; r < N; ++r) {
+          const float va = VbT[r * kVt + a];
+          const float4 vv = *reinterpret_cast<const float4*>(&VbT[r * kVt + c4]);
+          sa[0] = fmaf(va, vv.x, sa[0]); sa[1] = fmaf(va, vv.y, sa[1]);
+          sa[2] = fmaf(va, vv.z, sa[2]); sa[3] = fmaf(va, vv.w, sa[3]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          S[a * 33 + c4 + q] = sa[q];
+          Tm[a * 33 + c4 + q] = (a == c4 + q) ? tau[a] : 0.f;
+        }
+        bar_group1();
+        // U = diag(1/tau) + strict_upper(V_b^T V_b); the xLARFT forward recurrence
+        // T[0:c,c] = -tau_c T[0:c,0:c] S[0:c,c] is exactly T = U^-1 (induction on c).
+        // Recursive doubling: for h = 1, 2, .., 16 the off-diagonal block of each
+        // 2h x 2h diagonal block is -T11 U12 T22 (16 h entries, one per thread).
+#pragma unroll
+        for (int lh = 0; lh < 5; ++lh) {
+          const int h = 1 << lh;
+          const bool on = t < 16 * h;
+          const int m = t >> (2 * lh), e = t & (h * h - 1), i = e >> lh, j = e & (h - 1);
+          const int r1 = 2 * m * h, c2 = r1 + h;
+          if (on) {
+            float y = 0.f;
+            for (int k = 0; k < h; ++k) y = fmaf(S[(r1 + i) * 33 + c2 + k], Tm[(c2 + k) * 33 + c2 + j], y);
+            Yb[t] = y;
+          }
+          bar_group1();
+          if (on) {
+            float x = 0.f;
+            for (int k = 0; k < h; ++k) x = fmaf(Tm[(r1 + i) * 33 + r1 + k], Yb[(m << (2 * lh)) + k * h + j], x);
+            Tm[(r1 + i) * 33 + c2 + j] = -x;
+          }
+          bar_group1();
+        }
       }
       __syncthreads();
-      // ---- Z[r0:N, :] -= V_b W2 : thread = 4 rows x 4 columns per 32-row group ----
+      // ---- W2 = T W1 (T upper triangular; thread: 2 reflectors x 4 columns) ----
       {
-        const int rq = warp, jb = 4 * lane;   // 16 warps x 4 rows per 64-row sweep
+        const int a0 = 2 * warp, jb = 4 * lane;
+        float acc[2][4] = {};
+        for (int k = a0; k < kNbBt; ++k) {
+          const float4 ww = *reinterpret_cast<const float4*>(&W1[k * 128 + jb]);
+          const float t0 = Tm[a0 * 33 + k], t1 = (k > a0) ? Tm[(a0 + 1) * 33 + k] : 0.f;
+          acc[0][0] = fmaf(t0, ww.x, acc[0][0]); acc[0][1] = fmaf(t0, ww.y, acc[0][1]);
+          acc[0][2] = fmaf(t0, ww.z, acc[0][2]); acc[0][3] = fmaf(t0, ww.w, acc[0][3]);
+          acc[1][0] = fmaf(t1, ww.x, acc[1][0]); acc[1][1] = fmaf(t1, ww.y, acc[1][1]);
+          acc[1][2] = fmaf(t1, ww.z, acc[1][2]); acc[1][3] = fmaf(t1, ww.w, acc[1][3]);
+        }
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+          *reinterpret_cast<float4*>(&W2[(a0 + a) * 128 + jb]) = make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
+      }
+      __syncthreads();
+      // ---- Z[r0:N, :] -= V_b W2 : thread = 8 rows x 4 columns, warp = 8 rows ----
+      {
+        const int jb = 4 * lane;
         if (jb < Jp) {  // columns >= Jp of Z are zero
-          for (int rbase = r0 + 4 * rq; rbase < N; rbase += 4 * (kBtThreads / 32)) {
-            float acc[4][4] = {};
+          for (int rbase = r0 + 8 * warp; rbase < N; rbase += 8 * (kBtThreads / 32)) {
+            float acc[8][4] = {};
 #pragma unroll 4
-            for (int k = 0; k < nb; ++k) {
-              const float4 ww = *reinterpret_cast<const float4*>(&W2[k * 128 + jb]);
-              const float wa[4] = {ww.x, ww.y, ww.z, ww.w};
+            for (int k = 0; k < kNbBt; ++k) {
+              const float4 w4 = *reinterpret_cast<const float4*>(&W2[k * 128 + jb]);
 #pragma unroll
-              for (int a = 0; a < 4; ++a) {
-                const int r = rbase + a;
-                const float v = (r < N) ? Vb[k * kVld + r] : 0.f;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) acc[a][q] = fmaf(v, wa[q], acc[a][q]);
+              for (int a = 0; a < 8; ++a) {
+                const float v = VbT[(rbase + a) * kVt + k];   // rows >= N: never stored
+                acc[a][0] = fmaf(v, w4.x, acc[a][0]);
+                acc[a][1] = fmaf(v, w4.y, acc[a][1]);
+                acc[a][2] = fmaf(v, w4.z, acc[a][2]);
+                acc[a][3] = fmaf(v, w4.w, acc[a][3]);
               }
             }
 #pragma unroll
-            for (int a = 0; a < 4; ++a) {
+            for (int a = 0; a < 8; ++a) {
               const int r = rbase + a;
               if (r < N) {
                 float4 z = *reinterpret_cast<float4*>(&Zs[r * kZld + jb]);
@@ -201,9 +220,10 @@ __global__ void __launch_bounds__(kBtThreads, 1) bt_kernel(const Prob* __restric
       }
       __syncthreads();
     }
+    __syncthreads();
     // ---- Wt[j][r] = w_j U[r][j], transposed through per-warp 32 x 33 smem tiles ----
     {
-      float* tile = Vb + warp * 32 * 33;   // V_b / W1 / W2 are free now (16 x 4.1 KB)
+      float* tile = VbT + warp * 32 * 33;   // V_b^T / W1 / W2 are free now
       const int ntr = (N + 31) / 32, ntj = (J + 31) / 32;
       for (int t = warp; t < ntr * ntj; t += kBtThreads / 32) {
         const int rt = t / ntj, jt = t - rt * ntj;
@@ -225,7 +245,7 @@ __global__ void __launch_bounds__(kBtThreads, 1) bt_kernel(const Prob* __restric
 }
 
 size_t bt_smem_bytes() {
-  return sizeof(float) * ((size_t)kMaxNS * kZld + (size_t)kNbBt * kVld + 2 * kNbBt * 128 + 2 * kNbBt * 33 + kNbBt);
+  return sizeof(float) * ((size_t)kMaxNS * kZld + (size_t)kMaxNS * kVt + 2 * kNbBt * 128 + 2 * kNbBt * 33 + 256 + kNbBt);
 }
 
 bool bt_supported(int nmax, const Params& p) { return p.pretrd && nmax <= kMaxNS && p.ell - 1 <= 128; }
