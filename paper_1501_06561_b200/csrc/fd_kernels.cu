@@ -15,6 +15,7 @@
 // iteration (with modified Gram-Schmidt inside eigenvalue clusters) for the
 // ell-1 retained eigenvectors, and a fp32 Householder back-transform.
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <float.h>
 #include <math.h>
 #include <stdint.h>
@@ -304,9 +305,122 @@ __global__ void __launch_bounds__(256, 2) recon128_kernel(const Prob* __restrict
   }
 }
 
+// Reconstruct, pipelined variant (fp32, ldg % 4 == 0, ldb % 4 == 0): same product as
+// recon128_kernel with a 4-stage cp.async pipeline (BK = 16).  A keeps its [j][k]
+// layout in shared memory and is read as k-pairs; thread rows are ty + 16 i and
+// columns 4 tx + 64 h, so every shared-memory read is conflict-free.
+namespace {
+constexpr int kRcBK = 16, kRcStages = 4, kRcALd = 20, kRcBLd = 128;
+constexpr int kRcStageFloats = 128 * kRcALd + kRcBK * kRcBLd;
+
+__device__ __forceinline__ void cp_async16(float* dst, const float* src, int bytes) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory"); }
+}  // namespace
+
+__global__ void __launch_bounds__(256, 2) recon_pipe_kernel(const Prob* __restrict__ probs, Params p) {
+  const Prob P = probs[blockIdx.z];
+  const int N = P.rows0 + P.rows1;
+  const int n0 = blockIdx.x * 128, j0 = blockIdx.y * 128;
+  const int jrows = p.ell - 1;
+  if (j0 >= p.ell) return;
+  extern __shared__ __align__(16) float rsm[];
+  const float* Wt = static_cast<const float*>(P.Wt);
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int nk = (N + kRcBK - 1) / kRcBK;
+  // loader: A chunks (row tid >> 2 and 64 + (tid >> 2), k-quad tid & 3); B chunks
+  // (k-row tid >> 5 and 8 + (tid >> 5), column quad tid & 31)
+  auto issue = [&](int kt) {
+    float* As = rsm + (kt % kRcStages) * kRcStageFloats;
+    float* Bs = As + 128 * kRcALd;
+    const int k0 = kt * kRcBK;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int m = (tid >> 2) + 64 * h, kq = 4 * (tid & 3), k = k0 + kq, j = j0 + m;
+      const int bytes = (j < jrows && k < N) ? 4 * min(4, N - k) : 0;
+      const float* src = bytes ? Wt + (int64_t)j * p.ldg + k : Wt;
+      cp_async16(As + m * kRcALd + kq, src, bytes);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int kr = (tid >> 5) + 8 * h, nq = 4 * (tid & 31), k = k0 + kr, n = n0 + nq;
+      const bool ok = k < N && n < p.ldb;
+      const float* src = ok ? prob_row(P, k, p.ldb) + n : Wt;
+      cp_async16(Bs + kr * kRcBLd + nq, src, ok ? 16 : 0);
+    }
+  };
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+#pragma unroll
+  for (int st = 0; st < kRcStages - 1; ++st) {
+    if (st < nk) issue(st);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<kRcStages - 2>();
+    __syncthreads();
+    if (kt + kRcStages - 1 < nk) issue(kt + kRcStages - 1);
+    cp_async_commit();
+    const float* As = rsm + (kt % kRcStages) * kRcStageFloats;
+    const float* Bs = As + 128 * kRcALd;
+#pragma unroll
+    for (int kk = 0; kk < kRcBK; kk += 2) {
+      float2 a[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float2*>(&As[(ty + 16 * i) * kRcALd + kk]);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const float4 b0 = *reinterpret_cast<const float4*>(&Bs[(kk + u) * kRcBLd + 4 * tx]);
+        const float4 b1 = *reinterpret_cast<const float4*>(&Bs[(kk + u) * kRcBLd + 64 + 4 * tx]);
+        const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float av = u ? a[i].y : a[i].x;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av, bb[j], acc[i][j]);
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int j = j0 + ty + 16 * i;
+    if (j >= p.ell) continue;
+    float* dst = P.dst + (int64_t)j * p.ldb + n0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = 64 * h + 4 * tx;
+      if (n0 + c >= p.ldb) continue;
+      const float4 o = (j < jrows) ? make_float4(acc[i][4 * h], acc[i][4 * h + 1], acc[i][4 * h + 2], acc[i][4 * h + 3])
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(dst + c) = o;
+    }
+  }
+}
+
 cudaError_t launch_recon(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
   (void)nmax;
+  if (!p.f64 && (p.ldg % 4) == 0 && (p.ldb % 4) == 0 && !getenv("FD_RECON128")) {
+    constexpr int dyn = kRcStages * kRcStageFloats * (int)sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(recon_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    dim3 grid((unsigned)((p.ldb + 127) / 128), (unsigned)((p.ell + 127) / 128), count);
+    recon_pipe_kernel<<<grid, 256, dyn, s>>>(dev_probs, p);
+    return cudaGetLastError();
+  }
   if (!p.f64 && (p.ldg % 4) == 0) {
     dim3 grid((unsigned)((p.ldb + 127) / 128), (unsigned)((p.ell + 127) / 128), count);
     recon128_kernel<<<grid, 256, 0, s>>>(dev_probs, p);
