@@ -60,6 +60,10 @@ def lib():
                                      ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                      ctypes.c_void_p]
         L.oracle_cov_err.restype = ctypes.c_int
+        L.oracle_proj_err.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                      ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                      ctypes.c_int, ctypes.c_void_p]
+        L.oracle_proj_err.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -196,3 +200,25 @@ def cov_err(A, B, nthreads=0, jacobi_max=512, kmax=512):
     if rc:
         raise RuntimeError(f"oracle_cov_err rc={rc}")
     return dict(err=out[0], lmax=out[1], lmin=out[2], frob=out[3])
+
+
+def proj_err(A, B, k=10, nthreads=0, jacobi_max=512, kmax=512):
+    """proj-err (k = 10 per PAPER.md:572) =
+    ||A - pi_{B_k}(A)||_F^2 / ||A - A_k||_F^2, B_k = top-k right singular subspace of B.
+
+    Returns dict(err, num, den, frob): num = ||A - pi_{B_k}(A)||_F^2, den = ||A - A_k||_F^2."""
+    A = np.ascontiguousarray(A, dtype=np.float32)
+    B = np.ascontiguousarray(B, dtype=np.float64)
+    n, d = A.shape
+    if B.ndim != 2 or B.shape[1] != d:
+        raise ValueError("B must be ell x d")
+    out = np.zeros(4)
+    rc = lib().oracle_proj_err(A.ctypes.data, n, d, d, B.ctypes.data, B.shape[0], int(k), _nthreads(nthreads),
+                               jacobi_max, kmax, out.ctypes.data)
+    if rc == -4:
+        raise ValueError("||A||_F^2 = 0: proj-err undefined")
+    if rc == -5:
+        raise ValueError("||A - A_k||_F^2 = 0 (rank A <= k): proj-err undefined")
+    if rc:
+        raise RuntimeError(f"oracle_proj_err rc={rc}")
+    return dict(err=out[0], num=out[1], den=out[2], frob=out[3])

@@ -529,3 +529,132 @@ int oracle_cov_err(const float* A, int64_t n, int64_t lda, int64_t d, const doub
   free(M);
   return rc;
 }
+
+/* Ritz values of Lanczos (full re-orthogonalisation, as oracle_lanczos_extremes)
+ * on symmetric M, the top `ntop` of them descending into top[].  Returns the
+ * number of Lanczos steps, or -1. */
+static int lanczos_top(const double* M, int64_t d, int kmax, int ntop, double* top) {
+  int k = (int)(kmax < d ? kmax : d);
+  double* Q = calloc((size_t)(k + 1) * d, sizeof(double));
+  double* alpha = calloc(k, sizeof(double));
+  double* beta = calloc(k + 1, sizeof(double));
+  double* z = malloc(sizeof(double) * d);
+  double nrm = 0.0;
+  for (int64_t i = 0; i < d; ++i) { Q[i] = 1.0 + 0.001 * (double)((i * 7919) % 101); nrm += Q[i] * Q[i]; }
+  nrm = sqrt(nrm);
+  for (int64_t i = 0; i < d; ++i) Q[i] /= nrm;
+  int steps = 0;
+  for (int j = 0; j < k; ++j) {
+    const double* q = Q + (size_t)j * d;
+    for (int64_t r = 0; r < d; ++r) {
+      double s = 0.0;
+      for (int64_t c = 0; c < d; ++c) s += M[r * d + c] * q[c];
+      z[r] = s;
+    }
+    double a = 0.0;
+    for (int64_t r = 0; r < d; ++r) a += q[r] * z[r];
+    alpha[j] = a;
+    for (int pass = 0; pass < 2; ++pass)
+      for (int i = 0; i <= j; ++i) {
+        const double* qi = Q + (size_t)i * d;
+        double h = 0.0;
+        for (int64_t r = 0; r < d; ++r) h += qi[r] * z[r];
+        for (int64_t r = 0; r < d; ++r) z[r] -= h * qi[r];
+      }
+    double b = 0.0;
+    for (int64_t r = 0; r < d; ++r) b += z[r] * z[r];
+    b = sqrt(b);
+    steps = j + 1;
+    beta[j + 1] = b;
+    if (b <= 1e-13 * (fabs(a) + 1e-300) || j + 1 == k) break;
+    double* qn = Q + (size_t)(j + 1) * d;
+    for (int64_t r = 0; r < d; ++r) qn[r] = z[r] / b;
+  }
+  double* T = calloc((size_t)steps * steps, sizeof(double));
+  double* V = malloc(sizeof(double) * steps * steps);
+  double* w = malloc(sizeof(double) * steps);
+  int* ord = malloc(sizeof(int) * steps);
+  for (int i = 0; i < steps; ++i) {
+    T[(size_t)i * steps + i] = alpha[i];
+    if (i + 1 < steps) { T[(size_t)i * steps + i + 1] = beta[i + 1]; T[(size_t)(i + 1) * steps + i] = beta[i + 1]; }
+  }
+  int rc = oracle_jacobi_eig(T, steps, w, V) < 0 ? -1 : steps;
+  sort_desc(w, steps, ord);
+  for (int t = 0; t < ntop; ++t) top[t] = (t < steps) ? w[ord[t]] : 0.0;
+  free(Q); free(alpha); free(beta); free(z); free(T); free(V); free(w); free(ord);
+  return rc;
+}
+
+/* proj-err (k = 10 in the experiments):
+ *   proj-err(A, B) = ||A - pi_{B_k}(A)||_F^2 / ||A - A_k||_F^2.
+ * B_k = span of the top-k right singular vectors of B ("the best rank k subspace
+ * described by B"), from the Jacobi eigen-decomposition of B B^T = U S^2 U^T:
+ * v_j = B^T u_j / s_j for the top min(k, rank B) values (s_j^2 > 1e-12 s_1^2).
+ * With V_k orthonormal, ||A - A V_k V_k^T||_F^2 = ||A||_F^2 - sum_j v_j^T (A^T A) v_j,
+ * and ||A - A_k||_F^2 = ||A||_F^2 - sum_{j<=k} lambda_j(A^T A) (Eckart-Young), the
+ * top-k eigenvalues by full Jacobi when d <= jacobi_max, else Lanczos Ritz values.
+ * B: ell x d fp64 row-major.  out4 = {proj_err, numerator, denominator, frob}.
+ * Returns 0, -4 (||A||_F = 0), -5 (||A - A_k||_F = 0: undefined), -1. */
+int oracle_proj_err(const float* A, int64_t n, int64_t lda, int64_t d, const double* B, int ell, int k,
+                    int nthreads, int jacobi_max, int kmax, double* out4) {
+  double* M = malloc(sizeof(double) * d * d);
+  double frob = 0.0;
+  oracle_gram(A, n, lda, d, nthreads, M, &frob);
+  if (frob <= 0.0) { free(M); return -4; }
+  /* B B^T and its eigen-decomposition */
+  double* G = malloc(sizeof(double) * ell * ell);
+  double* U = malloc(sizeof(double) * ell * ell);
+  double* s2 = malloc(sizeof(double) * ell);
+  int* ord = malloc(sizeof(int) * ell);
+  for (int i = 0; i < ell; ++i)
+    for (int j = 0; j < ell; ++j) {
+      double s = 0.0;
+      for (int64_t c = 0; c < d; ++c) s += B[(size_t)i * d + c] * B[(size_t)j * d + c];
+      G[(size_t)i * ell + j] = s;
+    }
+  int rc = oracle_jacobi_eig(G, ell, s2, U) < 0 ? -1 : 0;
+  sort_desc(s2, ell, ord);
+  double captured = 0.0;
+  double* v = malloc(sizeof(double) * d);
+  const double smax = ell > 0 ? s2[ord[0]] : 0.0;
+  for (int t = 0; t < k && t < ell; ++t) {
+    const int j = ord[t];
+    if (!(s2[j] > 1e-12 * smax) || s2[j] <= 0.0) break;
+    const double inv = 1.0 / sqrt(s2[j]);
+    for (int64_t c = 0; c < d; ++c) {
+      double x = 0.0;
+      for (int i = 0; i < ell; ++i) x += B[(size_t)i * d + c] * U[(size_t)i * ell + j];
+      v[c] = x * inv;
+    }
+    double q = 0.0;
+    for (int64_t r = 0; r < d; ++r) {
+      double mv = 0.0;
+      for (int64_t c = 0; c < d; ++c) mv += M[r * d + c] * v[c];
+      q += v[r] * mv;
+    }
+    captured += q;
+  }
+  /* top-k eigenvalues of A^T A */
+  double* top = calloc(k > 0 ? k : 1, sizeof(double));
+  if (d <= jacobi_max) {
+    double* Mc = malloc(sizeof(double) * d * d);
+    double* W = malloc(sizeof(double) * d * d);
+    double* w = malloc(sizeof(double) * d);
+    int* o2 = malloc(sizeof(int) * d);
+    memcpy(Mc, M, sizeof(double) * d * d);
+    if (oracle_jacobi_eig(Mc, (int)d, w, W) < 0) rc = -1;
+    sort_desc(w, (int)d, o2);
+    for (int t = 0; t < k; ++t) top[t] = (t < d) ? w[o2[t]] : 0.0;
+    free(Mc); free(W); free(w); free(o2);
+  } else if (lanczos_top(M, d, kmax, k, top) < 0) {
+    rc = -1;
+  }
+  double best = 0.0;
+  for (int t = 0; t < k; ++t) best += top[t];
+  const double num = frob - captured, den = frob - best;
+  out4[0] = (den > 0.0) ? num / den : 0.0;
+  out4[1] = num; out4[2] = den; out4[3] = frob;
+  if (rc == 0 && !(den > 0.0)) rc = -5;
+  free(M); free(G); free(U); free(s2); free(ord); free(v); free(top);
+  return rc;
+}

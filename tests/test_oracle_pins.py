@@ -343,3 +343,68 @@ def test_paper_qualitative_order_c2():
         errs[v] = oracle.cov_err(A, r.B)["err"]
     assert errs["fd"] > errs["alpha_fd"] and errs["fd"] > errs["isvd"]
     assert errs["fd"] <= 1 / 20
+
+
+# ---------------------------------------------------------------------------
+# proj-err (k = 10)
+# ---------------------------------------------------------------------------
+def _orth(rng, n):
+    q, r = np.linalg.qr(rng.standard_normal((n, n)))
+    return q * np.sign(np.diag(r))
+
+
+def test_proj_err_closed_form_rotated():
+    """A = U diag(s) V^T, B = rows t_i v_i^T for i in S1 (large t) and S2 (small t):
+    B_k = span{v_i : i in S1}, so ||A - pi_{B_k}(A)||_F^2 = sum_{i not in S1} s_i^2 and
+    ||A - A_k||_F^2 = sum_{i >= k} s_i^2 (s sorted descending).  A transposed operand,
+    left instead of right singular vectors, or a wrong top-k order all fail this."""
+    rng = np.random.default_rng(7)
+    d, k = 24, 4
+    s = np.sort(rng.uniform(1.0, 10.0, d))[::-1]
+    U, V = _orth(rng, d), _orth(rng, d)
+    A = (U * s) @ V.T
+    S1 = [1, 5, 9, 20]                    # not the top-k of A
+    S2 = [0, 3, 7]                        # in B but with smaller weights
+    rows = [30.0 * (j + 1) * V[:, i] for j, i in enumerate(S1)] + [0.5 * V[:, i] for i in S2]
+    B = np.array(rows[::-1])              # row order must not matter
+    Af = A.astype(np.float32)
+    s32 = np.linalg.svd(Af.astype(np.float64), compute_uv=False)
+    r = oracle.proj_err(Af, B, k=k)
+    Vf = V[:, S1]
+    num = float(np.sum(Af.astype(np.float64) ** 2)) - float(np.sum((Af.astype(np.float64) @ Vf) ** 2))
+    den = float(np.sum(s32[k:] ** 2))
+    assert abs(r["num"] - num) < 1e-9 * r["frob"]
+    assert abs(r["den"] - den) < 1e-9 * r["frob"]
+    expect = float(np.sum(np.delete(s, S1) ** 2) / np.sum(s[k:] ** 2))
+    assert abs(r["err"] - expect) < 1e-5 * expect
+
+
+def test_proj_err_of_A_itself_is_one_and_random_B_at_least_one():
+    """B = A: B_k = A_k's subspace -> proj-err = 1; any B -> proj-err >= 1 (A_k optimal)."""
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((60, 20)).astype(np.float32)
+    r = oracle.proj_err(A, A.astype(np.float64), k=5)
+    assert abs(r["err"] - 1.0) < 1e-10
+    for seed in range(3):
+        B = np.random.default_rng(seed).standard_normal((8, 20))
+        assert oracle.proj_err(A, B, k=5)["err"] >= 1.0 - 1e-12
+
+
+def test_proj_err_fd_bound_and_lanczos_path():
+    """FD sketch of c1: 1 <= proj-err <= ell/(ell - k) (Theorem of
+    PAPER.md:374-377 at alpha = 1); the Lanczos top-k path agrees with full Jacobi."""
+    A = _c1()
+    ell, k = 16, 10
+    r = oracle.sketch(A, ell, "fd")
+    p = oracle.proj_err(A, r.B, k=k)
+    assert 1.0 - 1e-12 <= p["err"] <= ell / (ell - k)
+    p2 = oracle.proj_err(A, r.B, k=k, jacobi_max=0, kmax=64)
+    assert abs(p2["err"] - p["err"]) < 1e-9 * p["err"]
+
+
+def test_proj_err_undefined_cases():
+    with pytest.raises(ValueError):
+        oracle.proj_err(np.zeros((3, 4), np.float32), np.zeros((2, 4)), k=1)
+    A = np.zeros((5, 6), np.float32); A[0, 0] = 1.0; A[1, 2] = 2.0      # rank 2 <= k
+    with pytest.raises(ValueError):
+        oracle.proj_err(A, np.ones((2, 6)), k=2)
