@@ -191,6 +191,34 @@ fd_status fd_cov_err(const float* A, int64_t n, int64_t ld, const float* B, int3
                      double* err, double* lam_max, double* lam_min,
                      void* ws, size_t ws_bytes, void* cuda_stream);
 
+/* ---- proj-err -------------------------------------------
+ * proj-err(A, B) = ||A - pi_{B_k}(A)||_F^2 / ||A - A_k||_F^2   (the
+ * paper uses k = 10).  B_k = span of the top-k right singular
+ * vectors of B (fewer if rank B < k: singular values with s^2 <= 1e-12 s_1^2 are
+ * dropped), found from B B^T = U S^2 U^T (fp64, parallel-ordering Jacobi) as
+ * v_j = B^T u_j / s_j.  Numerator = frob_sq - sum_j v_j^T AtA v_j; denominator =
+ * frob_sq - sum_{j<=k} lambda_j(AtA) with the top-k eigenvalues as Lanczos Ritz
+ * values (min(d, 512) steps, full re-orthogonalisation; a top-k eigenvalue of
+ * exact multiplicity > 1 is found once: DESIGN.md reading E2). */
+
+/* Workspace bytes for fd_proj_err_from_gram / fd_proj_err (d, ell, k as passed). */
+size_t fd_proj_workspace_bytes(int64_t d, int32_t ell, int32_t k);
+
+/* proj-err of B [device] (ell x d fp32, ld = d) from AtA [device] (d x d fp64 as
+ * produced by fd_cov_gram_partial, summed over ranks) and frob_sq = ||A||_F^2
+ * [host].  Outputs [host]: proj_err, num = ||A - pi_{B_k}(A)||_F^2 and
+ * den = ||A - A_k||_F^2 (either may be NULL except proj_err).  1 <= k <= d.
+ * Synchronises.  Errors: INVALID_ARG, ZERO_NORM (frob_sq <= 0, or den <= 0:
+ * rank A <= k), WORKSPACE, CUDA. */
+fd_status fd_proj_err_from_gram(const double* AtA, const float* B, int32_t ell, int64_t d, double frob_sq,
+                                int32_t k, double* proj_err, double* num, double* den,
+                                void* ws, size_t ws_bytes, void* cuda_stream);
+
+/* Single-GPU convenience: AtA from A [device] (fp32, ld), frob_sq = trace(A^T A),
+ * then fd_proj_err_from_gram.  ws must hold fd_proj_workspace_bytes + d*d*8. */
+fd_status fd_proj_err(const float* A, int64_t n, int64_t ld, const float* B, int32_t ell, int64_t d, int32_t k,
+                      double* proj_err, void* ws, size_t ws_bytes, void* cuda_stream);
+
 /* Thread-local message for the last error on this thread ("" if none). */
 const char* fd_last_error(void);
 

@@ -16,7 +16,7 @@ import ctypes
 
 from ._lib import FD_MAX_N, VARIANT, FdConfig, FdError, FdStats, check, lib
 
-__all__ = ["Sketcher", "cov_err", "cov_gram_partial", "cov_err_from_gram", "FdError", "VARIANT", "FD_MAX_N",
+__all__ = ["Sketcher", "cov_err", "cov_gram_partial", "cov_err_from_gram", "proj_err", "proj_err_from_gram", "FdError", "VARIANT", "FD_MAX_N",
            "is_batched"]
 
 
@@ -191,3 +191,35 @@ def cov_err(A, B, stream=None):
                            ctypes.byref(hi), ctypes.byref(lo), ws.data_ptr(), n, s.cuda_stream))
     frob = None
     return dict(err=err.value, lmax=hi.value, lmin=lo.value, frob=frob)
+
+
+def proj_err_from_gram(AtA, B, frob_sq, k=10, stream=None):
+    """proj-err (k = 10 per PAPER.md:572) of sketch B (ell x d cuda fp32)
+    from AtA (d x d cuda fp64, fd_cov_gram_partial) and frob_sq = ||A||_F^2."""
+    torch = _torch()
+    d = AtA.shape[0]
+    B = B.contiguous()
+    n = lib().fd_proj_workspace_bytes(int(d), int(B.shape[0]), int(k))
+    ws = torch.empty(max(n, 1), dtype=torch.uint8, device=AtA.device)
+    s = stream if stream is not None else torch.cuda.current_stream(AtA.device)
+    pe, nu, de = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    check(lib().fd_proj_err_from_gram(AtA.data_ptr(), B.data_ptr(), B.shape[0], d, float(frob_sq), int(k),
+                                      ctypes.byref(pe), ctypes.byref(nu), ctypes.byref(de), ws.data_ptr(), n,
+                                      s.cuda_stream))
+    return dict(err=pe.value, num=nu.value, den=de.value, frob=float(frob_sq))
+
+
+def proj_err(A, B, k=10, stream=None):
+    """proj-err of sketch B (ell x d) for rows A (n x d), both cuda fp32."""
+    torch = _torch()
+    d = B.shape[1]
+    A = _as_rows(A, d)
+    B = B.contiguous()
+    n = lib().fd_proj_workspace_bytes(int(d), int(B.shape[0]), int(k))
+    nb = n + (d * d * 8 + 255) // 256 * 256
+    ws = torch.empty(nb, dtype=torch.uint8, device=A.device)
+    s = stream if stream is not None else torch.cuda.current_stream(A.device)
+    pe = ctypes.c_double()
+    check(lib().fd_proj_err(A.data_ptr(), A.shape[0], A.stride(0), B.data_ptr(), B.shape[0], d, int(k),
+                            ctypes.byref(pe), ws.data_ptr(), nb, s.cuda_stream))
+    return dict(err=pe.value)

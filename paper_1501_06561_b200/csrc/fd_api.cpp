@@ -749,6 +749,89 @@ fd_status fd_cov_err(const float* A, int64_t n, int64_t ld, const float* B, int3
   return fd_cov_err_from_gram(AtA, B, ell, d, frob, err, lam_max, lam_min, ws, ws_bytes, cuda_stream);
 }
 
+// ---- proj-err (fd_eval.cu) ----
+namespace {
+struct ProjLayout {
+  size_t G, V, w, ord, sweeps, vbuf, q, Q, work, out, top, total;
+};
+ProjLayout proj_layout(int64_t d, int32_t ell, int32_t k) {
+  ProjLayout L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, kAlign); return o; };
+  const int kl = lanczos_k(d);
+  L.G = take((size_t)ell * ell * sizeof(double));
+  L.V = take((size_t)ell * ell * sizeof(double));
+  L.w = take((size_t)ell * sizeof(double));
+  L.ord = take((size_t)ell * sizeof(int));
+  L.sweeps = take(sizeof(int));
+  L.vbuf = take((size_t)k * d * sizeof(double));
+  L.q = take((size_t)k * sizeof(double));
+  L.Q = take((size_t)(kl + 1) * d * sizeof(double));
+  L.work = take((size_t)(2 * kl + 2 + d + kl + 64) * sizeof(double));
+  L.out = take(2 * sizeof(double));
+  L.top = take((size_t)k * sizeof(double));
+  L.total = off;
+  return L;
+}
+}  // namespace
+
+size_t fd_proj_workspace_bytes(int64_t d, int32_t ell, int32_t k) {
+  if (d < 1 || ell < 1 || k < 1) return 0;
+  return proj_layout(d, ell, k).total;
+}
+
+fd_status fd_proj_err_from_gram(const double* AtA, const float* B, int32_t ell, int64_t d, double frob_sq, int32_t k,
+                                double* proj_err, double* num, double* den, void* ws, size_t ws_bytes,
+                                void* cuda_stream) {
+  if (!AtA || !B || !proj_err || ell < 1 || d < 1 || k < 1 || k > d) return fail(FD_ERR_INVALID_ARG, "bad argument");
+  if (!(frob_sq > 0.0)) return fail(FD_ERR_ZERO_NORM, "||A||_F^2 = 0: proj-err undefined");
+  const ProjLayout L = proj_layout(d, ell, k);
+  if (!ws || ws_bytes < L.total) return fail(FD_ERR_WORKSPACE, "proj-err workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+  char* w = static_cast<char*>(ws);
+  auto D = [&](size_t o) { return reinterpret_cast<double*>(w + o); };
+  cudaError_t e = fdk::launch_proj_parts(B, ell, d, k, AtA, D(L.G), D(L.V), D(L.w), reinterpret_cast<int*>(w + L.ord),
+                                         reinterpret_cast<int*>(w + L.sweeps), D(L.vbuf), D(L.q), s);
+  if (e != cudaSuccess) return cuda_fail(e, "proj-err parts");
+  e = fdk::launch_lanczos(AtA, d, lanczos_k(d), D(L.Q), D(L.work), D(L.out), s, k, D(L.top));
+  if (e != cudaSuccess) return cuda_fail(e, "lanczos top-k");
+  std::vector<double> q(k), top(k);
+  e = cudaMemcpyAsync(q.data(), D(L.q), k * sizeof(double), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(top.data(), D(L.top), k * sizeof(double), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "proj-err result");
+  double cap = 0.0, best = 0.0;
+  for (int t = 0; t < k; ++t) { cap += q[t]; best += top[t]; }
+  const double nu = frob_sq - cap, de = frob_sq - best;
+  if (num) *num = nu;
+  if (den) *den = de;
+  if (!(de > 0.0)) return fail(FD_ERR_ZERO_NORM, "||A - A_k||_F^2 = 0 (rank A <= k): proj-err undefined");
+  *proj_err = nu / de;
+  return FD_OK;
+}
+
+fd_status fd_proj_err(const float* A, int64_t n, int64_t ld, const float* B, int32_t ell, int64_t d, int32_t k,
+                      double* proj_err, void* ws, size_t ws_bytes, void* cuda_stream) {
+  if (!A || !B || !proj_err || d < 1 || ell < 1 || k < 1) return fail(FD_ERR_INVALID_ARG, "bad argument");
+  const size_t pb = fd_proj_workspace_bytes(d, ell, k);
+  const size_t ab = align_up((size_t)d * d * sizeof(double), kAlign);
+  if (!ws || ws_bytes < pb + ab) return fail(FD_ERR_WORKSPACE, "proj-err workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+  double* AtA = reinterpret_cast<double*>(static_cast<char*>(ws) + pb);
+  cudaError_t e = cudaMemsetAsync(AtA, 0, (size_t)d * d * sizeof(double), s);
+  if (e != cudaSuccess) return cuda_fail(e, "memset");
+  fd_status st = fd_cov_gram_partial(A, n, ld, d, AtA, nullptr, 0, cuda_stream);
+  if (st != FD_OK) return st;
+  std::vector<double> diag(d);
+  e = cudaMemcpy2DAsync(diag.data(), sizeof(double), AtA, (d + 1) * sizeof(double), sizeof(double), d,
+                        cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "trace");
+  double frob = 0.0;
+  for (double x : diag) frob += x;
+  return fd_proj_err_from_gram(AtA, B, ell, d, frob, k, proj_err, nullptr, nullptr, ws, pb, cuda_stream);
+}
+
 const char* fd_last_error(void) { return g_err.c_str(); }
 
 // debug: copy the phase trace (32 x int64, CTA 0 of the eig / trd kernels; FD_DEBUG_EIG set)

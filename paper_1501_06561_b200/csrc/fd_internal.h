@@ -82,6 +82,9 @@ cudaError_t launch_bt(const Prob* dev_probs, int count, const Params& p, cudaStr
 cudaError_t launch_syrk_f64(const float* A, int64_t n, int64_t ld, int64_t d, double* AtA, cudaStream_t s);
 cudaError_t launch_sub_btb(double* M, const double* AtA, const float* B, int ell, int64_t d, cudaStream_t s);
 cudaError_t launch_lanczos(const double* M, int64_t d, int kmax, double* Q, double* work, double* out2,
-                           cudaStream_t s);
+                           cudaStream_t s, int ntop = 0, double* top = nullptr);
+// proj-err parts (fd_eval.cu): G = B B^T, Jacobi -> (V, w, ord), q[t] = v_t^T AtA v_t
+cudaError_t launch_proj_parts(const float* B, int ell, int64_t d, int k, const double* AtA, double* G, double* V,
+                              double* w, int* ord, int* sweeps, double* vbuf, double* q, cudaStream_t s);
 
 }  // namespace fdk

@@ -1521,7 +1521,7 @@ __device__ int sturm_count_d(const double* a, const double* b, int k, double x) 
 
 __global__ void __launch_bounds__(1024, 1) lanczos_kernel(const double* __restrict__ M, int64_t d, int kmax,
                                                           double* __restrict__ Q, double* __restrict__ work,
-                                                          double* __restrict__ out2) {
+                                                          double* __restrict__ out2, int ntop, double* __restrict__ top) {
   double* alpha = work;
   double* beta = alpha + kmax;       // beta[j] couples q_{j-1}, q_j (beta[0] unused)
   double* z = beta + kmax + 1;
@@ -1589,6 +1589,30 @@ __global__ void __launch_bounds__(1024, 1) lanczos_kernel(const double* __restri
   __syncthreads();
   // extreme eigenvalues of the k x k tridiagonal by bisection (fp64)
   const int k = s_k;
+  // top-ntop Ritz values (descending) for the proj-err denominator: thread 2 + t
+  // bisects the (k - t)-th smallest; t >= k (Krylov space exhausted) -> 0
+  if (tid >= 2 && tid < 2 + ntop) {
+    const int t = tid - 2;
+    if (t >= k) {
+      top[t] = 0.0;
+    } else {
+      double gl = 1e308, gu = -1e308;
+      for (int i = 0; i < k; ++i) {
+        const double em = (i > 0) ? fabs(beta[i]) : 0.0;
+        const double ep = (i + 1 < k) ? fabs(beta[i + 1]) : 0.0;
+        gl = fmin(gl, alpha[i] - em - ep);
+        gu = fmax(gu, alpha[i] + em + ep);
+      }
+      double lo = gl - 1e-12 * fabs(gl) - 1e-300, hi = gu + 1e-12 * fabs(gu) + 1e-300;
+      for (int it = 0; it < 200; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        if (mid <= lo || mid >= hi) break;
+        if (sturm_count_d(alpha, beta, k, mid) >= k - t) hi = mid;
+        else lo = mid;
+      }
+      top[t] = 0.5 * (lo + hi);
+    }
+  }
   if (tid < 2) {
     double gl = 1e308, gu = -1e308;
     for (int i = 0; i < k; ++i) {
@@ -1611,8 +1635,8 @@ __global__ void __launch_bounds__(1024, 1) lanczos_kernel(const double* __restri
 }
 
 cudaError_t launch_lanczos(const double* M, int64_t d, int kmax, double* Q, double* work, double* out2,
-                           cudaStream_t s) {
-  lanczos_kernel<<<1, 1024, 0, s>>>(M, d, kmax, Q, work, out2);
+                           cudaStream_t s, int ntop, double* top) {
+  lanczos_kernel<<<1, 1024, 0, s>>>(M, d, kmax, Q, work, out2, ntop, top);
   return cudaGetLastError();
 }
 

@@ -389,3 +389,88 @@ def test_c4_fullsize_bench_config():
         ref = torch.dot(A[:, i].double(), A[:, j].double()).item()
         assert abs(AtA[i, j].item() - ref) <= 1e-9 * frob
     sk.close()
+
+
+# ---------------------------------------------------------------------------
+# proj-err evaluator (k = 10 per :572)
+# Tolerance: both sides are fp64 from the same fp32 (A, B); the quotient of two
+# tails (frob - captured) / (frob - best) loses at most frob / tail digits, so a
+# relative 1e-8 is ~1e5 x the fp64 rounding at these tails (reading E1).
+# ---------------------------------------------------------------------------
+PROJ_TOL = 1e-8
+
+
+def _proj_pair(A, B32, k):
+    po = oracle.proj_err(A, B32.astype(np.float64), k=k)
+    pg = fd().proj_err(torch.from_numpy(A).cuda(), torch.from_numpy(B32).cuda(), k=k)
+    return po, pg
+
+
+def test_proj_err_parity_fd_sketches():
+    """GPU proj-err vs oracle on the oracle's FD / Fast FD sketches of c1 and c2 (k = 10)."""
+    for cfg, ell, v in (("c1", 16, "fd"), ("c2", 20, "fast_fd"), ("c2", 100, "fast_alpha_fd")):
+        A = fdgen.host_rows(fdgen.config(cfg)) if cfg == "c1" else _c2()
+        r = oracle.sketch(A, ell, v, alpha=0.2 if "alpha" in v else None)
+        B32 = r.B.astype(np.float32)
+        po, pg = _proj_pair(A, B32, 10)
+        assert abs(pg["err"] - po["err"]) <= PROJ_TOL * po["err"], (cfg, ell, v, pg, po)
+        assert po["err"] >= 1.0 - 1e-12
+
+
+def test_proj_err_parity_gram_path_and_parts():
+    """proj_err_from_gram: numerator and denominator separately against the oracle."""
+    A = _c2()
+    r = oracle.sketch(A, 40, "fast_fd")
+    B32 = r.B.astype(np.float32)
+    po = oracle.proj_err(A, B32.astype(np.float64), k=10)
+    m = fd()
+    Ad = torch.from_numpy(A).cuda()
+    AtA = torch.zeros((A.shape[1], A.shape[1]), dtype=torch.float64, device="cuda")
+    m.cov_gram_partial(Ad, AtA)
+    frob = float(torch.trace(AtA).item())
+    pg = m.proj_err_from_gram(AtA, torch.from_numpy(B32).cuda(), frob, k=10)
+    assert abs(pg["num"] - po["num"]) <= 1e-10 * po["frob"]
+    assert abs(pg["den"] - po["den"]) <= 1e-10 * po["frob"]
+    assert abs(pg["err"] - po["err"]) <= PROJ_TOL * po["err"]
+
+
+def test_proj_err_edge_cases():
+    """B = A -> 1; rank B < k (3 rows); zero rows in B; odd ell (Jacobi padding); k = 1."""
+    rng = np.random.default_rng(11)
+    A = rng.standard_normal((300, 48)).astype(np.float32)
+    po, pg = _proj_pair(A, A, 10)
+    assert abs(pg["err"] - 1.0) < 1e-9 and abs(po["err"] - 1.0) < 1e-9
+    B = rng.standard_normal((3, 48)).astype(np.float32)
+    po, pg = _proj_pair(A, B, 10)
+    assert abs(pg["err"] - po["err"]) <= PROJ_TOL * po["err"]
+    B = np.zeros((13, 48), np.float32)
+    B[:5] = rng.standard_normal((5, 48))
+    po, pg = _proj_pair(A, B, 4)
+    assert abs(pg["err"] - po["err"]) <= PROJ_TOL * po["err"]
+    po, pg = _proj_pair(A, rng.standard_normal((7, 48)).astype(np.float32), 1)
+    assert abs(pg["err"] - po["err"]) <= PROJ_TOL * po["err"]
+    with pytest.raises(fd().FdError):
+        fd().proj_err(torch.zeros((4, 48), device="cuda"), torch.from_numpy(B).cuda(), k=2)
+
+
+def test_proj_err_fullsize_c4_bounds():
+    """c4 at full size (n = 8 388 608, d = 1024), the bench's Fast FD sketch (ell = 128,
+    P = 2368): properties that hold at any size -- 1 <= proj-err <= ell / (ell - k) --
+    and the Lanczos denominator against an independent fp64 eigvalsh of the same AtA."""
+    m = fd()
+    w = fdgen.config("c4")
+    gen = fdgen.DeviceGenerator(w)
+    A = torch.empty((w.n, w.d), dtype=torch.float32, device="cuda")
+    gen.fill(A)
+    sk = m.Sketcher(w.d, 128, "fast_fd", n_shards=2368)
+    sk.append(A)
+    B, _ = sk.sketch()
+    AtA = torch.zeros((w.d, w.d), dtype=torch.float64, device="cuda")
+    m.cov_gram_partial(A, AtA)
+    del A
+    frob = float(torch.trace(AtA).item())
+    pg = m.proj_err_from_gram(AtA, B, frob, k=10)
+    assert 1.0 - 1e-9 <= pg["err"] <= 128.0 / (128 - 10)
+    lam = np.linalg.eigvalsh(AtA.cpu().numpy())[::-1]
+    den = frob - float(np.sum(lam[:10]))
+    assert abs(pg["den"] - den) <= 1e-9 * frob
