@@ -61,11 +61,15 @@ def reduce_gram(AtA, group=None):
     return AtA, float(torch.diagonal(AtA).sum().item())
 
 
-def dist_cov_err(A_local, B, group=None):
-    """cov-err of B for the row-sharded A (sum of partial Grams by all_reduce)."""
-    from . import cov_err_from_gram, cov_gram_partial
+def dist_cov_err(A_local, B, group=None, proj_k=0):
+    """cov-err of B for the row-sharded A (sum of partial Grams by all_reduce); with
+    proj_k > 0 also proj-err at k = proj_k from the same A^T A."""
+    from . import cov_err_from_gram, cov_gram_partial, proj_err_from_gram
     d = B.shape[1]
     AtA = torch.zeros((d, d), dtype=torch.float64, device=B.device)
     cov_gram_partial(A_local, AtA)
     AtA, frob = reduce_gram(AtA, group)
-    return cov_err_from_gram(AtA, B, frob)
+    out = cov_err_from_gram(AtA, B, frob)
+    if proj_k > 0:
+        out["proj_err"] = proj_err_from_gram(AtA, B, frob, k=proj_k)["err"]
+    return out
