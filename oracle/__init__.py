@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
-RULE_FD, RULE_ISVD = 0, 1
+RULE_FD, RULE_ISVD, RULE_FD_T = 0, 1, 2
 # variant name -> (rule, alpha, batched)
 VARIANTS = {
     "fd": (RULE_FD, 1.0, False),           # Alg. 1 + FD rule, per-row
@@ -25,6 +25,9 @@ VARIANTS = {
     "fast_alpha_fd": (RULE_FD, None, True),  # Alg. 2 rule on the 2ell buffer (C3)
     "isvd": (RULE_ISVD, 1.0, False),
     "fast_isvd": (RULE_ISVD, 1.0, True),
+    # paper-literal Fast alpha-FD: ell-row buffer, delta = sigma_t^2,
+    # t = ell - ceil(alpha ell / 2) (C25)
+    "fast_alpha_fd_paper": (RULE_FD_T, None, "literal"),
 }
 
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -41,13 +44,16 @@ def lib():
         L.oracle_reduce_rank.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int,
                                          ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
         L.oracle_reduce_rank.restype = ctypes.c_int
+        L.oracle_reduce_rank_t.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int,
+                                           ctypes.c_double, ctypes.c_void_p]
+        L.oracle_reduce_rank_t.restype = ctypes.c_int
         L.oracle_sketch.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                     ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
                                     ctypes.c_void_p, ctypes.c_void_p]
         L.oracle_sketch.restype = ctypes.c_int
         L.oracle_merge.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
-                                   ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+                                   ctypes.c_int, ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p]
         L.oracle_merge.restype = ctypes.c_int
         L.oracle_gram.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                                   ctypes.c_void_p, _dp]
@@ -103,6 +109,17 @@ def reduce_rank(Bf, ell, rule=RULE_FD, alpha=1.0):
     return B, st[0], st[1]
 
 
+def reduce_rank_t(Bf, ell, alpha):
+    """One paper-literal Fast alpha-FD ReduceRank of the L x d buffer Bf."""
+    B = np.array(Bf, dtype=np.float64, order="C", copy=True)
+    L, d = B.shape
+    st = np.zeros(3)
+    rc = lib().oracle_reduce_rank_t(B.ctypes.data, L, d, ell, float(alpha), st.ctypes.data)
+    if rc:
+        raise RuntimeError(f"oracle_reduce_rank_t rc={rc}")
+    return B, st[0], st[1]
+
+
 class SketchResult:
     def __init__(self, B, stats, shards=None):
         self.B = B
@@ -121,7 +138,7 @@ def sketch(A, ell, variant="fd", alpha=None, n_shards=1, appends=None, nthreads=
         alpha = a0
     elif alpha is None:
         alpha = 0.2
-    L = 2 * ell if batched else ell
+    L = 2 * ell if batched is True else ell
     B = np.zeros((ell, d))
     shards = np.zeros((n_shards, ell, d)) if want_shards else None
     st = np.zeros(5)
@@ -151,7 +168,7 @@ def merge(sketches, ell, variant="fd", alpha=None):
     m = ell if rule == RULE_ISVD else alpha_m(ell, alpha)
     B = np.zeros((ell, d))
     st = np.zeros(5)
-    rc = lib().oracle_merge(S.ctypes.data, count, d, ell, rule, m, B.ctypes.data, st.ctypes.data)
+    rc = lib().oracle_merge(S.ctypes.data, count, d, ell, rule, m, float(alpha), B.ctypes.data, st.ctypes.data)
     if rc:
         raise RuntimeError(f"oracle_merge rc={rc}")
     return B, st
@@ -222,3 +239,13 @@ def proj_err(A, B, k=10, nthreads=0, jacobi_max=512, kmax=512):
     if rc:
         raise RuntimeError(f"oracle_proj_err rc={rc}")
     return dict(err=out[0], num=out[1], den=out[2], frob=out[3])
+
+
+def fd_t_indices(ell, alpha):
+    """(t, R) of the paper-literal Fast alpha-FD (C25):
+    delta = lambda_t (1-based), rows 0..R-1 kept.  Mirrors oracle.c fd_t_indices."""
+    import math
+    h = max(1, math.ceil(alpha * ell / 2.0 - 1e-9))
+    m = alpha_m(ell, alpha)
+    t = ell - h
+    return t, max(ell - m, t - 1)

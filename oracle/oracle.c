@@ -41,6 +41,8 @@
 
 #define ORC_RULE_FD 0   /* alpha-FD with alpha given; FD is alpha = 1 */
 #define ORC_RULE_ISVD 1
+#define ORC_RULE_FD_T 2 /* paper-literal Fast alpha-FD: delta = sigma_t^2,
+                           t = ell - ceil(alpha ell / 2), buffer of ell rows */
 
 /* ------------------------------------------------------------------------ */
 /* Symmetric eigen-decomposition: cyclic two-sided Jacobi (fp64).            */
@@ -116,13 +118,30 @@ typedef struct {
 
 typedef struct {
   int L, ell, rule, m;
+  int t;   /* delta = lambda_t (1-based): ell for every rule but ORC_RULE_FD_T     */
+  int R;   /* rows kept after a ReduceRank (slot semantics, C6): ell-1, or R_t    */
   int64_t d;
   double *G, *V, *lam, *w, *Bn;
   int* order;
 } orc_work;
 
+/* Paper-literal Fast alpha-FD: "delta_i = sigma_t^2 for
+ * t = ell - ell alpha/2", "only changing the last alpha ell singular values:
+ * sigma'_j^2 = max(sigma_j^2 - delta_i, 0)".  Integer reading (C25):
+ * t = ell - max(1, ceil(alpha ell / 2)), m = max(1, round(alpha ell)) (C5); the
+ * rows that can stay nonzero are j <= max(ell - m, t - 1), which are kept. */
+static void fd_t_indices(int ell, double alpha, int* t, int* R) {
+  int h = (int)ceil(alpha * (double)ell / 2.0 - 1e-9);
+  if (h < 1) h = 1;
+  int m = (int)llround(alpha * ell);
+  if (m < 1) m = 1;
+  *t = ell - h;
+  *R = (ell - m > *t - 1) ? ell - m : *t - 1;
+}
+
 static int work_init(orc_work* W, int L, int64_t d, int ell, int rule, int m) {
   W->L = L; W->d = d; W->ell = ell; W->rule = rule; W->m = m;
+  W->t = ell; W->R = ell - 1;
   W->G = malloc(sizeof(double) * L * L);
   W->V = malloc(sizeof(double) * L * L);
   W->lam = malloc(sizeof(double) * L);
@@ -159,12 +178,13 @@ static int reduce_rank(orc_work* W, double* Bf, orc_stats* st) {
     double v = W->lam[W->order[j]];
     lams[j] = v > 0.0 ? v : 0.0; /* clamp (reading C8) */
   }
-  /* delta = lambda_ell (1-based), i.e. sigma_ell^2 */
-  double delta = (ell <= L) ? lams[ell - 1] : 0.0;
+  /* delta = lambda_t (1-based), i.e. sigma_t^2: t = ell except the paper-literal
+   * Fast alpha-FD */
+  double delta = (W->t <= L) ? lams[W->t - 1] : 0.0;
   double removed = 0.0;
   for (int j = 0; j < L; ++j) {
     double sp2; /* sigma'_j^2 for 0-based j */
-    if (j >= ell - 1) sp2 = 0.0; /* rows ell.. are freed; sigma'_ell = 0 in every rule */
+    if (j >= W->R) sp2 = 0.0; /* rows R.. are freed; sigma'_ell = 0 in every rule */
     else if (W->rule == ORC_RULE_ISVD) sp2 = lams[j];
     else if (j < ell - W->m) sp2 = lams[j]; /* alpha-FD: first ell-m unchanged */
     else sp2 = (lams[j] - delta > 0.0) ? lams[j] - delta : 0.0;
@@ -173,7 +193,7 @@ static int reduce_rank(orc_work* W, double* Bf, orc_stats* st) {
   }
   /* B'_j = w_j * u_j^T Bf  (u_j = column order[j] of V) */
   memset(W->Bn, 0, sizeof(double) * (size_t)L * d);
-  for (int j = 0; j < ell - 1 && j < L; ++j) {
+  for (int j = 0; j < W->R && j < L; ++j) {
     double wj = W->w[j];
     if (wj == 0.0) continue;
     int c = W->order[j];
@@ -204,6 +224,21 @@ int oracle_reduce_rank(double* Bf, int L, int64_t d, int ell, int rule, int m, d
   return rc;
 }
 
+/* Rule-level entry for the paper-literal Fast alpha-FD: delta = lambda_t, rows
+ * 0..R-1 kept (t, R as fd_t_indices gives them for (ell, alpha)). */
+int oracle_reduce_rank_t(double* Bf, int L, int64_t d, int ell, double alpha, double* stats3) {
+  orc_work W;
+  int m = (int)llround(alpha * ell);
+  if (m < 1) m = 1;
+  if (work_init(&W, L, d, ell, ORC_RULE_FD_T, m)) return -2;
+  fd_t_indices(ell, alpha, &W.t, &W.R);
+  orc_stats st = {0};
+  int rc = reduce_rank(&W, Bf, &st);
+  work_free(&W);
+  if (stats3) { stats3[0] = st.delta_total; stats3[1] = st.removed; stats3[2] = (double)st.n_shrinks; }
+  return rc;
+}
+
 /* ------------------------------------------------------------------------ */
 /* One shard: Alg. 1 row loop with slot semantics, then a final ReduceRank.   */
 /* rows: pointers to the shard's row segments (one per append call).          */
@@ -211,7 +246,7 @@ int oracle_reduce_rank(double* Bf, int L, int64_t d, int ell, int rule, int m, d
 typedef struct {
   const float* A; int64_t lda, d;
   const int64_t* seg_start; const int64_t* seg_len; int nseg;
-  int L, ell, rule, m;
+  int L, ell, rule, m, t, R;
   double* B_out;   /* ell x d */
   orc_stats st;
   int rc;
@@ -220,6 +255,7 @@ typedef struct {
 static void run_shard(orc_shard_job* J) {
   orc_work W;
   if (work_init(&W, J->L, J->d, J->ell, J->rule, J->m)) { J->rc = -2; return; }
+  W.t = J->t; W.R = J->R;
   const int64_t d = J->d;
   double* Bf = calloc((size_t)J->L * d, sizeof(double));
   memset(&J->st, 0, sizeof(J->st));
@@ -236,7 +272,7 @@ static void run_shard(orc_shard_job* J) {
       occ += 1;
       if (occ == J->L) {
         if (reduce_rank(&W, Bf, &J->st)) { J->rc = -1; break; }
-        occ = J->ell - 1;
+        occ = J->R;
       }
     }
   }
@@ -263,10 +299,11 @@ static void* pool_worker(void* arg) {
 }
 
 /* merge(X, Y) = ReduceRank([X; Y]) with L = 2 ell (reading C10). */
-static int merge2(const double* X, const double* Y, int64_t d, int ell, int rule, int m,
+static int merge2(const double* X, const double* Y, int64_t d, int ell, int rule, int m, int t, int R,
                   double* out, orc_stats* st) {
   orc_work W;
   if (work_init(&W, 2 * ell, d, ell, rule, m)) return -2;
+  W.t = t; W.R = R;
   double* Bf = malloc(sizeof(double) * (size_t)2 * ell * d);
   memcpy(Bf, X, sizeof(double) * (size_t)ell * d);
   memcpy(Bf + (size_t)ell * d, Y, sizeof(double) * (size_t)ell * d);
@@ -278,27 +315,31 @@ static int merge2(const double* X, const double* Y, int64_t d, int ell, int rule
 }
 
 /* Recursive-halving tree over sketches [lo, hi): left half has ceil((hi-lo)/2). */
-static int merge_tree(double* S, int lo, int hi, int64_t d, int ell, int rule, int m,
+static int merge_tree(double* S, int lo, int hi, int64_t d, int ell, int rule, int m, int t, int R,
                       double* out, orc_stats* st) {
   size_t sz = (size_t)ell * d;
   if (hi - lo == 1) { memcpy(out, S + (size_t)lo * sz, sizeof(double) * sz); return 0; }
   int mid = lo + (hi - lo + 1) / 2;
   double* X = malloc(sizeof(double) * sz);
   double* Y = malloc(sizeof(double) * sz);
-  int rc = merge_tree(S, lo, mid, d, ell, rule, m, X, st);
-  if (!rc) rc = merge_tree(S, mid, hi, d, ell, rule, m, Y, st);
-  if (!rc) rc = merge2(X, Y, d, ell, rule, m, out, st);
+  int rc = merge_tree(S, lo, mid, d, ell, rule, m, t, R, X, st);
+  if (!rc) rc = merge_tree(S, mid, hi, d, ell, rule, m, t, R, Y, st);
+  if (!rc) rc = merge2(X, Y, d, ell, rule, m, t, R, out, st);
   free(X); free(Y);
   return rc;
 }
 
-int oracle_merge(const double* sketches, int count, int64_t d, int ell, int rule, int m,
+/* rule ORC_RULE_FD_T: alpha = the variant's alpha (t, R from fd_t_indices);
+ * other rules: alpha unused beyond m. */
+int oracle_merge(const double* sketches, int count, int64_t d, int ell, int rule, int m, double alpha,
                  double* B_out, double* stats5) {
   if (count < 1) return -3;
+  int t = ell, R = ell - 1;
+  if (rule == ORC_RULE_FD_T) fd_t_indices(ell, alpha, &t, &R);
   orc_stats st = {0};
   double* S = malloc(sizeof(double) * (size_t)count * ell * d);
   memcpy(S, sketches, sizeof(double) * (size_t)count * ell * d);
-  int rc = merge_tree(S, 0, count, d, ell, rule, m, B_out, &st);
+  int rc = merge_tree(S, 0, count, d, ell, rule, m, t, R, B_out, &st);
   free(S);
   if (stats5) { stats5[0] = 0; stats5[1] = st.delta_total; stats5[2] = st.removed; stats5[3] = (double)st.n_shrinks; stats5[4] = 0; }
   return rc;
@@ -318,6 +359,13 @@ int oracle_sketch(const float* A, int64_t n, int64_t lda, int64_t d, int ell, in
                   int nthreads, double* B_out, double* shard_out, double* stats5) {
   if (ell < 2 || P < 1 || d < 1 || L < ell || lda < d) return -3;
   int m = ell;
+  int tt = ell, RR = ell - 1;
+  if (rule == ORC_RULE_FD_T) {
+    if (!(alpha > 0.0 && alpha <= 1.0) || L != ell) return -3;
+    m = (int)llround(alpha * ell);
+    if (m < 1) m = 1;
+    fd_t_indices(ell, alpha, &tt, &RR);
+  }
   if (rule == ORC_RULE_FD) {
     if (!(alpha > 0.0 && alpha <= 1.0)) return -3;
     m = (int)llround(alpha * ell);
@@ -344,7 +392,7 @@ int oracle_sketch(const float* A, int64_t n, int64_t lda, int64_t d, int ell, in
     orc_shard_job* J = &jobs[s];
     J->A = A; J->lda = lda; J->d = d;
     J->seg_start = starts + (size_t)s * nappend; J->seg_len = lens + (size_t)s * nappend; J->nseg = nappend;
-    J->L = L; J->ell = ell; J->rule = rule; J->m = m;
+    J->L = L; J->ell = ell; J->rule = rule; J->m = m; J->t = tt; J->R = RR;
     J->B_out = S + (size_t)s * ell * d;
   }
   if (nthreads < 1) nthreads = 1;
@@ -365,7 +413,7 @@ int oracle_sketch(const float* A, int64_t n, int64_t lda, int64_t d, int ell, in
     tot.rows_seen += jobs[s].st.rows_seen;
   }
   if (shard_out) memcpy(shard_out, S, sizeof(double) * (size_t)P * ell * d);
-  if (!rc && B_out) rc = merge_tree(S, 0, P, d, ell, rule, m, B_out, &tot);
+  if (!rc && B_out) rc = merge_tree(S, 0, P, d, ell, rule, m, tt, RR, B_out, &tot);
   if (stats5) {
     stats5[0] = tot.frob_sq; stats5[1] = tot.delta_total; stats5[2] = tot.removed;
     stats5[3] = (double)tot.n_shrinks; stats5[4] = (double)tot.rows_seen;

@@ -111,25 +111,29 @@ def test_lanczos_vs_jacobi():
 # eigenpairs of C (d x d), which share their nonzero spectrum with the Gram form
 # the oracle uses; slot counting is the same (occ -> ell-1 after each shrink).
 # ---------------------------------------------------------------------------
-def _cov_reduce(C, L, ell, rule, m):
+def _cov_reduce(C, L, ell, rule, m, t=None, R=None):
+    # t: delta = lambda_t (1-based); R: rows kept.  Every rule but the paper-literal
+    # Fast alpha-FD has t = ell, R = ell - 1.
+    t = ell if t is None else t
+    R = ell - 1 if R is None else R
     d = C.shape[0]
     mu, V = np.linalg.eigh(C)
     mu, V = mu[::-1], V[:, ::-1]
     lam = np.zeros(max(L, d))
     lam[: min(d, L)] = np.maximum(mu[: min(d, L)], 0)
-    delta = lam[ell - 1] if ell <= L else 0.0
+    delta = lam[t - 1] if t <= L else 0.0
     sp2 = np.zeros_like(lam)
-    for j in range(ell - 1):
+    for j in range(R):
         if rule == "isvd" or j < ell - m:
             sp2[j] = lam[j]
         else:
             sp2[j] = max(lam[j] - delta, 0.0)
-    k = min(d, ell - 1)
+    k = min(d, R)
     Cn = (V[:, :k] * sp2[:k][None, :]) @ V[:, :k].T
     return Cn, delta, float(np.sum(lam[:L] - sp2[:L]))
 
 
-def _cov_sketch(A, ell, rule, m, L):
+def _cov_sketch(A, ell, rule, m, L, t=None, R=None):
     d = A.shape[1]
     C = np.zeros((d, d))
     occ = 0
@@ -138,15 +142,16 @@ def _cov_sketch(A, ell, rule, m, L):
         C += np.outer(a, a)
         occ += 1
         if occ == L:
-            C, dl, _ = _cov_reduce(C, L, ell, rule, m)
+            C, dl, _ = _cov_reduce(C, L, ell, rule, m, t, R)
             Delta += dl
-            occ = ell - 1
-    C, dl, _ = _cov_reduce(C, L, ell, rule, m)
+            occ = ell - 1 if R is None else R
+    C, dl, _ = _cov_reduce(C, L, ell, rule, m, t, R)
     return C, Delta + dl
 
 
 @pytest.mark.parametrize("seed", range(6))
-@pytest.mark.parametrize("variant", ["fd", "fast_fd", "alpha_fd", "fast_alpha_fd", "isvd", "fast_isvd"])
+@pytest.mark.parametrize("variant", ["fd", "fast_fd", "alpha_fd", "fast_alpha_fd", "isvd", "fast_isvd",
+                                     "fast_alpha_fd_paper"])
 def test_bruteforce_covariance_form(seed, variant):
     rng = np.random.default_rng(100 + seed)
     n = int(rng.integers(1, 13))
@@ -156,9 +161,10 @@ def test_bruteforce_covariance_form(seed, variant):
     rule, a0, batched = oracle.VARIANTS[variant]
     alpha = 0.5 if a0 is None else a0
     m = ell if rule == oracle.RULE_ISVD else oracle.alpha_m(ell, alpha)
-    L = 2 * ell if batched else ell
+    L = 2 * ell if batched is True else ell
+    t, R = oracle.fd_t_indices(ell, alpha) if rule == oracle.RULE_FD_T else (None, None)
     r = oracle.sketch(A, ell, variant, alpha=alpha)
-    C, Delta = _cov_sketch(A, ell, "isvd" if rule == oracle.RULE_ISVD else "fd", m, L)
+    C, Delta = _cov_sketch(A, ell, "isvd" if rule == oracle.RULE_ISVD else "fd", m, L, t, R)
     np.testing.assert_allclose(r.B.T @ r.B, C, atol=1e-10 * max(1.0, np.abs(C).max()))
     assert abs(r.delta_total - Delta) < 1e-10 * max(1.0, Delta)
 
@@ -189,6 +195,10 @@ def test_properties_lemma1_lemma3(variant):
     if rule == oracle.RULE_ISVD:
         if not batched:
             assert abs(r.removed - r.delta_total) <= 1e-9 * frob
+    elif rule == oracle.RULE_FD_T:
+        # paper-literal Fast alpha-FD: rows ell-m+1..t lose exactly delta each
+        t, _ = oracle.fd_t_indices(ell, alpha)
+        assert r.removed >= (t - ell + m) * r.delta_total * (1 - 1e-12)
     elif not batched:
         assert abs(r.removed - m * r.delta_total) <= 1e-9 * frob
     else:
@@ -408,3 +418,72 @@ def test_proj_err_undefined_cases():
     A = np.zeros((5, 6), np.float32); A[0, 0] = 1.0; A[1, 2] = 2.0      # rank 2 <= k
     with pytest.raises(ValueError):
         oracle.proj_err(A, np.ones((2, 6)), k=2)
+
+
+# ---------------------------------------------------------------------------
+# paper-literal Fast alpha-FD
+# ---------------------------------------------------------------------------
+def test_fd_t_indices_reading():
+    """t = ell - ceil(alpha ell / 2), R = max(ell - m, t - 1) (C25)."""
+    assert oracle.fd_t_indices(128, 0.2) == (115, 114)     # alpha ell / 2 = 12.8 -> 13
+    assert oracle.fd_t_indices(20, 0.2) == (18, 17)        # 2.0 exactly -> 2
+    assert oracle.fd_t_indices(20, 1.0) == (10, 9)         # Fast FD with an ell-row buffer
+    assert oracle.fd_t_indices(50, 0.02) == (49, 49)       # m = 1: only sigma_ell shrinks
+
+
+def test_fast_alpha_fd_paper_rule_closed_form():
+    """One ReduceRank of a buffer with known singular values (rows s_j e_{pi(j)}):
+    PAPER.md:391 -- delta = sigma_t^2, sigma'_j^2 = sigma_j^2 for j <= ell - alpha ell,
+    max(sigma_j^2 - delta, 0) for the last alpha ell -- written out here directly."""
+    ell, alpha, d = 20, 0.4, 31
+    rng = np.random.default_rng(5)
+    s = np.sort(rng.uniform(1.0, 9.0, ell))[::-1]
+    perm = rng.permutation(d)[:ell]
+    Bf = np.zeros((ell, d))
+    for j in range(ell):
+        Bf[j, perm[j]] = s[j]
+    Bf = Bf[rng.permutation(ell)]           # row order of the buffer must not matter
+    t, R = oracle.fd_t_indices(ell, alpha)
+    m = oracle.alpha_m(ell, alpha)
+    B, delta, removed = oracle.reduce_rank_t(Bf, ell, alpha)
+    assert abs(delta - s[t - 1] ** 2) < 1e-12 * s[0] ** 2
+    sp2 = np.where(np.arange(1, ell + 1) <= ell - m, s ** 2, np.maximum(s ** 2 - delta, 0.0))
+    sp2[R:] = 0.0
+    got = np.sort(np.sum(B ** 2, axis=1))[::-1]
+    np.testing.assert_allclose(got, sp2, atol=1e-10 * s[0] ** 2)
+    assert np.all(np.sum(B[R:] ** 2, axis=1) == 0.0)
+    assert abs(removed - (np.sum(s ** 2) - np.sum(sp2))) < 1e-10 * s[0] ** 2
+
+
+def test_fast_alpha_fd_paper_alpha1_is_fast_fd():
+    """alpha = 1 with 2 ell' rows is Fast FD with ell' (delta = lambda_ell' of a 2 ell'
+    buffer, ell' - 1 rows kept): the same sketch, bit for bit, at P = 1 and P = 3."""
+    A = _c1()
+    for P in (1, 3):
+        r1 = oracle.sketch(A, 8, "fast_fd", n_shards=P)
+        r2 = oracle.sketch(A, 16, "fast_alpha_fd_paper", alpha=1.0, n_shards=P)
+        assert np.array_equal(r2.B[:8], r1.B) and not np.any(r2.B[8:])
+        assert r2.delta_total == r1.delta_total
+
+
+def test_fast_alpha_fd_paper_bounds():
+    """Fast alpha-FD with ell rows meets alpha-FD's bounds at half the
+    rows: 0 <= ||Ax||^2 - ||Bx||^2 <= ||A - A_k||_F^2 / (alpha ell / 2 - k) for
+    k < alpha ell / 2; the Frobenius ledger ||A||^2 - ||B||^2 = removed >= (t - ell + m) Delta."""
+    A = _c1().astype(np.float64)
+    n, d = A.shape
+    sv = np.linalg.svd(A, compute_uv=False)
+    for ell, alpha in ((16, 1.0), (40, 0.5), (60, 0.4)):
+        r = oracle.sketch(A.astype(np.float32), ell, "fast_alpha_fd_paper", alpha=alpha)
+        M = A.T @ A - r.B.T @ r.B
+        w = np.linalg.eigvalsh((M + M.T) / 2)
+        assert w[0] >= -1e-9 * sv[0] ** 2
+        half = alpha * ell / 2
+        for k in range(0, int(np.ceil(half))):
+            if k < half:
+                assert w[-1] <= np.sum(sv[k:] ** 2) / (half - k) * (1 + 1e-9)
+        t, R = oracle.fd_t_indices(ell, alpha)
+        m = oracle.alpha_m(ell, alpha)
+        frob_a, frob_b = np.sum(A ** 2), np.sum(r.B ** 2)
+        assert abs((frob_a - frob_b) - r.removed) < 1e-8 * frob_a
+        assert (frob_a - frob_b) >= (t - ell + m) * r.delta_total * (1 - 1e-9)
