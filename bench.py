@@ -49,7 +49,19 @@ def peaks():
     return p
 
 
-def algorithmic_work(ell, d, N):
+def retained_and_t(variant, ell, alpha):
+    """(R, t): rows kept per ReduceRank and the delta index (1-based). ell-1, ell for
+    every variant but the paper-literal Fast alpha-FD (C25)."""
+    import math
+    if variant != "fast_alpha_fd_paper":
+        return ell - 1, ell
+    h = max(1, math.ceil(alpha * ell / 2.0 - 1e-9))
+    m = max(1, int(alpha * ell + 0.5))
+    t = ell - h
+    return max(ell - m, t - 1), t
+
+
+def algorithmic_work(ell, d, N, R=None, t=None):
     """Algorithmic work of one ReduceRank:
     gram  = [2(ell^2-1) + (ell+1)(ell+2)] d flops (cross + new blocks; the retained
             block is diag(sigma'^2))
@@ -61,17 +73,20 @@ def algorithmic_work(ell, d, N):
             retained vector; latency-bound)
     ingest= 2 (ell+1) d 4 bytes             (read the rows, write the buffer)"""
     import math
-    K = min(ell, N)
-    J = min(ell - 1, N)
+    R = ell - 1 if R is None else R          # rows kept (diag(sigma'^2) block of the next Gram)
+    t = ell if t is None else t
+    nw = N - R                               # new rows per ReduceRank
+    K = min(max(t, R), N)
+    J = min(R, N)
     kp = 1 << max(0, (K - 1).bit_length())
-    lean = 32 < N <= 256 and ell - 1 <= 128
+    lean = 32 < N <= 256 and R <= 128
     g = max(1, min(32, (256 if lean else 512) // kp))
     iters = math.ceil(27.0 / math.log2(g + 1))
     return {
-        "gram": (2 * (ell * ell - 1) + (ell + 1) * (ell + 2)) * d,
-        "recon": 4 * ell * (ell - 1) * d,
+        "gram": (2 * R * nw + nw * (nw + 1)) * d,
+        "recon": 2 * R * N * d,
         "trd": (4.0 / 3.0) * N ** 3,
-        "bt": 2.0 * N * N * (ell - 1),
+        "bt": 2.0 * N * N * R,
         "eig": K * g * iters * N * 5.0 + 3.0 * J * 13.0 * N,
     }
 
@@ -142,14 +157,15 @@ def dist_env():
 # ---------------------------------------------------------------------------
 # CPU oracle timing (cpu_baseline and the --impl reference arm)
 # ---------------------------------------------------------------------------
-def oracle_sample(wl, rows_per_shard=None, nshards=None):
+def oracle_sample(wl, rows_per_shard=None, nshards=None, variant=None, alpha=0.2):
     """Time the oracle (as it stands) on a bounded sample of the workload: `nshards`
     shard streams of the bench DAG (one thread each, all host cores)."""
     import numpy as np  # noqa: F401
     import concurrent.futures as cf
     import fdgen
     import oracle
-    cfgname, ell, variant, P = WORKLOADS[wl]
+    cfgname, ell, v0, P = WORKLOADS[wl]
+    variant = variant or v0
     w = fdgen.config(cfgname)
     cores = os.cpu_count() or 1
     nshards = nshards or cores
@@ -165,7 +181,7 @@ def oracle_sample(wl, rows_per_shard=None, nshards=None):
     rows = [fdgen.host_rows(w, a, b) for a, b in jobs]
     t0 = time.perf_counter()
     with cf.ThreadPoolExecutor(nshards) as ex:
-        list(ex.map(lambda A: oracle.sketch(A, ell, variant, nthreads=1), rows))
+        list(ex.map(lambda A: oracle.sketch(A, ell, variant, alpha=alpha, nthreads=1), rows))
     dt = time.perf_counter() - t0
     nrows = sum(b for _, b in jobs)
     return {"value": nrows / dt, "unit": "rows/s", "cores": min(cores, nshards), "kind": "oracle",
@@ -180,11 +196,12 @@ def run_reference(args):
         return 0
     wl = args.workload
     cfgname, ell, variant, P = WORKLOADS[wl]
+    variant = args.variant or variant
     rows_per_shard = 2064 if wl == "c4" else None  # 256 + 14*129 rows: 15 ReduceRanks per shard
     times = []
     res = None
     for i in range(args.warmup + args.steps):
-        res = oracle_sample(wl, rows_per_shard=rows_per_shard)
+        res = oracle_sample(wl, rows_per_shard=rows_per_shard, variant=variant, alpha=args.alpha)
         if i >= args.warmup:
             times.append(res)
     vals = [t["value"] for t in times]
@@ -194,7 +211,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.median(ms) if ms else None,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(wl, variant, P, world),
+        "config": config_dict(wl, variant, P, world, args.alpha),
         "cpu_baseline": {"value": value, "unit": "rows/s", "cores": res["cores"], "kind": "oracle",
                          "sample": res["sample"]},
         "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -203,13 +220,17 @@ def run_reference(args):
     return 0
 
 
-def config_dict(wl, variant, P, world):
+def config_dict(wl, variant, P, world, alpha=None):
     cfgname, ell, _, _ = WORKLOADS[wl]
     import fdgen
     w = fdgen.config(cfgname)
-    return {"workload": f"{wl}: noisy low-rank n={w.n} d={w.d} k={w.k} zeta=10 fp32, ell={ell}, {variant}",
-            "n": w.n, "d": w.d, "ell": ell, "variant": variant, "n_shards_total": P,
-            "parallelism": f"rows dp{world}", "l2": "inputs larger than L2 (A is streamed from HBM every step)"}
+    va = f"{variant} alpha={alpha}" if (alpha is not None and "alpha" in variant) else variant
+    out = {"workload": f"{wl}: noisy low-rank n={w.n} d={w.d} k={w.k} zeta=10 fp32, ell={ell}, {va}",
+           "n": w.n, "d": w.d, "ell": ell, "variant": variant, "n_shards_total": P,
+           "parallelism": f"rows dp{world}", "l2": "inputs larger than L2 (A is streamed from HBM every step)"}
+    if alpha is not None and "alpha" in variant:
+        out["alpha"] = alpha
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -242,7 +263,7 @@ def run_ours(args):
     A = torch.empty((nloc, w.d), dtype=torch.float32, device=dev)
     gen.fill(A, r0)
     torch.cuda.synchronize()
-    sk = fd.Sketcher(w.d, ell, variant, n_shards=P // world, device=dev)
+    sk = fd.Sketcher(w.d, ell, variant, alpha=args.alpha, n_shards=P // world, device=dev)
 
     def step():
         sk.reset()
@@ -287,8 +308,9 @@ def run_ours(args):
 
     # ---- roofline of the dominant kernel (live CUDA-event times of this run) ----
     pk = peaks()
-    N = 2 * ell if fd.is_batched(variant) else ell
-    work = algorithmic_work(ell, w.d, N)
+    N = 2 * ell if (fd.is_batched(variant) and variant != "fast_alpha_fd_paper") else ell
+    R_, t_ = retained_and_t(variant, ell, args.alpha)
+    work = algorithmic_work(ell, w.d, N, R_, t_)
     sk.reset()
     sk.append(A)
     Bst, st = sk.sketch(stats=True)
@@ -388,7 +410,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32 (Gram: 3xTF32 tensor cores, fp32-accurate)",
         "data": "synthetic (seeded fdgen, generated on device)",
-        "config": config_dict(wl, variant, P, world),
+        "config": config_dict(wl, variant, P, world, args.alpha),
         "roofline": roof,
         "gpu_launches": gpu_launches,
         "clocks": {"sm_mhz": clk["sm_mhz"], "sm_max_mhz": clk["sm_max_mhz"], "reasons": clk["reasons"]},
@@ -396,7 +418,8 @@ def run_ours(args):
         "e2e": e2e,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = oracle_sample(wl, rows_per_shard=2064 if wl == "c4" else None)
+        line["cpu_baseline"] = oracle_sample(wl, rows_per_shard=2064 if wl == "c4" else None, variant=variant,
+                                             alpha=args.alpha)
     if rank == 0:
         print(json.dumps(line), flush=True)
     sk.close()
@@ -413,6 +436,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--variant", default=None)
+    ap.add_argument("--alpha", type=float, default=0.2, help="alpha of the alpha-FD variants")
     ap.add_argument("--shards", type=int, default=None, help="P_total shard streams (default: the workload's)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -17,7 +17,8 @@ STATUS = {
     -4: "FD_ERR_WORKSPACE", -5: "FD_ERR_NONFINITE", -6: "FD_ERR_ZERO_NORM", -7: "FD_ERR_CUDA",
     -8: "FD_ERR_UNSUPPORTED", -9: "FD_ERR_STATE",
 }
-VARIANT = {"fd": 0, "fast_fd": 1, "alpha_fd": 2, "fast_alpha_fd": 3, "isvd": 4, "fast_isvd": 5}
+VARIANT = {"fd": 0, "fast_fd": 1, "alpha_fd": 2, "fast_alpha_fd": 3, "isvd": 4, "fast_isvd": 5,
+           "fast_alpha_fd_paper": 6}
 FD_MAX_N = 416
 
 # every symbol include/fd.h declares (checked by tests/test_abi.py)

@@ -53,6 +53,8 @@ struct Layout {
 struct Derived {
   int64_t d, ldb;
   int ell, L, P, rule, m, ldg, nmax;
+  int R;         // rows kept by a ReduceRank (ell-1; paper-literal Fast alpha-FD: max(ell-m, t-1))
+  int t;         // delta = lambda_t (ell; paper-literal Fast alpha-FD: ell - ceil(alpha ell/2))
   bool perrow;   // Alg. 1 per-row chain (buffer L = ell)
   size_t gbytes; // element size of the Gram / Wt scratch
 };
@@ -68,10 +70,11 @@ bool derive(const fd_config* c, Derived* D, std::string* why) {
   if (c->d < 1) { *why = "d < 1"; return false; }
   if (c->ell < 2) { *why = "ell < 2"; return false; }
   if (c->n_shards < 1) { *why = "n_shards < 1"; return false; }
-  if (c->variant < FD_FD || c->variant > FD_FAST_ISVD) { *why = "unknown variant"; return false; }
+  if (c->variant < FD_FD || c->variant > FD_FAST_ALPHA_FD_PAPER) { *why = "unknown variant"; return false; }
+  const bool literal = (c->variant == FD_FAST_ALPHA_FD_PAPER);
   const bool batched = (c->variant == FD_FAST_FD || c->variant == FD_FAST_ALPHA_FD || c->variant == FD_FAST_ISVD);
   const bool isvd = (c->variant == FD_ISVD || c->variant == FD_FAST_ISVD);
-  const bool alpha_v = (c->variant == FD_ALPHA_FD || c->variant == FD_FAST_ALPHA_FD);
+  const bool alpha_v = (c->variant == FD_ALPHA_FD || c->variant == FD_FAST_ALPHA_FD || literal);
   D->d = c->d;
   D->ldb = (c->d + 3) / 4 * 4;
   D->ell = c->ell;
@@ -84,11 +87,22 @@ bool derive(const fd_config* c, Derived* D, std::string* why) {
     // m = max(1, round(alpha*ell)) (reading C5; round half away from zero)
     D->m = std::max(1, (int)(c->alpha * c->ell + 0.5));
   }
-  D->perrow = !batched;
+  D->R = c->ell - 1;
+  D->t = c->ell;
+  if (literal) {
+    // paper-literal Fast alpha-FD (C25): an ell-row buffer,
+    // delta = lambda_t, t = ell - max(1, ceil(alpha ell / 2)); rows j <= max(ell-m, t-1)
+    // can stay nonzero and are kept, the others are free slots
+    int h = (int)std::ceil(c->alpha * (double)c->ell / 2.0 - 1e-9);
+    h = std::max(1, h);
+    D->t = c->ell - h;
+    D->R = std::max(c->ell - D->m, D->t - 1);
+  }
+  D->perrow = !batched && !literal;
   D->gbytes = D->perrow ? sizeof(double) : sizeof(float);
-  D->nmax = std::max(D->L, 2 * c->ell - 2);
+  D->nmax = std::max(D->L, 2 * D->R);
   if (c->n_shards == 1) D->nmax = D->L;  // merges only via fd_merge (checked there)
-  D->ldg = (std::max(D->nmax, 2 * c->ell - 2) + 3) / 4 * 4;
+  D->ldg = (std::max(D->nmax, 2 * D->R) + 3) / 4 * 4;
   return true;
 }
 
@@ -272,7 +286,7 @@ int build_tree(int lo, int hi, int* next_id, std::vector<Merge>* plan, std::vect
 // Merge the `count` leaves already in node slots 0..count-1 (node stats set).
 fd_status run_tree(fd_handle* h, int count, int* root) {
   if (count == 1) { *root = 0; return FD_OK; }
-  if (2 * h->D.ell - 2 > fdk::kMaxN)
+  if (2 * h->D.R > fdk::kMaxN)
     return fail(FD_ERR_UNSUPPORTED, "merge Gram size 2*ell-2 exceeds FD_MAX_N");
   std::vector<Merge> plan;
   std::vector<int> height(count, 0);
@@ -280,14 +294,14 @@ fd_status run_tree(fd_handle* h, int count, int* root) {
   *root = build_tree(0, count, &next, &plan, &height);
   int maxh = 0;
   for (const Merge& m : plan) maxh = std::max(maxh, m.height);
-  const int ell = h->D.ell;
+  const int R = h->D.R;
   for (int lvl = 1; lvl <= maxh; ++lvl) {
     std::vector<Prob> probs;
     for (const Merge& m : plan) {
       if (m.height != lvl) continue;
       const int slot = (int)probs.size();
-      // [X; Y] without their zero last rows: Gram size 2*ell-2 (same nonzero spectrum)
-      probs.push_back(make_prob(h, slot, node_buf(h, m.a), ell - 1, node_buf(h, m.b), ell - 1, node_buf(h, m.node),
+      // [X; Y] without their zero last rows: Gram size 2R = 2*ell-2 (same nonzero spectrum)
+      probs.push_back(make_prob(h, slot, node_buf(h, m.a), R, node_buf(h, m.b), R, node_buf(h, m.node),
                                 node_stats(h, m.node), node_stats(h, m.a), node_stats(h, m.b)));
     }
     fd_status s = run_reduce(h, probs);
@@ -357,7 +371,7 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
   std::string why;
   if (!derive(cfg, &D, &why)) return fail(FD_ERR_INVALID_ARG, why);
   if (D.L > fdk::kMaxN) return fail(FD_ERR_UNSUPPORTED, "buffer Gram size exceeds FD_MAX_N");
-  if (D.P > 1 && 2 * D.ell - 2 > fdk::kMaxN) return fail(FD_ERR_UNSUPPORTED, "merge Gram size exceeds FD_MAX_N");
+  if (D.P > 1 && 2 * D.R > fdk::kMaxN) return fail(FD_ERR_UNSUPPORTED, "merge Gram size exceeds FD_MAX_N");
   Layout Lo = layout(D);
   if (!ws || ws_bytes < Lo.total) return fail(FD_ERR_WORKSPACE, "workspace too small");
   fd_handle* h = new fd_handle();
@@ -368,6 +382,7 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
   h->stream = static_cast<cudaStream_t>(cuda_stream);
   h->device = cfg->device;
   h->prm.d = D.d; h->prm.ldb = D.ldb; h->prm.ldg = D.ldg; h->prm.ell = D.ell; h->prm.rule = D.rule; h->prm.m = D.m;
+  h->prm.ret = D.R; h->prm.tdel = D.t;
   h->prm.f64 = 0;
   h->prm.pretrd = 0;
   h->prm.zld = D.ldg;
@@ -463,7 +478,7 @@ static fd_status append_impl(fd_handle* h, const float* rows, int64_t n_rows, in
       st[s] += c;
       rm[s] -= c;
       occ[s] += c;
-      if (occ[s] == L) occ[s] = ell - 1;
+      if (occ[s] == L) occ[s] = h->D.R;
     }
   };
   // host staging: copy the chunks of a round into stage slot k (chunk i at i * maxc * ld)
@@ -525,7 +540,7 @@ static fd_status append_impl(fd_handle* h, const float* rows, int64_t n_rows, in
         probs.push_back(make_prob(h, slot, shard_buf(h, s, h->cur[s]), L, nullptr, 0, shard_buf(h, s, h->cur[s] ^ 1),
                                   h->stats + s));
         h->cur[s] ^= 1;
-        h->occ[s] = ell - 1;
+        h->occ[s] = h->D.R;
       }
     }
     if (ing.empty()) break;

@@ -69,12 +69,11 @@ __global__ void __launch_bounds__(kBtThreads, 1) bt_kernel(const Prob* __restric
   float* tau = Yb + 256;                           // [32]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grp = warp >> 3, wg8 = warp & 7;
-  const int ell = p.ell;
 
   for (int pi = blockIdx.x; pi < count; pi += gridDim.x) {
     const Prob P = probs[pi];
     const int N = P.rows0 + P.rows1;
-    const int J = min(ell - 1, N);
+    const int J = min(p.ret, N);
     const int Jp = (J + 3) & ~3;                   // columns updated (multiple of 4, <= 128)
     const float* V = static_cast<const float*>(P.G);
     const float* taug = V + (N * (N + 1) / 2 + 3) / 4 * 4 + 2 * N;
@@ -248,7 +247,7 @@ size_t bt_smem_bytes() {
   return sizeof(float) * ((size_t)kMaxNS * kZld + (size_t)kMaxNS * kVt + 2 * kNbBt * 128 + 2 * kNbBt * 33 + 256 + kNbBt);
 }
 
-bool bt_supported(int nmax, const Params& p) { return p.pretrd && nmax <= kMaxNS && p.ell - 1 <= 128; }
+bool bt_supported(int nmax, const Params& p) { return p.pretrd && nmax <= kMaxNS && p.ret <= 128; }
 
 cudaError_t launch_bt(const Prob* dev_probs, int count, const Params& p, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;

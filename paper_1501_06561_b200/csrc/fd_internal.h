@@ -54,6 +54,8 @@ struct Params {
   int ell;
   int rule;
   int m;         // alpha-FD: number of trailing values that shrink
+  int ret;       // rows kept by a ReduceRank: ell-1, or R of the paper-literal Fast alpha-FD
+  int tdel;      // delta = lambda_tdel (1-based): ell, or t of the paper-literal Fast alpha-FD
   int f64;       // 1: Gram / eigen / reconstruct accumulate in fp64 (per-row chains)
   int pretrd;    // 1: the Gram scratch already holds the tridiagonal form (trd_kernel)
   int zld;       // eig_kernel fp64 scratch stride (>= every problem size of the handle)

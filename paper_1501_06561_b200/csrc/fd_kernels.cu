@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(256) recon_kernel(const Prob* __restrict__ pro
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int r = r0 + wk + q;
-      Ws[wk + q][wj] = (jrow < p.ell - 1 && r < N) ? Wt[(int64_t)jrow * p.ldg + r] : T(0);
+      Ws[wk + q][wj] = (jrow < p.ret && r < N) ? Wt[(int64_t)jrow * p.ldg + r] : T(0);
     }
     float4 bv = z4;
     const int r = r0 + bk;
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(256) recon_kernel(const Prob* __restrict__ pro
     const int c = c0 + tx * 4;
     if (c >= p.ldb) continue;
     float4 o = z4;
-    if (j < p.ell - 1) o = make_float4((float)acc[i][0], (float)acc[i][1], (float)acc[i][2], (float)acc[i][3]);
+    if (j < p.ret) o = make_float4((float)acc[i][0], (float)acc[i][1], (float)acc[i][2], (float)acc[i][3]);
     *reinterpret_cast<float4*>(P.dst + (int64_t)j * p.ldb + c) = o;
   }
 }
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(256, 2) recon128_kernel(const Prob* __restrict
   const Prob P = probs[blockIdx.z];
   const int N = P.rows0 + P.rows1;
   const int n0 = blockIdx.x * 128, j0 = blockIdx.y * 128;
-  const int jrows = p.ell - 1;
+  const int jrows = p.ret;
   if (j0 >= p.ell) return;
   __shared__ __align__(16) float As[2][8][128 + 4];
   __shared__ __align__(16) float Bs[2][8][128 + 4];
@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(256, 2) recon_pipe_kernel(const Prob* __restri
   const Prob P = probs[blockIdx.z];
   const int N = P.rows0 + P.rows1;
   const int n0 = blockIdx.x * 128, j0 = blockIdx.y * 128;
-  const int jrows = p.ell - 1;
+  const int jrows = p.ret;
   if (j0 >= p.ell) return;
   extern __shared__ __align__(16) float rsm[];
   const float* Wt = static_cast<const float*>(P.Wt);
@@ -811,11 +811,13 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
     }  // !p.pretrd
     if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[2] += t_ - t_ph0; t_ph0 = t_; }
     // ---------------- eigenvalues: multisection bisection ----------------
-    const int K = min(ell, N);        // top-K eigenvalues needed (lambda_ell = delta)
-    const int J = min(ell - 1, N);    // retained eigenvectors
+    const int K = min(max(p.tdel, p.ret), N);   // top-K eigenvalues needed (lambda_tdel = delta)
+    const int J = min(p.ret, N);                // retained eigenvectors
     // iSVD's weights jump between J-1 (kept) and J (dropped): a cluster straddling
     // that boundary needs its members beyond J, so a margin of eigenvalues is found
-    const int KC = (p.rule == RULE_ISVD) ? min(N, ell + 16) : K;
+    // (and any rule whose weights drop from unchanged to 0 at J: alpha-FD with m = 1,
+    // the paper-literal Fast alpha-FD when ell - m >= R)
+    const int KC = (p.rule == RULE_ISVD || ell - p.m >= p.ret) ? min(N, max(K, J) + 16) : K;
     T glo = Lim<T>::big(), ghi = -Lim<T>::big(), emax2 = T(0);
     for (int i = tid; i < N; i += blockDim.x) {
       const T em = (i > 0) ? fabs(ee[i - 1]) : T(0);
@@ -908,7 +910,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
     __syncthreads();
     if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[3] += t_ - t_ph0; t_ph0 = t_; }
     // ---------------- ReduceRank rule ----------------
-    const T delta = (ell <= N) ? lam[ell - 1] : T(0);
+    const T delta = (p.tdel <= N) ? lam[p.tdel - 1] : T(0);
     if (tid < J) {
       const T l = lam[tid];
       T sp2;
@@ -1384,7 +1386,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
       }
     }
     // rows J..ell-2 of Wt (only when N < ell-1) are zero
-    for (int j = J + warp; j < ell - 1; j += kNW)
+    for (int j = J + warp; j < p.ret; j += kNW)
       for (int r = lane; r < p.ldg; r += 32) Wt[(int64_t)j * p.ldg + r] = T(0);
     __syncthreads();
     if (p.dbg && blockIdx.x == 0 && tid == 0) {

@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) recon_tc_kernel(const Prob* __r
   const uint32_t tbase = s_tmem;
   uint32_t uses[2] = {0, 0};
   const uint32_t idesc = tc::idesc_tf32(128, 128, 0, 0);
-  const int ell = p.ell, jrows = ell - 1;
+  const int ell = p.ell, jrows = p.ret;
   // TMEM: partials of chunk parity b: hi.hi at 128 b, cross terms at 256 + 128 b
   const uint32_t lanebase = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
   const int half = warp >> 2;                    // columns 64 half .. 64 half + 63 of the tile
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) recon_tc_kernel(const Prob* __r
 }
 
 bool recon_tc_supported(int nmax, const Params& p) {
-  return !p.f64 && p.ell - 1 <= 128 && nmax >= 1 && nmax <= 1024 && (p.ldg % 4) == 0 && (p.ldb % 4) == 0;
+  return !p.f64 && p.ret <= 128 && nmax >= 1 && nmax <= 1024 && (p.ldg % 4) == 0 && (p.ldb % 4) == 0;
 }
 
 cudaError_t launch_recon_tc(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s) {

@@ -409,7 +409,7 @@ static cudaError_t launch_trd_t(const Prob* dev_probs, int count, const Params& 
   return cudaGetLastError();
 }
 
-bool trd_supported(int nmax, const Params& p) { return !p.f64 && nmax > 32 && nmax <= 256 && p.ell - 1 <= 128; }
+bool trd_supported(int nmax, const Params& p) { return !p.f64 && nmax > 32 && nmax <= 256 && p.ret <= 128; }
 
 cudaError_t launch_trd(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;

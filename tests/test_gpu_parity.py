@@ -474,3 +474,35 @@ def test_proj_err_fullsize_c4_bounds():
     lam = np.linalg.eigvalsh(AtA.cpu().numpy())[::-1]
     den = frob - float(np.sum(lam[:10]))
     assert abs(pg["den"] - den) <= 1e-9 * frob
+
+
+# ---------------------------------------------------------------------------
+# paper-literal Fast alpha-FD (C25)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("alpha", [0.2, 0.5, 1.0])
+@pytest.mark.parametrize("shards", [1, 4])
+def test_parity_fast_alpha_fd_paper_c1(alpha, shards):
+    """c1, ell = 16 (N = 16: fused small-N eigensolver), shard streams + merge tree."""
+    check_parity(fdgen.host_rows(fdgen.config("c1")), 16, "fast_alpha_fd_paper", alpha=alpha, n_shards=shards)
+
+
+@pytest.mark.parametrize("ell,alpha", [(40, 0.2), (100, 0.2), (100, 0.8), (128, 0.2)])
+def test_parity_fast_alpha_fd_paper_c2(ell, alpha):
+    """c2: ell-row buffers N = 40..128 (register tridiagonalisation path for N > 32),
+    t = ell - ceil(alpha ell / 2) and R = max(ell - m, t - 1) rows kept."""
+    check_parity(_c2(), ell, "fast_alpha_fd_paper", alpha=alpha, n_shards=2)
+
+
+def test_parity_fast_alpha_fd_paper_c3():
+    """c3's image-like rows (d = 3072), ell = 200, alpha = 0.2: N = 200, 2 shards + merge (R = 179, merge Gram 2R = 358)."""
+    check_parity(_c3(3000), 200, "fast_alpha_fd_paper", alpha=0.2, n_shards=2)
+
+
+def test_fast_alpha_fd_paper_alpha1_matches_fast_fd_on_gpu():
+    """alpha = 1 with 2 ell' rows is Fast FD with ell' (oracle pin): the GPU sketches agree."""
+    A = _c2()
+    B1, _, _ = gpu_sketch(A, 40, "fast_fd", n_shards=3)
+    B2, _, _ = gpu_sketch(A, 80, "fast_alpha_fd_paper", alpha=1.0, n_shards=3)
+    assert not np.any(B2[39:])
+    frob = float(np.sum(A.astype(np.float64) ** 2))
+    assert spec_norm(B1.T @ B1 - B2[:40].T @ B2[:40]) <= 1e-5 * frob
