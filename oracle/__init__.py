@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
-RULE_FD, RULE_ISVD, RULE_FD_T = 0, 1, 2
+RULE_FD, RULE_ISVD, RULE_FD_T, RULE_SS, RULE_CFD = 0, 1, 2, 3, 4
 # variant name -> (rule, alpha, batched)
 VARIANTS = {
     "fd": (RULE_FD, 1.0, False),           # Alg. 1 + FD rule, per-row
@@ -28,6 +28,10 @@ VARIANTS = {
     # paper-literal Fast alpha-FD: ell-row buffer, delta = sigma_t^2,
     # t = ell - ceil(alpha ell / 2) (C25)
     "fast_alpha_fd_paper": (RULE_FD_T, None, "literal"),
+    # SpaceSaving Directions: Alg. 1 with ReduceRank-SS (Alg. 3), per-row
+    "ssd": (RULE_SS, 1.0, False),
+    # Compensative FD: FD, final sigma_hat = sqrt(sigma'^2 + Delta), per-row
+    "cfd": (RULE_CFD, 1.0, False),
 }
 
 _dp = ctypes.POINTER(ctypes.c_double)

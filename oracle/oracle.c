@@ -24,6 +24,12 @@
  *                                 alpha*ell values shrink (m = max(1, round(alpha*ell)),
  *                                 reading C5).
  *   Delta = sum_i delta_i.
+ *   paper-literal Fast alpha-FD: delta = sigma_t^2, t = ell - ceil(alpha ell/2),
+ *                                 ell-row buffer (reading C25).
+ *   SpaceSaving Directions (Alg. 3): delta = sigma_{ell-1}^2,
+ *                                 S' = diag(sigma_1..sigma_{ell-2}, 0, sqrt(sigma_ell^2 + delta)).
+ *   Compensative FD: FD, final step sigma_hat = sqrt(sigma'^2 + Delta).
+ *   proj-err.
  *   cov-err = ||A^T A - B^T B||_2 / ||A||_F^2.
  * Slot semantics (reading C6), final ReduceRank (C9), shard ranges and the
  * recursive-halving merge tree (C10) are the DESIGN.md readings.
@@ -41,6 +47,8 @@
 
 #define ORC_RULE_FD 0   /* alpha-FD with alpha given; FD is alpha = 1 */
 #define ORC_RULE_ISVD 1
+#define ORC_RULE_CFD 4  /* Compensative FD: FD rule + compensated final step */
+#define ORC_RULE_SS 3   /* SpaceSaving Directions, ReduceRank-SS (Alg. 3)  */
 #define ORC_RULE_FD_T 2 /* paper-literal Fast alpha-FD: delta = sigma_t^2,
                            t = ell - ceil(alpha ell / 2), buffer of ell rows */
 
@@ -119,6 +127,7 @@ typedef struct {
 typedef struct {
   int L, ell, rule, m;
   int t;   /* delta = lambda_t (1-based): ell for every rule but ORC_RULE_FD_T     */
+  double comp;  /* >= 0: Compensative FD final step with this Delta */
   int R;   /* rows kept after a ReduceRank (slot semantics, C6): ell-1, or R_t    */
   int64_t d;
   double *G, *V, *lam, *w, *Bn;
@@ -141,7 +150,7 @@ static void fd_t_indices(int ell, double alpha, int* t, int* R) {
 
 static int work_init(orc_work* W, int L, int64_t d, int ell, int rule, int m) {
   W->L = L; W->d = d; W->ell = ell; W->rule = rule; W->m = m;
-  W->t = ell; W->R = ell - 1;
+  W->t = ell; W->R = ell - 1; W->comp = -1.0;
   W->G = malloc(sizeof(double) * L * L);
   W->V = malloc(sizeof(double) * L * L);
   W->lam = malloc(sizeof(double) * L);
@@ -182,21 +191,52 @@ static int reduce_rank(orc_work* W, double* Bf, orc_stats* st) {
    * Fast alpha-FD */
   double delta = (W->t <= L) ? lams[W->t - 1] : 0.0;
   double removed = 0.0;
+  int src_last = -1;   /* SS: output row ell-2 takes direction ell-1 (0-based) */
+  if (W->rule == ORC_RULE_SS) {
+    /* ReduceRank-SS: delta = sigma_{ell-1}^2; return diag(sigma_1..sigma_{ell-2}, 0,
+     * sqrt(sigma_ell^2 + delta)).  Slot semantics: the direction of sigma_ell is kept
+     * in row ell-2 (0-based), row ell-1 is the free slot.  Reading C26: if sigma_ell = 0
+     * (buffer rank <= ell-1; sigma_ell^2 <= 1e-12 sigma_1^2, the fp64 eigensolver's
+     * resolution) the step is lossless (delta = 0, nothing moves). */
+    delta = 0.0;
+    if (ell <= L && lams[ell - 1] > 1e-12 * lams[0]) { delta = lams[ell - 2]; src_last = ell - 1; }
+  }
+  double sp2s[1024];
+  double* sp2v = (L <= 1024) ? sp2s : malloc(sizeof(double) * L);
   for (int j = 0; j < L; ++j) {
     double sp2; /* sigma'_j^2 for 0-based j */
-    if (j >= W->R) sp2 = 0.0; /* rows R.. are freed; sigma'_ell = 0 in every rule */
+    if (W->rule == ORC_RULE_SS) {
+      if (src_last >= 0) sp2 = (j < ell - 2) ? lams[j] : (j == ell - 1 ? lams[j] + delta : 0.0);
+      else sp2 = (j < ell - 1) ? lams[j] : 0.0;
+    }
+    else if (j >= W->R) sp2 = 0.0; /* rows R.. are freed; sigma'_ell = 0 in every rule */
     else if (W->rule == ORC_RULE_ISVD) sp2 = lams[j];
     else if (j < ell - W->m) sp2 = lams[j]; /* alpha-FD: first ell-m unchanged */
     else sp2 = (lams[j] - delta > 0.0) ? lams[j] - delta : 0.0;
     removed += lams[j] - sp2;
-    W->w[j] = (lams[j] > 0.0) ? sqrt(sp2) / sqrt(lams[j]) : 0.0;
+    sp2v[j] = sp2;
   }
+  /* Compensative FD, final step: sigma_hat_j = sqrt(sigma'_j^2 + Delta)
+   * for every one of the ell directions, Delta including this step's delta.  A
+   * direction with sigma_j = 0 has no defined v_j here and gets nothing (reading C27). */
+  int nout = (W->rule == ORC_RULE_SS) ? ell - 1 : W->R;
+  if (W->comp >= 0.0) {
+    const double Dt = W->comp + delta;
+    nout = ell;
+    for (int j = 0; j < ell && j < L; ++j) {
+      const double add = (lams[j] > 0.0) ? Dt : 0.0;
+      removed -= add;
+      sp2v[j] += add;
+    }
+  }
+  for (int j = 0; j < L; ++j) W->w[j] = (lams[j] > 0.0) ? sqrt(sp2v[j]) / sqrt(lams[j]) : 0.0;
   /* B'_j = w_j * u_j^T Bf  (u_j = column order[j] of V) */
   memset(W->Bn, 0, sizeof(double) * (size_t)L * d);
-  for (int j = 0; j < W->R && j < L; ++j) {
-    double wj = W->w[j];
+  for (int j = 0; j < nout && j < L; ++j) {
+    const int sj = (src_last >= 0 && j == ell - 2) ? src_last : j;
+    double wj = W->w[sj];
     if (wj == 0.0) continue;
-    int c = W->order[j];
+    int c = W->order[sj];
     double* out = W->Bn + (size_t)j * d;
     for (int r = 0; r < L; ++r) {
       double coef = wj * W->V[(size_t)r * L + c];
@@ -205,6 +245,7 @@ static int reduce_rank(orc_work* W, double* Bf, orc_stats* st) {
       for (int64_t k = 0; k < d; ++k) out[k] += coef * in[k];
     }
   }
+  if (sp2v != sp2s) free(sp2v);
   memcpy(Bf, W->Bn, sizeof(double) * (size_t)L * d);
   st->delta_total += delta;
   st->removed += removed;
@@ -247,6 +288,9 @@ typedef struct {
   const float* A; int64_t lda, d;
   const int64_t* seg_start; const int64_t* seg_len; int nseg;
   int L, ell, rule, m, t, R;
+  int comp_final;  /* Compensative FD with P = 1: the shard's final ReduceRank compensates */
+  int lazy;        /* Compensative FD: ReduceRank when a row arrives at a full buffer, so the
+                      final step (C9) is the last full-buffer SVD (reading C27) */
   double* B_out;   /* ell x d */
   orc_stats st;
   int rc;
@@ -264,18 +308,23 @@ static void run_shard(orc_shard_job* J) {
   for (int s = 0; s < J->nseg && J->rc == 0; ++s) {
     for (int64_t r = 0; r < J->seg_len[s]; ++r) {
       const float* a = J->A + (J->seg_start[s] + r) * J->lda;
+      if (J->lazy && occ == J->L) {
+        if (reduce_rank(&W, Bf, &J->st)) { J->rc = -1; break; }
+        occ = J->R;
+      }
       double* slot = Bf + (size_t)occ * d;
       double nrm = 0.0;
       for (int64_t k = 0; k < d; ++k) { slot[k] = (double)a[k]; nrm += slot[k] * slot[k]; }
       J->st.frob_sq += nrm;
       J->st.rows_seen += 1;
       occ += 1;
-      if (occ == J->L) {
+      if (!J->lazy && occ == J->L) {
         if (reduce_rank(&W, Bf, &J->st)) { J->rc = -1; break; }
         occ = J->R;
       }
     }
   }
+  if (J->comp_final) W.comp = J->st.delta_total;
   if (J->rc == 0 && reduce_rank(&W, Bf, &J->st)) J->rc = -1; /* final ReduceRank (C9) */
   memcpy(J->B_out, Bf, sizeof(double) * (size_t)J->ell * d);
   free(Bf);
@@ -300,10 +349,10 @@ static void* pool_worker(void* arg) {
 
 /* merge(X, Y) = ReduceRank([X; Y]) with L = 2 ell (reading C10). */
 static int merge2(const double* X, const double* Y, int64_t d, int ell, int rule, int m, int t, int R,
-                  double* out, orc_stats* st) {
+                  double comp, double* out, orc_stats* st) {
   orc_work W;
   if (work_init(&W, 2 * ell, d, ell, rule, m)) return -2;
-  W.t = t; W.R = R;
+  W.t = t; W.R = R; W.comp = comp;
   double* Bf = malloc(sizeof(double) * (size_t)2 * ell * d);
   memcpy(Bf, X, sizeof(double) * (size_t)ell * d);
   memcpy(Bf + (size_t)ell * d, Y, sizeof(double) * (size_t)ell * d);
@@ -315,16 +364,18 @@ static int merge2(const double* X, const double* Y, int64_t d, int ell, int rule
 }
 
 /* Recursive-halving tree over sketches [lo, hi): left half has ceil((hi-lo)/2). */
+/* comp_root: Compensative FD -- the root merge (the last ReduceRank of the DAG) is
+ * the compensated final step, with Delta = everything accumulated before it. */
 static int merge_tree(double* S, int lo, int hi, int64_t d, int ell, int rule, int m, int t, int R,
-                      double* out, orc_stats* st) {
+                      int comp_root, double* out, orc_stats* st) {
   size_t sz = (size_t)ell * d;
   if (hi - lo == 1) { memcpy(out, S + (size_t)lo * sz, sizeof(double) * sz); return 0; }
   int mid = lo + (hi - lo + 1) / 2;
   double* X = malloc(sizeof(double) * sz);
   double* Y = malloc(sizeof(double) * sz);
-  int rc = merge_tree(S, lo, mid, d, ell, rule, m, t, R, X, st);
-  if (!rc) rc = merge_tree(S, mid, hi, d, ell, rule, m, t, R, Y, st);
-  if (!rc) rc = merge2(X, Y, d, ell, rule, m, t, R, out, st);
+  int rc = merge_tree(S, lo, mid, d, ell, rule, m, t, R, 0, X, st);
+  if (!rc) rc = merge_tree(S, mid, hi, d, ell, rule, m, t, R, 0, Y, st);
+  if (!rc) rc = merge2(X, Y, d, ell, rule, m, t, R, comp_root ? st->delta_total : -1.0, out, st);
   free(X); free(Y);
   return rc;
 }
@@ -333,13 +384,13 @@ static int merge_tree(double* S, int lo, int hi, int64_t d, int ell, int rule, i
  * other rules: alpha unused beyond m. */
 int oracle_merge(const double* sketches, int count, int64_t d, int ell, int rule, int m, double alpha,
                  double* B_out, double* stats5) {
-  if (count < 1) return -3;
+  if (count < 1 || rule == ORC_RULE_CFD) return -3;   /* CFD: no merge of finished sketches (C27) */
   int t = ell, R = ell - 1;
   if (rule == ORC_RULE_FD_T) fd_t_indices(ell, alpha, &t, &R);
   orc_stats st = {0};
   double* S = malloc(sizeof(double) * (size_t)count * ell * d);
   memcpy(S, sketches, sizeof(double) * (size_t)count * ell * d);
-  int rc = merge_tree(S, 0, count, d, ell, rule, m, t, R, B_out, &st);
+  int rc = merge_tree(S, 0, count, d, ell, rule, m, t, R, 0, B_out, &st);
   free(S);
   if (stats5) { stats5[0] = 0; stats5[1] = st.delta_total; stats5[2] = st.removed; stats5[3] = (double)st.n_shrinks; stats5[4] = 0; }
   return rc;
@@ -393,6 +444,8 @@ int oracle_sketch(const float* A, int64_t n, int64_t lda, int64_t d, int ell, in
     J->A = A; J->lda = lda; J->d = d;
     J->seg_start = starts + (size_t)s * nappend; J->seg_len = lens + (size_t)s * nappend; J->nseg = nappend;
     J->L = L; J->ell = ell; J->rule = rule; J->m = m; J->t = tt; J->R = RR;
+    J->comp_final = (rule == ORC_RULE_CFD && P == 1);
+    J->lazy = (rule == ORC_RULE_CFD);
     J->B_out = S + (size_t)s * ell * d;
   }
   if (nthreads < 1) nthreads = 1;
@@ -413,7 +466,7 @@ int oracle_sketch(const float* A, int64_t n, int64_t lda, int64_t d, int ell, in
     tot.rows_seen += jobs[s].st.rows_seen;
   }
   if (shard_out) memcpy(shard_out, S, sizeof(double) * (size_t)P * ell * d);
-  if (!rc && B_out) rc = merge_tree(S, 0, P, d, ell, rule, m, tt, RR, B_out, &tot);
+  if (!rc && B_out) rc = merge_tree(S, 0, P, d, ell, rule, m, tt, RR, rule == ORC_RULE_CFD, B_out, &tot);
   if (stats5) {
     stats5[0] = tot.frob_sq; stats5[1] = tot.delta_total; stats5[2] = tot.removed;
     stats5[3] = (double)tot.n_shrinks; stats5[4] = (double)tot.rows_seen;

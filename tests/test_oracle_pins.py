@@ -174,7 +174,11 @@ def _c1():
     return fdgen.host_rows(w)
 
 
-@pytest.mark.parametrize("variant", list(oracle.VARIANTS))
+# the FD family (SSD and CFD have their own bounds, Theorem SS / PAPER.md:436, below)
+FD_FAMILY = [v for v in oracle.VARIANTS if v not in ("ssd", "cfd")]
+
+
+@pytest.mark.parametrize("variant", FD_FAMILY)
 def test_properties_lemma1_lemma3(variant):
     """Props 1-2 via Lemma 1 (PAPER.md:330-347): 0 <= ||Ax||^2-||Bx||^2 <= Delta;
     Lemma 3: ||A||_F^2 - ||B||_F^2 = removed, = ell*Delta (FD per-row),
@@ -487,3 +491,86 @@ def test_fast_alpha_fd_paper_bounds():
         frob_a, frob_b = np.sum(A ** 2), np.sum(r.B ** 2)
         assert abs((frob_a - frob_b) - r.removed) < 1e-8 * frob_a
         assert (frob_a - frob_b) >= (t - ell + m) * r.delta_total * (1 - 1e-9)
+
+
+# ---------------------------------------------------------------------------
+# SpaceSaving Directions and Compensative FD
+# ---------------------------------------------------------------------------
+def test_ss_rule_closed_form():
+    """ReduceRank-SS (Alg. 3) on a buffer with known singular values
+    s_j e_{pi(j)}: delta = s_{ell-1}^2; the result has s_1..s_{ell-2}, 0 and
+    sqrt(s_ell^2 + delta) along e_{pi(ell)}; the squared mass is unchanged."""
+    ell, d = 9, 23
+    rng = np.random.default_rng(21)
+    s = np.sort(rng.uniform(1.0, 5.0, ell))[::-1]
+    perm = rng.permutation(d)[:ell]
+    Bf = np.zeros((ell, d))
+    for j in range(ell):
+        Bf[j, perm[j]] = s[j]
+    Bf = Bf[rng.permutation(ell)]
+    B, delta, removed = oracle.reduce_rank(Bf, ell, rule=oracle.RULE_SS)
+    assert abs(delta - s[ell - 2] ** 2) < 1e-12 * s[0] ** 2
+    assert abs(removed) < 1e-10 * s[0] ** 2
+    col = np.sum(B ** 2, axis=0)                      # mass per original axis
+    expect = np.zeros(d)
+    expect[perm[: ell - 2]] = s[: ell - 2] ** 2
+    expect[perm[ell - 1]] = s[ell - 1] ** 2 + s[ell - 2] ** 2
+    np.testing.assert_allclose(col, expect, atol=1e-10 * s[0] ** 2)
+    assert np.all(B[ell - 1] == 0.0)                   # the free slot
+
+
+def test_ssd_theorem_ss_bounds():
+    """Theorem SS (PAPER.md:417-421): ||A||_F^2 = ||B||_F^2;
+    | ||Ax||^2 - ||Bx||^2 | <= ||A - A_k||_F^2 / (ell/2 - 1/2 - k) for k < ell/2 - 1/2;
+    ||A - pi_B^k(A)||_F^2 <= ||A - A_k||_F^2 (ell - 1) / (ell - 1 - 2k) for k < ell/2 - 1."""
+    A = _c1()
+    A64 = A.astype(np.float64)
+    sv2 = np.linalg.svd(A64, compute_uv=False) ** 2
+    for ell in (12, 16, 24):
+        r = oracle.sketch(A, ell, "ssd")
+        fa = float(np.sum(A64 ** 2))
+        assert abs(float(np.sum(r.B ** 2)) - fa) <= 1e-9 * fa
+        w = np.linalg.eigvalsh(A64.T @ A64 - r.B.T @ r.B)
+        nrm = max(abs(w[0]), abs(w[-1]))
+        k = 0
+        while k < ell / 2 - 0.5:
+            assert nrm <= np.sum(sv2[k:]) / (ell / 2 - 0.5 - k) * (1 + 1e-9)
+            k += 1
+        for k in range(1, int(np.ceil(ell / 2 - 1))):
+            if k < ell / 2 - 1:
+                p = oracle.proj_err(A, r.B, k=k)
+                assert p["err"] <= (ell - 1) / (ell - 1 - 2 * k) * (1 + 1e-9)
+
+
+def test_ssd_lossless_when_rank_below_ell():
+    """Reading C26: a buffer of rank <= ell-1 (sigma_ell = 0) is compressed losslessly."""
+    rng = np.random.default_rng(4)
+    ell, d = 7, 19
+    A = (rng.standard_normal((200, ell - 1)) @ rng.standard_normal((ell - 1, d))).astype(np.float32)
+    r = oracle.sketch(A, ell, "ssd")
+    AtA, frob = oracle.gram(A)
+    assert np.abs(AtA - r.B.T @ r.B).max() <= 1e-10 * frob
+    assert r.delta_total == 0.0
+
+
+@pytest.mark.parametrize("shards", [1, 3])
+def test_cfd_is_fd_plus_delta_on_ell_directions(shards):
+    """CFD runs FD and compensates only the final step: B_cfd^T B_cfd -
+    B_fd^T B_fd = Delta * (projector onto the final ell directions): ell eigenvalues
+    Delta, the rest 0.  With one stream the mass is preserved, ||A||_F^2 = ||B||_F^2, and
+    | ||Ax||^2 - ||Bx||^2 | <= Delta (PAPER.md:436)."""
+    A = _c1()
+    ell = 16
+    rf = oracle.sketch(A, ell, "fd", n_shards=shards)
+    rc = oracle.sketch(A, ell, "cfd", n_shards=shards)
+    assert abs(rc.delta_total - rf.delta_total) <= 1e-12 * rf.delta_total
+    Dl = rf.delta_total
+    w = np.linalg.eigvalsh(rc.B.T @ rc.B - rf.B.T @ rf.B)[::-1]
+    np.testing.assert_allclose(w[:ell], Dl, rtol=1e-8)
+    assert np.all(np.abs(w[ell:]) <= 1e-8 * Dl)
+    A64 = A.astype(np.float64)
+    if shards == 1:
+        fa = float(np.sum(A64 ** 2))
+        assert abs(float(np.sum(rc.B ** 2)) - fa) <= 1e-9 * fa
+        m = np.linalg.eigvalsh(A64.T @ A64 - rc.B.T @ rc.B)
+        assert max(abs(m[0]), abs(m[-1])) <= Dl * (1 + 1e-9)
