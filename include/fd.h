@@ -67,10 +67,16 @@ typedef enum {
   FD_FAST_ALPHA_FD = 3, /* Alg. 2 rule on the 2*ell buffer (C3)                                  */
   FD_ISVD = 4,          /* sigma'_j = sigma_j for j < ell, sigma'_ell = 0, per-row */
   FD_FAST_ISVD = 5,     /* iSVD rule on the 2*ell buffer                                         */
-  FD_FAST_ALPHA_FD_PAPER = 6 /* paper-literal Fast alpha-FD: ell-row buffer,
+  FD_FAST_ALPHA_FD_PAPER = 6, /* paper-literal Fast alpha-FD: ell-row buffer,
                            delta = sigma_t^2 with t = ell - max(1, ceil(alpha*ell/2)); the last
                            m = max(1, round(alpha*ell)) values shrink; rows j <= max(ell-m, t-1)
                            are kept (C25).  Output: ell rows, rows >= that count 0 */
+  FD_SSD = 7,           /* SpaceSaving Directions: Alg. 1 with ReduceRank-SS (Alg. 3):
+                           delta = sigma_{ell-1}^2, sigma_{ell-1} -> 0, sigma_ell -> sqrt(sigma_ell^2 + delta);
+                           per-row (C26) */
+  FD_CFD = 8            /* Compensative FD: FD per-row, the final step returns
+                           sqrt(sigma'^2 + Delta) on all ell directions; ReduceRank runs when a row
+                           arrives at a full buffer (C27).  fd_merge: UNSUPPORTED */
 } fd_variant;
 
 /* Largest eigen-problem (buffer Gram) size supported by this build. */

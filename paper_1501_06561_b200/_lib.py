@@ -18,7 +18,7 @@ STATUS = {
     -8: "FD_ERR_UNSUPPORTED", -9: "FD_ERR_STATE",
 }
 VARIANT = {"fd": 0, "fast_fd": 1, "alpha_fd": 2, "fast_alpha_fd": 3, "isvd": 4, "fast_isvd": 5,
-           "fast_alpha_fd_paper": 6}
+           "fast_alpha_fd_paper": 6, "ssd": 7, "cfd": 8}
 FD_MAX_N = 416
 
 # every symbol include/fd.h declares (checked by tests/test_abi.py)

@@ -55,6 +55,7 @@ struct Derived {
   int ell, L, P, rule, m, ldg, nmax;
   int R;         // rows kept by a ReduceRank (ell-1; paper-literal Fast alpha-FD: max(ell-m, t-1))
   int t;         // delta = lambda_t (ell; paper-literal Fast alpha-FD: ell - ceil(alpha ell/2))
+  bool cfd;      // Compensative FD: lazy ReduceRank + compensated final step (reading C27)
   bool perrow;   // Alg. 1 per-row chain (buffer L = ell)
   size_t gbytes; // element size of the Gram / Wt scratch
 };
@@ -70,7 +71,7 @@ bool derive(const fd_config* c, Derived* D, std::string* why) {
   if (c->d < 1) { *why = "d < 1"; return false; }
   if (c->ell < 2) { *why = "ell < 2"; return false; }
   if (c->n_shards < 1) { *why = "n_shards < 1"; return false; }
-  if (c->variant < FD_FD || c->variant > FD_FAST_ALPHA_FD_PAPER) { *why = "unknown variant"; return false; }
+  if (c->variant < FD_FD || c->variant > FD_CFD) { *why = "unknown variant"; return false; }
   const bool literal = (c->variant == FD_FAST_ALPHA_FD_PAPER);
   const bool batched = (c->variant == FD_FAST_FD || c->variant == FD_FAST_ALPHA_FD || c->variant == FD_FAST_ISVD);
   const bool isvd = (c->variant == FD_ISVD || c->variant == FD_FAST_ISVD);
@@ -80,7 +81,8 @@ bool derive(const fd_config* c, Derived* D, std::string* why) {
   D->ell = c->ell;
   D->L = batched ? 2 * c->ell : c->ell;
   D->P = c->n_shards;
-  D->rule = isvd ? fdk::RULE_ISVD : fdk::RULE_FD;
+  D->rule = isvd ? fdk::RULE_ISVD : (c->variant == FD_SSD ? fdk::RULE_SS : fdk::RULE_FD);
+  D->cfd = (c->variant == FD_CFD);
   D->m = c->ell;
   if (alpha_v) {
     if (!(c->alpha > 0.0 && c->alpha <= 1.0)) { *why = "alpha must be in (0,1]"; return false; }
@@ -221,7 +223,7 @@ cudaError_t timed(fd_handle* h, int kind, F f) {
   return e;
 }
 
-fd_status run_reduce(fd_handle* h, const std::vector<Prob>& probs) {
+fd_status run_reduce(fd_handle* h, const std::vector<Prob>& probs, bool comp = false) {
   if (probs.empty()) return FD_OK;
   int nmax = 0;
   for (const Prob& p : probs) nmax = std::max(nmax, p.rows0 + p.rows1);
@@ -230,6 +232,10 @@ fd_status run_reduce(fd_handle* h, const std::vector<Prob>& probs) {
   if (s != FD_OK) return s;
   const int n = (int)probs.size();
   Params prm = h->prm;
+  if (comp) {   // Compensative FD final step: all ell directions get sigma'^2 + Delta
+    prm.comp = 1;
+    prm.ret = h->D.ell;
+  }
   prm.f64 = use_f64(h->D, nmax) ? 1 : 0;
   prm.pretrd = (!h->legacy_trd && fdk::trd_supported(nmax, prm)) ? 1 : 0;
   cudaError_t e;
@@ -284,7 +290,7 @@ int build_tree(int lo, int hi, int* next_id, std::vector<Merge>* plan, std::vect
 }
 
 // Merge the `count` leaves already in node slots 0..count-1 (node stats set).
-fd_status run_tree(fd_handle* h, int count, int* root) {
+fd_status run_tree(fd_handle* h, int count, int* root, bool comp = false) {
   if (count == 1) { *root = 0; return FD_OK; }
   if (2 * h->D.R > fdk::kMaxN)
     return fail(FD_ERR_UNSUPPORTED, "merge Gram size 2*ell-2 exceeds FD_MAX_N");
@@ -304,7 +310,7 @@ fd_status run_tree(fd_handle* h, int count, int* root) {
       probs.push_back(make_prob(h, slot, node_buf(h, m.a), R, node_buf(h, m.b), R, node_buf(h, m.node),
                                 node_stats(h, m.node), node_stats(h, m.a), node_stats(h, m.b)));
     }
-    fd_status s = run_reduce(h, probs);
+    fd_status s = run_reduce(h, probs, comp && lvl == maxh);   // CFD: the root is the final step
     if (s != FD_OK) return s;
   }
   return FD_OK;
@@ -341,7 +347,7 @@ fd_status read_stats(fd_handle* h, const Stats* dev, fd_stats* st) {
 }
 
 // Final ReduceRank of shards [s0, s1) into node slots (non-destructive snapshot).
-fd_status finalize_shards(fd_handle* h, int s0, int s1) {
+fd_status finalize_shards(fd_handle* h, int s0, int s1, bool comp = false) {
   // leaf node stats start as copies of the shard stats
   FD_CUDA(cudaMemcpyAsync(node_stats(h, s0), h->stats + s0, sizeof(Stats) * (s1 - s0), cudaMemcpyDeviceToDevice,
                           h->stream));
@@ -350,7 +356,7 @@ fd_status finalize_shards(fd_handle* h, int s0, int s1) {
     probs.push_back(make_prob(h, (int)probs.size(), shard_buf(h, s, h->cur[s]), h->occ[s], nullptr, 0,
                               node_buf(h, s), node_stats(h, s)));
   }
-  return run_reduce(h, probs);
+  return run_reduce(h, probs, comp);
 }
 
 }  // namespace
@@ -382,7 +388,7 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
   h->stream = static_cast<cudaStream_t>(cuda_stream);
   h->device = cfg->device;
   h->prm.d = D.d; h->prm.ldb = D.ldb; h->prm.ldg = D.ldg; h->prm.ell = D.ell; h->prm.rule = D.rule; h->prm.m = D.m;
-  h->prm.ret = D.R; h->prm.tdel = D.t;
+  h->prm.ret = D.R; h->prm.tdel = D.t; h->prm.comp = 0;
   h->prm.f64 = 0;
   h->prm.pretrd = 0;
   h->prm.zld = D.ldg;
@@ -478,7 +484,7 @@ static fd_status append_impl(fd_handle* h, const float* rows, int64_t n_rows, in
       st[s] += c;
       rm[s] -= c;
       occ[s] += c;
-      if (occ[s] == L) occ[s] = h->D.R;
+      if (occ[s] == L && (!h->D.cfd || rm[s] > 0)) occ[s] = h->D.R;
     }
   };
   // host staging: copy the chunks of a round into stage slot k (chunk i at i * maxc * ld)
@@ -502,6 +508,19 @@ static fd_status append_impl(fd_handle* h, const float* rows, int64_t n_rows, in
     FD_CUDA(cudaEventRecord(h->ev_copied[slot], h->copy_stream));
     return FD_OK;
   };
+  if (h->D.cfd) {   // Compensative FD, lazy ReduceRank: buffers the previous call left full
+    std::vector<Prob> pre;
+    for (int s = 0; s < P; ++s) {
+      if (h->occ[s] == L && rem[s] > 0) {
+        pre.push_back(make_prob(h, (int)pre.size(), shard_buf(h, s, h->cur[s]), L, nullptr, 0,
+                                shard_buf(h, s, h->cur[s] ^ 1), h->stats + s));
+        h->cur[s] ^= 1;
+        h->occ[s] = h->D.R;
+      }
+    }
+    fd_status e = run_reduce(h, pre);
+    if (e != FD_OK) return e;
+  }
   std::vector<int> pocc = h->occ;   // planning copies (host staging runs one round ahead)
   std::vector<int64_t> pst = start, prm = rem;
   std::vector<Chunk> cur_ch, next_ch;
@@ -535,7 +554,7 @@ static fd_status append_impl(fd_handle* h, const float* rows, int64_t n_rows, in
       start[s] += c;
       rem[s] -= c;
       h->occ[s] += c;
-      if (h->occ[s] == L) {
+      if (h->occ[s] == L && (!h->D.cfd || rem[s] > 0)) {   // CFD: lazy (reading C27)
         const int slot = (int)probs.size();
         probs.push_back(make_prob(h, slot, shard_buf(h, s, h->cur[s]), L, nullptr, 0, shard_buf(h, s, h->cur[s] ^ 1),
                                   h->stats + s));
@@ -585,10 +604,11 @@ fd_status fd_append_rows_host(fd_handle* h, const float* host_rows, int64_t n_ro
 fd_status fd_sketch(fd_handle* h, float* B_out, fd_stats* st) {
   if (!h || !B_out) return fail(FD_ERR_INVALID_ARG, "NULL argument");
   if (h->dead) return fail(FD_ERR_STATE, "handle refuses work after a sticky error");
-  fd_status s = finalize_shards(h, 0, h->D.P);
+  const bool cfd = h->D.cfd;
+  fd_status s = finalize_shards(h, 0, h->D.P, cfd && h->D.P == 1);
   if (s != FD_OK) return s;
   int root = 0;
-  s = run_tree(h, h->D.P, &root);
+  s = run_tree(h, h->D.P, &root, cfd);
   if (s != FD_OK) return s;
   FD_CUDA(cudaMemcpy2DAsync(B_out, h->D.d * sizeof(float), node_buf(h, root), h->D.ldb * sizeof(float),
                             h->D.d * sizeof(float), h->D.ell, cudaMemcpyDeviceToDevice, h->stream));
@@ -600,6 +620,8 @@ fd_status fd_merge(fd_handle* h, const float* sketches, int32_t count, float* B_
   if (!h || !sketches || !B_out) return fail(FD_ERR_INVALID_ARG, "NULL argument");
   if (h->dead) return fail(FD_ERR_STATE, "handle refuses work after a sticky error");
   if (count < 1 || count > kMergeMax) return fail(FD_ERR_INVALID_ARG, "count must be in [1, 64]");
+  if (h->D.cfd)
+    return fail(FD_ERR_UNSUPPORTED, "Compensative FD sketches are final (compensated); merge the handle's shards via fd_sketch");
   const int ell = h->D.ell;
   FD_CUDA(cudaMemcpy2DAsync(node_buf(h, 0), h->D.ldb * sizeof(float), sketches, h->D.d * sizeof(float),
                             h->D.d * sizeof(float), (size_t)count * ell, cudaMemcpyDeviceToDevice, h->stream));

@@ -12,7 +12,7 @@ constexpr int kMaxNS = 256;         // largest size whose packed matrix / eigenv
 constexpr int kMaxN64 = 160;        // largest problem run in fp64 (per-row chains)
 constexpr int kEigThreads = 512;
 
-enum Rule : int { RULE_FD = 0, RULE_ISVD = 1 };
+enum Rule : int { RULE_FD = 0, RULE_ISVD = 1, RULE_SS = 3 };   // SS: ReduceRank-SS (Alg. 3)
 
 // Per-shard / per-node statistics, fp64 (device).
 struct Stats {
@@ -56,6 +56,7 @@ struct Params {
   int m;         // alpha-FD: number of trailing values that shrink
   int ret;       // rows kept by a ReduceRank: ell-1, or R of the paper-literal Fast alpha-FD
   int tdel;      // delta = lambda_tdel (1-based): ell, or t of the paper-literal Fast alpha-FD
+  int comp;      // 1: Compensative FD final step, sigma_hat^2 = sigma'^2 + Delta on ret = ell rows
   int f64;       // 1: Gram / eigen / reconstruct accumulate in fp64 (per-row chains)
   int pretrd;    // 1: the Gram scratch already holds the tridiagonal form (trd_kernel)
   int zld;       // eig_kernel fp64 scratch stride (>= every problem size of the handle)

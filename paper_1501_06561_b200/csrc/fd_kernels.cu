@@ -910,12 +910,42 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
     __syncthreads();
     if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[3] += t_ - t_ph0; t_ph0 = t_; }
     // ---------------- ReduceRank rule ----------------
-    const T delta = (p.tdel <= N) ? lam[p.tdel - 1] : T(0);
+    // s_a1 = delta; s_a2 = 1 when ReduceRank-SS moves sigma_{ell-1}^2;
+    // red[50] = Delta after this step (Compensative FD final step)
+    if (tid == 0) {
+      T dl = (p.tdel <= N) ? lam[p.tdel - 1] : T(0);
+      T moved = T(0);
+      if (p.rule == RULE_SS) {
+        // delta = sigma_{ell-1}^2; the direction of sigma_ell (position ell-1) takes it
+        // and is kept in output row ell-2 (swap, so the kept set stays 0..ell-2).
+        // Reading C26: sigma_ell = 0 (buffer rank <= ell-1) -> lossless, nothing moves.
+        const T tol = (sizeof(T) == 8) ? T(1e-12) : T(1e-5);
+        dl = T(0);
+        if (ell <= N && lam[ell - 1] > tol * lam[0]) {
+          dl = lam[ell - 2];
+          const T x = lam[ell - 2];
+          lam[ell - 2] = lam[ell - 1];
+          lam[ell - 1] = x;
+          moved = T(1);
+        }
+      }
+      s_a1 = dl;
+      s_a2 = moved;
+      if (p.comp) {
+        double dt = (double)dl;
+        if (P.stats) dt += P.child0 ? (P.child0->delta + P.child1->delta) : P.stats->delta;
+        red[50] = (T)dt;
+      }
+    }
+    __syncthreads();
+    const T delta = s_a1;
     if (tid < J) {
       const T l = lam[tid];
       T sp2;
-      if (p.rule == RULE_ISVD || tid < ell - p.m) sp2 = l;
+      if (p.rule == RULE_SS) sp2 = (s_a2 != T(0) && tid == ell - 2) ? l + delta : l;
+      else if (p.rule == RULE_ISVD || tid < ell - p.m) sp2 = l;
       else sp2 = fmax(l - delta, T(0));
+      if (p.comp && l > T(0)) sp2 += red[50];   // reading C27: sigma_j = 0 gets nothing
       spv[tid] = sp2;
       wgt[tid] = (l > T(0)) ? sqrt(sp2 / l) : T(0);
     }
