@@ -253,3 +253,22 @@ def fd_t_indices(ell, alpha):
     m = alpha_m(ell, alpha)
     t = ell - h
     return t, max(ell - m, t - 1)
+
+
+def hash_sketch(A, ell, s=4, seed=0, row0=0, B=None):
+    """Hashing (s = 1) / OSNAP (s stacked blocks) sketch: B += S A with
+    S = s count-sketch blocks of ell/s rows, entries +-1/sqrt(s) (C28)."""
+    A = np.ascontiguousarray(A, dtype=np.float32)
+    n, d = A.shape
+    out = np.zeros((ell, d)) if B is None else B
+    assert out.shape == (ell, d) and out.dtype == np.float64 and out.flags.c_contiguous
+    L = lib()
+    if not getattr(L, "_hash_typed", False):
+        L.oracle_hash_sketch.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                         ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p]
+        L.oracle_hash_sketch.restype = ctypes.c_int
+        L._hash_typed = True
+    rc = L.oracle_hash_sketch(A.ctypes.data, n, d, d, int(ell), int(s), int(seed), int(row0), out.ctypes.data)
+    if rc:
+        raise ValueError("hash_sketch: need 1 <= s <= ell and s | ell")
+    return out

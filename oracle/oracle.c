@@ -759,3 +759,38 @@ int oracle_proj_err(const float* A, int64_t n, int64_t lda, int64_t d, const dou
   free(M); free(G); free(U); free(s2); free(ord); free(v); free(top);
   return rc;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Hashing / OSNAP.                    */
+/* B = S A, S = s stacked count-sketch matrices of ell' = ell / s rows each:   */
+/* row i of A is added to row h_j(i) of block j with sign sigma_j(i), scaled   */
+/* 1/sqrt(s) (reading C28; s = 1 is Hashing, s = 4 OSNAP).  h and sigma come   */
+/* from a counter-based generator (splitmix64 of (seed, i, j)), which the CUDA */
+/* path implements separately.                                                 */
+/* ------------------------------------------------------------------------ */
+static uint64_t orc_splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+/* B (ell x d fp64) += S A for rows row0 .. row0 + n - 1 of the stream. */
+int oracle_hash_sketch(const float* A, int64_t n, int64_t lda, int64_t d, int ell, int s, uint64_t seed,
+                       int64_t row0, double* B) {
+  if (s < 1 || ell < s || ell % s != 0) return -3;
+  const int lb = ell / s;
+  const double scale = 1.0 / sqrt((double)s);
+  for (int64_t r = 0; r < n; ++r) {
+    const uint64_t i = (uint64_t)(row0 + r);
+    const float* a = A + r * lda;
+    for (int j = 0; j < s; ++j) {
+      const uint64_t x = orc_splitmix64(seed ^ (i * (uint64_t)s + (uint64_t)j) * 0xD1B54A32D192ED03ull);
+      const int h = (int)((x >> 32) % (uint64_t)lb);
+      const double sg = (x & 1ull) ? -scale : scale;
+      double* b = B + (size_t)(j * lb + h) * d;
+      for (int64_t c = 0; c < d; ++c) b[c] += sg * (double)a[c];
+    }
+  }
+  return 0;
+}

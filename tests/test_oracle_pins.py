@@ -574,3 +574,46 @@ def test_cfd_is_fd_plus_delta_on_ell_directions(shards):
         assert abs(float(np.sum(rc.B ** 2)) - fa) <= 1e-9 * fa
         m = np.linalg.eigvalsh(A64.T @ A64 - rc.B.T @ rc.B)
         assert max(abs(m[0]), abs(m[-1])) <= Dl * (1 + 1e-9)
+
+
+# ---------------------------------------------------------------------------
+# Hashing / OSNAP (reading C28)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("s", [1, 4])
+def test_hash_sketch_is_a_signed_bucket_matrix(s):
+    """A = I_n: B = S itself.  Every column has exactly one nonzero per block, of
+    magnitude 1/sqrt(s) (PAPER.md:198: one non-zero per column, +-1; :200: s stacked)."""
+    n, ell = 200, 16
+    S = oracle.hash_sketch(np.eye(n, dtype=np.float32), ell, s=s, seed=3)
+    lb = ell // s
+    for j in range(s):
+        blk = S[j * lb:(j + 1) * lb]
+        assert np.all(np.count_nonzero(blk, axis=0) == 1)
+        assert np.allclose(np.abs(blk).sum(axis=0), 1.0 / np.sqrt(s), rtol=0, atol=1e-15)
+
+
+def test_hash_sketch_linear_and_mergeable():
+    """B(A) for one call = B(first part) + B(second part, row0 offset), exactly (fp64,
+    same summation order), and B is linear in A."""
+    A = _c1()
+    B = oracle.hash_sketch(A, 16, s=4, seed=9)
+    B2 = oracle.hash_sketch(A[:700], 16, s=4, seed=9)
+    oracle.hash_sketch(A[700:], 16, s=4, seed=9, row0=700, B=B2)
+    assert np.array_equal(B, B2)
+    C = oracle.hash_sketch(2.0 * A, 16, s=4, seed=9)
+    assert np.array_equal(C, 2.0 * B)
+
+
+def test_hash_sketch_unbiased_covariance():
+    """E[B^T B] = A^T A: over 400 seeds the mean of B^T B approaches A^T A (the
+    off-diagonal terms cancel in expectation: independent signs), within 5 standard errors."""
+    rng = np.random.default_rng(2)
+    A = rng.standard_normal((60, 5)).astype(np.float32)
+    AtA = A.astype(np.float64).T @ A.astype(np.float64)
+    acc = []
+    for seed in range(400):
+        B = oracle.hash_sketch(A, 8, s=4, seed=seed)
+        acc.append(B.T @ B)
+    acc = np.array(acc)
+    mean, se = acc.mean(0), acc.std(0) / np.sqrt(len(acc))
+    assert np.all(np.abs(mean - AtA) <= 5 * se + 1e-9)
