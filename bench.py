@@ -428,6 +428,175 @@ def run_ours(args):
     return 0
 
 
+# ---------------------------------------------------------------------------
+# Hashing / OSNAP arm: --variant osnap | hashing
+# ---------------------------------------------------------------------------
+HASH_S = {"osnap": 4, "hashing": 1}
+
+
+def hash_oracle_sample(wl, s, ell, rows=1_000_000):
+    """The oracle's hash sketch (as it stands, one thread) on the first `rows` rows."""
+    import fdgen
+    import oracle
+    cfgname = WORKLOADS[wl][0]
+    w = fdgen.config(cfgname)
+    nr = min(rows, w.n)
+    A = fdgen.host_rows(w, 0, nr)
+    t0 = time.perf_counter()
+    oracle.hash_sketch(A, ell, s=s, seed=0)
+    dt = time.perf_counter() - t0
+    return {"value": nr / dt, "unit": "rows/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {nr} rows of {wl}, fp64 oracle hash sketch, one thread, {dt:.1f} s"}
+
+
+def run_hash(args):
+    import torch
+    import torch.distributed as dist
+
+    import fdgen
+    import paper_1501_06561_b200 as fd
+    from paper_1501_06561_b200.dist import local_range
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    wl = args.workload
+    cfgname, ell, _, _ = WORKLOADS[wl]
+    s = HASH_S[args.variant]
+    w = fdgen.config(cfgname)
+    r0, r1 = local_range(w.n, rank, world)
+    nloc = r1 - r0
+    gen = fdgen.DeviceGenerator(w, device=dev)
+    A = torch.empty((nloc, w.d), dtype=torch.float32, device=dev)
+    gen.fill(A, r0)
+    B = torch.zeros((ell, w.d), dtype=torch.float64, device=dev)
+    nws = fd.lib().fd_hash_workspace_bytes(w.d, ell)
+    ws = torch.empty(nws, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        B.zero_()
+        fd.check(fd.lib().fd_hash_sketch(A.data_ptr(), nloc, A.stride(0), w.d, ell, s, 0, r0, B.data_ptr(),
+                                         ws.data_ptr(), nws, stream.cuda_stream))
+        if world > 1:
+            dist.all_reduce(B)        # the sketch is linear: the merge is a sum
+        return B
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0.record(stream)
+    kern_ms = 0.0
+    for _ in range(args.steps):
+        B.zero_()
+        k0.record(stream)
+        fd.check(fd.lib().fd_hash_sketch(A.data_ptr(), nloc, A.stride(0), w.d, ell, s, 0, r0, B.data_ptr(),
+                                         ws.data_ptr(), nws, stream.cuda_stream))
+        k1.record(stream)
+        if world > 1:
+            dist.all_reduce(B)
+        k1.synchronize()
+        kern_ms += k0.elapsed_time(k1)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    value = w.n / (ms_step / 1e3)
+    pk = peaks()
+    kms = kern_ms / args.steps
+    bytes_launch = nloc * w.d * 4.0 + 2.0 * fd.lib().fd_hash_workspace_bytes(w.d, ell) + 2.0 * ell * w.d * 8
+    roof = {"bound": "hbm", "achieved": bytes_launch / (kms / 1e3) / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "kernel": "hash_kernel+hash_reduce_kernel",
+            "algorithmic_bytes": "n d 4 (read A) + 2 x partials (write + read, fp64) + B read/write",
+            "traffic": None, "peak_source": f"hbm_gbs {pk['source']}", "ms_per_launch": kms}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    # error of the hash sketch (GPU evaluator, outside the timed region)
+    from paper_1501_06561_b200.dist import dist_cov_err
+    Bf = B.to(torch.float32)
+    ce = dist_cov_err(A, Bf, proj_k=10)
+    e2e = None
+    if not args.no_e2e:
+        chunk = 1 << 18
+        Ah = torch.empty((nloc, w.d), dtype=torch.float32, pin_memory=True)
+        Ah.copy_(A)
+        del A
+        torch.cuda.empty_cache()
+        bufs = [torch.empty((chunk, w.d), dtype=torch.float32, device=dev) for _ in range(2)]
+        copy_s = torch.cuda.Stream(dev)
+        done = [torch.cuda.Event() for _ in range(2)]
+        copied = [torch.cuda.Event() for _ in range(2)]
+
+        def e2e_step():
+            # chunk k+1 is copied (copy stream) while chunk k is hashed (compute stream)
+            B.zero_()
+            for ci, a in enumerate(range(0, nloc, chunk)):
+                b = min(nloc, a + chunk)
+                k = ci & 1
+                with torch.cuda.stream(copy_s):
+                    if ci >= 2:
+                        copy_s.wait_event(done[k])
+                    bufs[k][: b - a].copy_(Ah[a:b], non_blocking=True)
+                    copied[k].record(copy_s)
+                stream.wait_event(copied[k])
+                fd.check(fd.lib().fd_hash_sketch(bufs[k].data_ptr(), b - a, w.d, w.d, ell, s, 0, r0 + a,
+                                                 B.data_ptr(), ws.data_ptr(), nws, stream.cuda_stream))
+                done[k].record(stream)
+            if world > 1:
+                dist.all_reduce(B)
+            return B.cpu()
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ks = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
+        for _ in range(ks):
+            e2e_step()
+        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        sec = float(el.item()) / ks
+        e2e = {"value": w.n / sec, "unit": "rows/s", "h2d_bytes_per_step": int(w.n * w.d * 4),
+               "d2h_bytes_per_step": int(ell * w.d * 8 * world), "steps": ks,
+               "note": "wall clock: pinned host rows -> H2D chunks (2 streams) -> fd_hash_sketch -> D2H of B"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64 accumulation of f32 rows", "data": "synthetic (seeded fdgen, generated on device)",
+        "config": {"workload": f"{wl}: n={w.n} d={w.d} ell={ell}, {args.variant} (s={s}), seed 0",
+                   "n": w.n, "d": w.d, "ell": ell, "variant": args.variant, "s": s,
+                   "parallelism": f"rows dp{world} + all_reduce(B)",
+                   "l2": "inputs larger than L2 (A is streamed from HBM every step)"},
+        "roofline": roof, "gpu_launches": 2 * args.steps,
+        "clocks": {"sm_mhz": clk["sm_mhz"], "sm_max_mhz": clk["sm_max_mhz"], "reasons": clk["reasons"]},
+        "cov_err": ce["err"], "cov_err_lmin": ce["lmin"], "proj_err_k10": ce.get("proj_err"), "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = hash_oracle_sample(wl, s, ell)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -443,6 +612,18 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup < 3 is below the timing rules", file=sys.stderr)
+    if args.variant in HASH_S:
+        if args.impl == "reference":
+            rank, _, _ = dist_env()
+            if rank == 0:
+                res = hash_oracle_sample(args.workload, HASH_S[args.variant], WORKLOADS[args.workload][1])
+                print(json.dumps({"impl": "reference", "metric": METRIC, "value": res["value"], "unit": "rows/s",
+                                  "n_gpus": args.gpus, "steps": 1, "warmup": 0, "higher_is_better": True,
+                                  "dtype": "f64", "data": "synthetic", "cpu_baseline": res,
+                                  "e2e": {"value": res["value"], "unit": "rows/s", "h2d_bytes_per_step": 0,
+                                          "d2h_bytes_per_step": 0}}), flush=True)
+            return 0
+        return run_hash(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

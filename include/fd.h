@@ -229,6 +229,24 @@ fd_status fd_proj_err_from_gram(const double* AtA, const float* B, int32_t ell, 
 fd_status fd_proj_err(const float* A, int64_t n, int64_t ld, const float* B, int32_t ell, int64_t d, int32_t k,
                       double* proj_err, void* ws, size_t ws_bytes, void* cuda_stream);
 
+/* ---- Hashing / OSNAP -------------------------------------
+ * B = S A with S = s stacked count-sketch matrices of ell/s rows each (PAPER.md:198-201:
+ * "exactly 1 non-zero element per column ... -1 or +1", OSNAP "stacks s instances";
+ * s = 1 is Hashing, the paper uses s = 4): row i of the stream is added to row
+ * h_j(i) of block j with sign sigma_j(i), scaled 1/sqrt(s) (C28).  h and
+ * sigma come from splitmix64 of (seed, i, j) with i the row's GLOBAL stream index. */
+
+/* Workspace bytes of fd_hash_sketch at dimension d and ell. */
+size_t fd_hash_workspace_bytes(int64_t d, int32_t ell);
+
+/* B_acc [device] (ell x d fp64, row-major, caller-owned) += S A for the n rows of
+ * A [device] (fp32, ld >= d), which are rows row0 .. row0+n-1 of the stream.  B is
+ * linear in A, so successive calls (or ranks, by an all-reduce sum) add up.  Fixed
+ * summation order (deterministic).  1 <= s <= 8, s | ell, ell * 512 B <= 200 KiB.
+ * Asynchronous.  Errors: INVALID_ARG, SHAPE (ld < d), UNSUPPORTED, WORKSPACE, CUDA. */
+fd_status fd_hash_sketch(const float* A, int64_t n, int64_t ld, int64_t d, int32_t ell, int32_t s, uint64_t seed,
+                         int64_t row0, double* B_acc, void* ws, size_t ws_bytes, void* cuda_stream);
+
 /* Thread-local message for the last error on this thread ("" if none). */
 const char* fd_last_error(void);
 

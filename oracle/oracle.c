@@ -786,7 +786,7 @@ int oracle_hash_sketch(const float* A, int64_t n, int64_t lda, int64_t d, int el
     const float* a = A + r * lda;
     for (int j = 0; j < s; ++j) {
       const uint64_t x = orc_splitmix64(seed ^ (i * (uint64_t)s + (uint64_t)j) * 0xD1B54A32D192ED03ull);
-      const int h = (int)((x >> 32) % (uint64_t)lb);
+      const int h = (int)(((uint64_t)(uint32_t)(x >> 32) * (uint64_t)lb) >> 32);   /* multiply-shift into [0, lb) */
       const double sg = (x & 1ull) ? -scale : scale;
       double* b = B + (size_t)(j * lb + h) * d;
       for (int64_t c = 0; c < d; ++c) b[c] += sg * (double)a[c];

@@ -16,7 +16,7 @@ import ctypes
 
 from ._lib import FD_MAX_N, VARIANT, FdConfig, FdError, FdStats, check, lib
 
-__all__ = ["Sketcher", "cov_err", "cov_gram_partial", "cov_err_from_gram", "proj_err", "proj_err_from_gram", "FdError", "VARIANT", "FD_MAX_N",
+__all__ = ["Sketcher", "cov_err", "cov_gram_partial", "cov_err_from_gram", "proj_err", "proj_err_from_gram", "hash_sketch", "FdError", "VARIANT", "FD_MAX_N",
            "is_batched"]
 
 
@@ -223,3 +223,20 @@ def proj_err(A, B, k=10, stream=None):
     check(lib().fd_proj_err(A.data_ptr(), A.shape[0], A.stride(0), B.data_ptr(), B.shape[0], d, int(k),
                             ctypes.byref(pe), ws.data_ptr(), nb, s.cuda_stream))
     return dict(err=pe.value)
+
+
+def hash_sketch(A, ell, s=4, seed=0, row0=0, B=None, stream=None):
+    """Hashing (s = 1) / OSNAP sketch: B (ell x d cuda fp64) += S A for the
+    rows A (n x d cuda fp32) = rows row0.. of the stream.  Returns B (fp64 accumulator)."""
+    torch = _torch()
+    d = A.shape[1]
+    A = _as_rows(A, d)
+    if B is None:
+        B = torch.zeros((ell, d), dtype=torch.float64, device=A.device)
+    assert B.dtype == torch.float64 and B.is_contiguous() and tuple(B.shape) == (ell, d)
+    n = lib().fd_hash_workspace_bytes(int(d), int(ell))
+    ws = torch.empty(max(n, 1), dtype=torch.uint8, device=A.device)
+    st = stream if stream is not None else torch.cuda.current_stream(A.device)
+    check(lib().fd_hash_sketch(A.data_ptr(), A.shape[0], A.stride(0), d, int(ell), int(s), int(seed), int(row0),
+                               B.data_ptr(), ws.data_ptr(), n, st.cuda_stream))
+    return B

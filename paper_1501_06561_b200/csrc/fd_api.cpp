@@ -869,6 +869,24 @@ fd_status fd_proj_err(const float* A, int64_t n, int64_t ld, const float* B, int
   return fd_proj_err_from_gram(AtA, B, ell, d, frob, k, proj_err, nullptr, nullptr, ws, pb, cuda_stream);
 }
 
+size_t fd_hash_workspace_bytes(int64_t d, int32_t ell) {
+  if (d < 1 || ell < 1) return 0;
+  return (size_t)fdk::hash_ranges(d) * (size_t)ell * (size_t)d * sizeof(double);
+}
+
+fd_status fd_hash_sketch(const float* A, int64_t n, int64_t ld, int64_t d, int32_t ell, int32_t s, uint64_t seed,
+                         int64_t row0, double* B_acc, void* ws, size_t ws_bytes, void* cuda_stream) {
+  if (!B_acc || (n > 0 && !A) || n < 0 || d < 1 || ell < 1 || row0 < 0) return fail(FD_ERR_INVALID_ARG, "bad argument");
+  if (ld < d) return fail(FD_ERR_SHAPE, "ld < d");
+  if (!fdk::hash_supported(ell, s)) return fail(FD_ERR_UNSUPPORTED, "hash sketch: need 1 <= s <= 8, s | ell, ell <= 400");
+  if (n == 0) return FD_OK;
+  if (!ws || ws_bytes < fd_hash_workspace_bytes(d, ell)) return fail(FD_ERR_WORKSPACE, "hash workspace too small");
+  cudaError_t e = fdk::launch_hash(A, n, ld, d, ell, s, seed, row0, static_cast<double*>(ws), B_acc,
+                                   static_cast<cudaStream_t>(cuda_stream));
+  if (e != cudaSuccess) return cuda_fail(e, "hash sketch");
+  return FD_OK;
+}
+
 const char* fd_last_error(void) { return g_err.c_str(); }
 
 // debug: copy the phase trace (32 x int64, CTA 0 of the eig / trd kernels; FD_DEBUG_EIG set)

@@ -86,6 +86,11 @@ cudaError_t launch_syrk_f64(const float* A, int64_t n, int64_t ld, int64_t d, do
 cudaError_t launch_sub_btb(double* M, const double* AtA, const float* B, int ell, int64_t d, cudaStream_t s);
 cudaError_t launch_lanczos(const double* M, int64_t d, int kmax, double* Q, double* work, double* out2,
                            cudaStream_t s, int ntop = 0, double* top = nullptr);
+// Hashing / OSNAP (fd_hash.cu): B (ell x d fp64) += S A; partials: hash_ranges(d) * ell * d doubles
+int hash_ranges(int64_t d);
+bool hash_supported(int ell, int s);
+cudaError_t launch_hash(const float* A, int64_t n, int64_t ld, int64_t d, int ell, int s, uint64_t seed, int64_t row0,
+                        double* partials, double* B, cudaStream_t st);
 // proj-err parts (fd_eval.cu): G = B B^T, Jacobi -> (V, w, ord), q[t] = v_t^T AtA v_t
 cudaError_t launch_proj_parts(const float* B, int ell, int64_t d, int k, const double* AtA, double* G, double* V,
                               double* w, int* ord, int* sweeps, double* vbuf, double* q, cudaStream_t s);

@@ -582,3 +582,54 @@ def test_cfd_merge_unsupported():
     with pytest.raises(m.FdError):
         sk.merge(torch.zeros((2, 4, 16), device="cuda"))
     sk.close()
+
+
+# ---------------------------------------------------------------------------
+# Hashing / OSNAP (reading C28).  Both sides
+# accumulate in fp64 from the same fp32 rows with different association (range
+# partials vs one running sum): |dB| <= n eps64 sum_i |a_i| per column; the test
+# uses 1e-12 * max_c sum_i |A[i, c]| (>= 10x that bound at these n).
+# ---------------------------------------------------------------------------
+def _hash_tol(A):
+    return 1e-12 * float(np.abs(A.astype(np.float64)).sum(axis=0).max())
+
+
+@pytest.mark.parametrize("s,ell", [(1, 16), (4, 16), (4, 128), (2, 30)])
+def test_hash_parity_c2(s, ell):
+    A = _c2()
+    Bg = fd().hash_sketch(torch.from_numpy(A).cuda(), ell, s=s, seed=17).cpu().numpy()
+    Bo = oracle.hash_sketch(A, ell, s=s, seed=17)
+    assert np.abs(Bg - Bo).max() <= _hash_tol(A)
+
+
+def test_hash_multi_call_and_padded_rows():
+    """Calls with row0 offsets add up to the single call; ld > d rows; empty call."""
+    A = fdgen.host_rows(fdgen.config("c1"))
+    m = fd()
+    big = torch.zeros((A.shape[0], A.shape[1] + 5), dtype=torch.float32, device="cuda")
+    big[:, :A.shape[1]] = torch.from_numpy(A)
+    Ad = big[:, :A.shape[1]]
+    B = m.hash_sketch(Ad[:777], 32, s=4, seed=5)
+    m.hash_sketch(Ad[777:777], 32, s=4, seed=5, row0=777, B=B)
+    m.hash_sketch(Ad[777:], 32, s=4, seed=5, row0=777, B=B)
+    Bo = oracle.hash_sketch(A, 32, s=4, seed=5)
+    assert np.abs(B.cpu().numpy() - Bo).max() <= _hash_tol(A)
+    with pytest.raises(m.FdError):
+        m.hash_sketch(Ad, 30, s=4)          # s must divide ell
+
+
+def test_hash_fullsize_c4_sampled_columns():
+    """c4 at full size (n = 8 388 608, d = 1024), OSNAP s = 4, ell = 128, the bench's
+    launch: the oracle recomputes 16 sampled columns (the hash depends on the row index
+    only) from the same device-generated rows."""
+    m = fd()
+    w = fdgen.config("c4")
+    gen = fdgen.DeviceGenerator(w)
+    A = torch.empty((w.n, w.d), dtype=torch.float32, device="cuda")
+    gen.fill(A)
+    B = m.hash_sketch(A, 128, s=4, seed=0).cpu().numpy()
+    cols = np.random.default_rng(0).choice(w.d, 16, replace=False)
+    As = A[:, torch.from_numpy(cols).cuda()].contiguous().cpu().numpy()
+    del A
+    Bo = oracle.hash_sketch(As, 128, s=4, seed=0)
+    assert np.abs(B[:, cols] - Bo).max() <= _hash_tol(As)
