@@ -223,7 +223,7 @@ cudaError_t timed(fd_handle* h, int kind, F f) {
   return e;
 }
 
-fd_status run_reduce(fd_handle* h, const std::vector<Prob>& probs, bool comp = false) {
+fd_status run_reduce(fd_handle* h, const std::vector<Prob>& probs, bool comp = false, bool merge = false) {
   if (probs.empty()) return FD_OK;
   int nmax = 0;
   for (const Prob& p : probs) nmax = std::max(nmax, p.rows0 + p.rows1);
@@ -232,6 +232,7 @@ fd_status run_reduce(fd_handle* h, const std::vector<Prob>& probs, bool comp = f
   if (s != FD_OK) return s;
   const int n = (int)probs.size();
   Params prm = h->prm;
+  prm.merge = merge ? 1 : 0;
   if (comp) {   // Compensative FD final step: all ell directions get sigma'^2 + Delta
     prm.comp = 1;
     prm.ret = h->D.ell;
@@ -310,7 +311,7 @@ fd_status run_tree(fd_handle* h, int count, int* root, bool comp = false) {
       probs.push_back(make_prob(h, slot, node_buf(h, m.a), R, node_buf(h, m.b), R, node_buf(h, m.node),
                                 node_stats(h, m.node), node_stats(h, m.a), node_stats(h, m.b)));
     }
-    fd_status s = run_reduce(h, probs, comp && lvl == maxh);   // CFD: the root is the final step
+    fd_status s = run_reduce(h, probs, comp && lvl == maxh, true);   // CFD: the root is the final step
     if (s != FD_OK) return s;
   }
   return FD_OK;
@@ -388,7 +389,7 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
   h->stream = static_cast<cudaStream_t>(cuda_stream);
   h->device = cfg->device;
   h->prm.d = D.d; h->prm.ldb = D.ldb; h->prm.ldg = D.ldg; h->prm.ell = D.ell; h->prm.rule = D.rule; h->prm.m = D.m;
-  h->prm.ret = D.R; h->prm.tdel = D.t; h->prm.comp = 0;
+  h->prm.ret = D.R; h->prm.tdel = D.t; h->prm.comp = 0; h->prm.merge = 0;
   h->prm.f64 = 0;
   h->prm.pretrd = 0;
   h->prm.zld = D.ldg;

@@ -57,6 +57,7 @@ struct Params {
   int ret;       // rows kept by a ReduceRank: ell-1, or R of the paper-literal Fast alpha-FD
   int tdel;      // delta = lambda_tdel (1-based): ell, or t of the paper-literal Fast alpha-FD
   int comp;      // 1: Compensative FD final step, sigma_hat^2 = sigma'^2 + Delta on ret = ell rows
+  int merge;     // 1: a merge level (large eigenvalue clusters expected: eig panel variant)
   int f64;       // 1: Gram / eigen / reconstruct accumulate in fp64 (per-row chains)
   int pretrd;    // 1: the Gram scratch already holds the tridiagonal form (trd_kernel)
   int zld;       // eig_kernel fp64 scratch stride (>= every problem size of the handle)

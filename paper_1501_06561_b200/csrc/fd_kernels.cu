@@ -442,7 +442,11 @@ constexpr int kSmallCl = 8;             // clusters up to this size: warp MGS; l
 #ifndef FD_INV_ITERS
 #define FD_INV_ITERS 2
 #endif
-constexpr int kInvIters = FD_INV_ITERS;  // inverse-iteration sweeps (2: same parity as 3)
+constexpr int kInvIters = FD_INV_ITERS;
+#ifndef FD_SOLVE_BATCH
+#define FD_SOLVE_BATCH 8
+#endif
+constexpr int kSB = FD_SOLVE_BATCH;   // rows per load batch of the twisted solves  // inverse-iteration sweeps (2: same parity as 3)
 
 // fp64 reciprocal: fp32 estimate + two Newton steps (each squares the ~6e-8
 // relative error of the estimate), cheaper than the IEEE division.
@@ -588,7 +592,142 @@ __device__ __forceinline__ T coarse_pt(int t, int fam, int H, T gl, T gu) {
 
 // PRE = true: the lean variant for the tridiagonal-kernel path (p.pretrd): 256
 // threads, small shared memory, several CTAs (problems) per SM.
-template <typename T, int NM, bool GAPK, bool PRE = false>
+// Large clusters (> kSmallCl members) of the inverse iteration: panels of 8 members,
+// block Gram-Schmidt twice against the earlier members + warp MGS inside the panel (see
+// the call site).  Out of line so its registers do not perturb the solver loop's.
+template <int NM, int kNT>
+__device__
+#ifdef FD_PANEL_INLINE
+__forceinline__
+#else
+__noinline__
+#endif
+void panel_cgs(double* __restrict__ Zs, int kMaxN, double* __restrict__ pscl,
+                                       double* __restrict__ cpart, const int* __restrict__ cstart,
+                                       const int* __restrict__ clen, int ncl, int N) {
+  constexpr int kNW = kNT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int c = 0; c < ncl; ++c) {
+      const int j0 = cstart[c], nc = clen[c];
+      if (nc <= kSmallCl) continue;
+      const int rpw = (N + kNW - 1) / kNW;   // rows per warp (<= 32 for every instantiation)
+      double* cp = cpart;                    // [kNW][32][8] partial dots
+      double* hq = cpart + kNW * 256;        // [32][8] projection coefficients
+      for (int p0 = j0; p0 < j0 + nc; p0 += 8) {
+        const int pb = min(8, j0 + nc - p0);
+        __syncthreads();   // previous panel finished; pscl stable
+        for (int i = tid; i < N; i += kNT)
+          for (int m = 0; m < pb; ++m) Zs[(size_t)i * kMaxN + p0 + m] *= pscl[p0 + m];
+        __syncthreads();
+        const int kq = p0 - j0;
+        for (int pass = 0; pass < 2 && kq > 0; ++pass) {
+          for (int q0 = 0; q0 < kq; q0 += 32) {
+            const int nq = min(32, kq - q0);
+            {
+              const int ia = warp * rpw, ir = ia + lane;
+              const int q = j0 + q0 + lane;
+              for (int mh = 0; mh < 8; mh += 4) {   // half a panel at a time (register pressure)
+                double pv[4];
+#pragma unroll
+                for (int m = 0; m < 4; ++m)
+                  pv[m] = (lane < rpw && ir < N && mh + m < pb) ? Zs[(size_t)ir * kMaxN + p0 + mh + m] : 0.0;
+                double h[4] = {0.0, 0.0, 0.0, 0.0};
+                for (int r = 0; r < rpw; r += 4) {
+                  double zq[4];
+#pragma unroll
+                  for (int u = 0; u < 4; ++u) {
+                    const int i = ia + r + u;
+                    zq[u] = (r + u < rpw && i < N && lane < nq) ? Zs[(size_t)i * kMaxN + q] : 0.0;
+                  }
+#pragma unroll
+                  for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int m = 0; m < 4; ++m)
+                      h[m] = fma(zq[u], __shfl_sync(0xffffffffu, pv[m], (r + u) & 31), h[m]);
+                }
+#pragma unroll
+                for (int m = 0; m < 4; ++m) cp[(warp * 32 + lane) * 8 + mh + m] = h[m];
+              }
+            }
+            __syncthreads();
+            if (tid < 256) {
+              double sum = 0.0;
+              for (int w = 0; w < kNW; ++w) sum += cp[w * 256 + tid];
+              hq[tid] = sum;
+            }
+            __syncthreads();
+            for (int i = tid; i < N; i += kNT) {
+              double* zi = Zs + (size_t)i * kMaxN;
+              double z[8];
+#pragma unroll
+              for (int m = 0; m < 8; ++m) z[m] = (m < pb) ? zi[p0 + m] : 0.0;
+              int l = 0;
+              for (; l + 4 <= nq; l += 4) {
+                double zl[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) zl[u] = zi[j0 + q0 + l + u];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                  for (int m = 0; m < 8; ++m) z[m] = fma(-hq[(l + u) * 8 + m], zl[u], z[m]);
+              }
+              for (; l < nq; ++l) {
+                const double zl = zi[j0 + q0 + l];
+#pragma unroll
+                for (int m = 0; m < 8; ++m) z[m] = fma(-hq[l * 8 + m], zl, z[m]);
+              }
+#pragma unroll
+              for (int m = 0; m < 8; ++m)
+                if (m < pb) zi[p0 + m] = z[m];
+            }
+            __syncthreads();
+          }
+        }
+        if (warp == 0) {   // the panel itself: MGS twice, normalise (registers)
+          for (int k = p0; k < p0 + pb; ++k) {
+            double* zk = Zs + k;
+            double zr[NM / 32];
+#pragma unroll
+            for (int t = 0; t < NM / 32; ++t) {
+              const int i = 32 * t + lane;
+              zr[t] = (i < N) ? zk[(size_t)i * kMaxN] : 0.0;
+            }
+            for (int pass = 0; pass < 2; ++pass)
+              for (int q = p0; q < k; ++q) {
+                const double* zq = Zs + q;
+                double zqr[NM / 32];
+                double hh = 0.0;
+#pragma unroll
+                for (int t = 0; t < NM / 32; ++t) {
+                  const int i = 32 * t + lane;
+                  zqr[t] = (i < N) ? zq[(size_t)i * kMaxN] : 0.0;
+                  hh = fma(zqr[t], zr[t], hh);
+                }
+                hh = warp_sum_d(hh);
+#pragma unroll
+                for (int t = 0; t < NM / 32; ++t) zr[t] = fma(-hh, zqr[t], zr[t]);
+              }
+            double n2 = 0.0;
+#pragma unroll
+            for (int t = 0; t < NM / 32; ++t) n2 = fma(zr[t], zr[t], n2);
+            n2 = warp_sum_d(n2);
+            const double inv = (n2 > 0.0) ? 1.0 / sqrt(n2) : 0.0;
+#pragma unroll
+            for (int t = 0; t < NM / 32; ++t) {
+              const int i = 32 * t + lane;
+              if (i < N) zk[(size_t)i * kMaxN] = zr[t] * inv;
+            }
+            __syncwarp();
+          }
+        }
+        __syncthreads();
+        if (tid < pb) pscl[p0 + tid] = 1.0;
+      }
+    }
+    
+}
+
+template <typename T, int NM, bool GAPK, bool PRE = false, bool BIG = false>
 __global__ void __launch_bounds__(PRE ? 256 : kEigThreads, PRE ? kEigPreCtasPerSM : 1)
 eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restrict__ scratch) {
   using C = EigCfg<T, NM, GAPK, PRE>;
@@ -625,7 +764,6 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
   constexpr size_t kOffD = C::kT * sizeof(T) + (4 * NM + kNT) * sizeof(int);
   double* pscl = reinterpret_cast<double*>(smraw + kOffD + 8 - (kOffD & 7));  // per-vector scale (fp64)
   double* cpart = PRE ? pscl + NM : reinterpret_cast<double*>(ppart);  // [kNW][kCpStride] block-CGS dots
-  double* chq = cpart + kNW * kCpStride; // [NM] projection coefficients
   __shared__ int s_ncl, s_jx, s_nrr;
   __shared__ T s_gl, s_gu, s_a1, s_a2;
 
@@ -1042,14 +1180,14 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
           const int cnt = side ? (N - 1 - m) : m;     // rows of this side (<= m)
           const int dir = side ? -1 : 1, ist = side ? N - 1 : 0;
           double rd = 0.0, w = 0.0, eprev = 0.0;
-          for (int k0 = 0; k0 < m; k0 += 8) {
-            double zb[8];
+          for (int k0 = 0; k0 < m; k0 += kSB) {
+            double zb[kSB];
             if (it > 0) {
 #pragma unroll
-              for (int q = 0; q < 8; ++q) zb[q] = (k0 + q < cnt) ? z[(size_t)(ist + dir * (k0 + q)) * kMaxN] : 0.0;
+              for (int q = 0; q < kSB; ++q) zb[q] = (k0 + q < cnt) ? z[(size_t)(ist + dir * (k0 + q)) * kMaxN] : 0.0;
             }
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
+            for (int q = 0; q < kSB; ++q) {
               const int k = k0 + q;
               if (k < cnt) {
                 const int i = ist + dir * k;
@@ -1071,7 +1209,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
               }
             }
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
+            for (int q = 0; q < kSB; ++q)
               if (k0 + q < cnt) z[(size_t)(ist + dir * (k0 + q)) * kMaxN] = zb[q];
           }
           double tS = 0.0, wS = 0.0;   // this side's term of the twist row
@@ -1096,17 +1234,17 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
           // bottom i = m+1..N-1 (u_{i-1} = lf[i-1])
           double next = zm;
           const int bst = side ? m + 1 : m - 1, bdir = side ? 1 : -1;
-          for (int k0 = 0; k0 < m; k0 += 8) {
-            double zb[8], lb[8];
+          for (int k0 = 0; k0 < m; k0 += kSB) {
+            double zb[kSB], lb[kSB];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
+            for (int q = 0; q < kSB; ++q) {
               const int i = bst + bdir * (k0 + q);
               const bool ok = k0 + q < cnt;
               zb[q] = ok ? z[(size_t)i * kMaxN] : 0.0;
               lb[q] = ok ? lf[(size_t)(i - side) * kMaxN] : 0.0;
             }
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
+            for (int q = 0; q < kSB; ++q) {
               if (k0 + q < cnt) {
                 next = zb[q] - lb[q] * next;
                 zb[q] = next;
@@ -1114,7 +1252,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
               }
             }
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
+            for (int q = 0; q < kSB; ++q)
               if (k0 + q < cnt) z[(size_t)(bst + bdir * (k0 + q)) * kMaxN] = zb[q];
           }
           nr += __shfl_xor_sync(pmask, nr, 1);
@@ -1166,6 +1304,19 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
           }
         }
         if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[17] += t_ - t_iv; t_iv = t_; }
+        // larger clusters (wide-spread Grams put many small eigenvalues within ctol,
+        // e.g. at merge levels): the whole CTA, one cluster at a time, in panels of 8
+        // members.  Per panel: two passes of block Gram-Schmidt against the cluster's
+        // earlier (orthonormal) members in chunks of 32 -- dots: warp w takes rows
+        // w*rpw.., lane = earlier member (contiguous in the element-major scratch), the
+        // panel's values of a row broadcast by shuffle from the lane holding that row;
+        // update: a thread per row -- then one warp orthonormalises the panel itself
+        // (modified Gram-Schmidt twice, registers).
+        if constexpr (BIG) {   // merge launches: panels of 8 (block CGS2 + warp MGS)
+          panel_cgs<NM, kNT>(Zs, kMaxN, pscl, cpart, cstart, clen, ncl, N);
+          __syncthreads();
+        } else {
+          double* chq = cpart + kNW * kCpStride;   // [NM] projection coefficients
         // larger clusters (wide-spread Grams put many small eigenvalues within ctol,
         // e.g. at merge levels): the whole CTA, one cluster at a time, classical
         // Gram-Schmidt twice per member.  Dots: warp w sweeps its rows, lane = earlier
@@ -1239,6 +1390,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
           }
         }
         __syncthreads();
+        }
         if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[18] += t_ - t_iv; t_iv = t_; }
       }
       for (int j = tid; j < JX; j += blockDim.x)
@@ -1428,25 +1580,32 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
   }
 }
 
-template <typename T, int NM, bool GAPK, bool PRE = false>
+template <typename T, int NM, bool GAPK, bool PRE = false, bool BIG = false>
 static cudaError_t launch_eig_t(const Prob* dev_probs, int count, const Params& p, double* scratch, cudaStream_t s) {
   using C = EigCfg<T, NM, GAPK, PRE>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(eig_kernel<T, NM, GAPK, PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kBytes);
+    cudaError_t e = cudaFuncSetAttribute(eig_kernel<T, NM, GAPK, PRE, BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)C::kBytes);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int slots = kNumSMs * (PRE ? kEigPreCtasPerSM : 1);
   const int grid = count < slots ? count : slots;
-  eig_kernel<T, NM, GAPK, PRE><<<grid, PRE ? 256 : kEigThreads, C::kBytes, s>>>(dev_probs, count, p, scratch);
+  eig_kernel<T, NM, GAPK, PRE, BIG><<<grid, PRE ? 256 : kEigThreads, C::kBytes, s>>>(dev_probs, count, p, scratch);
   return cudaGetLastError();
 }
 
 cudaError_t launch_eig(const Prob* dev_probs, int count, const Params& p, double* scratch, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
   if (p.f64) return launch_eig_t<double, kMaxN64, false>(dev_probs, count, p, scratch, s);
-  if (p.pretrd) return launch_eig_t<float, kMaxNS, false, true>(dev_probs, count, p, scratch, s);
+  if (p.pretrd) {
+    // merge levels (p.merge) carry the large eigenvalue clusters: the panel variant;
+    // stream rounds keep the member-wise variant (its register allocation is the
+    // solver loop's)
+    if (p.merge) return launch_eig_t<float, kMaxNS, false, true, true>(dev_probs, count, p, scratch, s);
+    return launch_eig_t<float, kMaxNS, false, true>(dev_probs, count, p, scratch, s);
+  }
   if (p.zld <= kMaxNS) return launch_eig_t<float, kMaxNS, false>(dev_probs, count, p, scratch, s);
   return launch_eig_t<float, kMaxN, true>(dev_probs, count, p, scratch, s);
 }
