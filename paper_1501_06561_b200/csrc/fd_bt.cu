@@ -80,9 +80,21 @@ __global__ void __launch_bounds__(kBtThreads, 1) bt_kernel(const Prob* __restric
     const float* wg = taug + N;
     float* Wt = static_cast<float*>(P.Wt);
     // Z [r][j] (ld 128) -> Zs
-    for (int x = tid; x < N * 32; x += kBtThreads) {
-      const int r = x >> 5, j4 = 4 * (x & 31);
-      *reinterpret_cast<float4*>(&Zs[r * kZld + j4]) = *reinterpret_cast<const float4*>(Wt + (int64_t)r * 128 + j4);
+    {  // 4 independent 16-byte loads in flight per thread
+      const int j4 = 4 * (tid & 31);
+      for (int r0 = tid >> 5; r0 < N; r0 += 4 * (kBtThreads / 32)) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int r = r0 + u * (kBtThreads / 32);
+          v[u] = (r < N) ? *reinterpret_cast<const float4*>(Wt + (int64_t)r * 128 + j4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int r = r0 + u * (kBtThreads / 32);
+          if (r < N) *reinterpret_cast<float4*>(&Zs[r * kZld + j4]) = v[u];
+        }
+      }
     }
     const int nref = N - 2;                        // reflectors 0..N-3
     const int nblk = nref > 0 ? (nref + kNbBt - 1) / kNbBt : 0;
