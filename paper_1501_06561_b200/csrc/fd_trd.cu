@@ -148,7 +148,7 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
   __shared__ __align__(16) float s_x[NM];      // x~_s: column s of A^(s-1), rows >= s+1 (else 0)
   __shared__ __align__(16) float s_nxt[NM];    // look-ahead: column s+1 of A^(s-1)
   __shared__ __align__(16) float s_ctb[NB][NB][32];  // SYMV contributions [block][slot][row]
-  __shared__ float s_sig[NB];                  // per-block partial sums of squares (rows >= s+2)
+  __shared__ __align__(16) float s_sq[NM];     // squares of the column entries that enter sigma
   __shared__ __align__(16) float s_xax[(W + 3) / 4 * 4];  // per-warp partials of x^T A x (zero-padded)
   __shared__ float s_d[NM], s_e[NM], s_tau[NM];
   __shared__ float s_corner, s_dlast;          // A[N-1][N-1] (look-ahead / updated)
@@ -208,10 +208,7 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
       const float c = (r < N) ? G[(int64_t)r * p.ldg] : 0.f;
       s_x[r] = (r >= 1) ? c : 0.f;
       if (r == 0) s_d[0] = c;
-      float sq = (r >= 2 && r < N) ? c * c : 0.f;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-      if (lane == 0) s_sig[warp] = sq;
+      s_sq[r] = (r >= 2 && r < N) ? c * c : 0.f;
       s_v[r] = 0.f;
       s_w[r] = 0.f;
       if (r == N - 1) s_dlast = G[(int64_t)r * p.ldg + r];
@@ -235,8 +232,9 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
 
     // Step s: reflector H_s of column s.  Invariant at the top of phase A(s): the
     // tiles hold A^(s-2) with the rank-2 update of step s-1 pending (s_v, s_w);
-    // s_x = x~_s = column s of A^(s-1) on rows >= s+1 (else 0); s_sig = its
-    // per-block partial sums of squares over rows >= s+2.  The Householder x_s
+    // s_x = x~_s = column s of A^(s-1) on rows >= s+1 (else 0); s_sq = the squares of its
+    // entries on rows >= s+2 (sigma of the reflector, reduced by the row warps in phase A,
+    // off the critical path: the SYMV does not need the reflector).  The Householder x_s
     // differs from x~_s only in row s+1 (alpha - beta instead of alpha): the SYMV
     // runs on x~_s and phase B adds delta * A[:, s+1] (the look-ahead column).
     for (int s = 0; s <= N - 3; ++s) {
@@ -250,10 +248,12 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
           if (ov[0] && 32 * oJ[0] + 31 > s) tile_update<false>(a0, 32 * oI[0] + 8 * rg, 32 * oJ[0] + 4 * cg, s_v, s_w);
           if (ov[1] && 32 * oJ[1] + 31 > s) tile_update<false>(a1, 32 * oI[1] + 8 * rg, 32 * oJ[1] + 4 * cg, s_v, s_w);
         }
-        {  // reflector (every warp, identical arithmetic)
-          float x = ((lane & 7) < NB) ? s_sig[lane & 7] : 0.f;
+        if (warp < NB) {  // reflector (the row warps of phase B, identical arithmetic)
+          float x = 0.f;
 #pragma unroll
-          for (int o = 4; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+          for (int t = 0; t < NB; ++t) x += s_sq[32 * t + lane];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
           const float sig = x;
           al = s_x[s + 1];
           float beta;
@@ -362,10 +362,7 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
         if (r >= s + 2 && r < N) Vout[pk_off_t(s, N) - s + r] = vr;   // Householder vector s
         if (r == s) { s_e[s] = beta_s; s_tau[s] = tau_s; }
         if (r == s + 1) s_d[s + 1] = col;
-        float sq = (r >= s + 3 && r < N) ? col * col : 0.f;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-        if (lane == 0) s_sig[warp] = sq;
+        s_sq[r] = (r >= s + 3 && r < N) ? col * col : 0.f;
         if (last && r == N - 1) s_dlast = s_corner - 2.f * vr * wr;
       }
       __syncthreads();
