@@ -406,9 +406,109 @@ __global__ void __launch_bounds__(256, 2) recon_pipe_kernel(const Prob* __restri
   }
 }
 
+// Default reconstruct: CTA tile 128 (j) x 256 (n), thread tile 16 x 8 (rows ty + 8 i,
+// columns 4 lane + 128 h), 256 threads / 255 registers, one CTA per SM; the same
+// 4-stage cp.async pipeline (recon_pipe_kernel, 8 x 8 tiles, is FD_RECON1=1).
+constexpr int kRc2BLd = 256;
+constexpr int kRc2StageFloats = 128 * kRcALd + kRcBK * kRc2BLd;
+
+__global__ void __launch_bounds__(256, 1) recon_pipe2_kernel(const Prob* __restrict__ probs, Params p) {
+  const Prob P = probs[blockIdx.z];
+  const int N = P.rows0 + P.rows1;
+  const int n0 = blockIdx.x * 256, j0 = blockIdx.y * 128;
+  const int jrows = p.ret;
+  if (j0 >= p.ell) return;
+  extern __shared__ __align__(16) float rsm[];
+  const float* Wt = static_cast<const float*>(P.Wt);
+  const int tid = threadIdx.x, lane = tid & 31, ty = tid >> 5;
+  const int nk = (N + kRcBK - 1) / kRcBK;
+  auto issue = [&](int kt) {
+    float* As = rsm + (kt % kRcStages) * kRc2StageFloats;
+    float* Bs = As + 128 * kRcALd;
+    const int k0 = kt * kRcBK;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int m = (tid >> 2) + 64 * h, kq = 4 * (tid & 3), k = k0 + kq, j = j0 + m;
+      const int bytes = (j < jrows && k < N) ? 4 * min(4, N - k) : 0;
+      const float* src = bytes ? Wt + (int64_t)j * p.ldg + k : Wt;
+      cp_async16(As + m * kRcALd + kq, src, bytes);
+    }
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int kr = (tid >> 6) + 4 * h, nq = 4 * (tid & 63), k = k0 + kr, n = n0 + nq;
+      const bool ok = k < N && n < p.ldb;
+      const float* src = ok ? prob_row(P, k, p.ldb) + n : Wt;
+      cp_async16(Bs + kr * kRc2BLd + nq, src, ok ? 16 : 0);
+    }
+  };
+  float acc[16][8];
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+#pragma unroll
+  for (int st = 0; st < kRcStages - 1; ++st) {
+    if (st < nk) issue(st);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<kRcStages - 2>();
+    __syncthreads();
+    if (kt + kRcStages - 1 < nk) issue(kt + kRcStages - 1);
+    cp_async_commit();
+    const float* As = rsm + (kt % kRcStages) * kRc2StageFloats;
+    const float* Bs = As + 128 * kRcALd;
+#pragma unroll
+    for (int kk = 0; kk < kRcBK; kk += 2) {
+      float2 a[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) a[i] = *reinterpret_cast<const float2*>(&As[(ty + 8 * i) * kRcALd + kk]);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const float4 b0 = *reinterpret_cast<const float4*>(&Bs[(kk + u) * kRc2BLd + 4 * lane]);
+        const float4 b1 = *reinterpret_cast<const float4*>(&Bs[(kk + u) * kRc2BLd + 128 + 4 * lane]);
+        const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float av = u ? a[i].y : a[i].x;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av, bb[j], acc[i][j]);
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int j = j0 + ty + 8 * i;
+    if (j >= p.ell) continue;
+    float* dst = P.dst + (int64_t)j * p.ldb + n0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = 128 * h + 4 * lane;
+      if (n0 + c >= p.ldb) continue;
+      const float4 o = (j < jrows) ? make_float4(acc[i][4 * h], acc[i][4 * h + 1], acc[i][4 * h + 2], acc[i][4 * h + 3])
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(dst + c) = o;
+    }
+  }
+}
+
 cudaError_t launch_recon(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
   (void)nmax;
+  if (!p.f64 && (p.ldg % 4) == 0 && (p.ldb % 4) == 0 && !getenv("FD_RECON1") && !getenv("FD_RECON128")) {
+    constexpr int dyn = kRcStages * kRc2StageFloats * (int)sizeof(float);
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaError_t e = cudaFuncSetAttribute(recon_pipe2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+      if (e != cudaSuccess) return e;
+      attr2 = true;
+    }
+    dim3 grid((unsigned)((p.ldb + 255) / 256), (unsigned)((p.ell + 127) / 128), count);
+    recon_pipe2_kernel<<<grid, 256, dyn, s>>>(dev_probs, p);
+    return cudaGetLastError();
+  }
   if (!p.f64 && (p.ldg % 4) == 0 && (p.ldb % 4) == 0 && !getenv("FD_RECON128")) {
     constexpr int dyn = kRcStages * kRcStageFloats * (int)sizeof(float);
     static bool attr = false;
