@@ -633,3 +633,42 @@ def test_hash_fullsize_c4_sampled_columns():
     del A
     Bo = oracle.hash_sketch(As, 128, s=4, seed=0)
     assert np.abs(B[:, cols] - Bo).max() <= _hash_tol(As)
+
+
+@pytest.mark.parametrize("variant,P,apps", [("cfd", 3, [1000, 40, 1, 2959]), ("fast_alpha_fd_paper", 5, [2500, 1500]),
+                                            ("ssd", 2, [777, 3223])])
+def test_host_input_append_new_variants(variant, P, apps):
+    """The host-staged append plans its rounds ahead of the device (copy/compute overlap):
+    for CFD's lazy ReduceRank (a full buffer is reduced when the next call brings rows),
+    the paper-literal Fast alpha-FD (R = max(ell-m, t-1) rows kept) and SSD it must
+    produce the same DAG as device input -- identical sketches and statistics -- and
+    match the oracle."""
+    m = fd()
+    A = _c2()[:4000]
+    outs = []
+    for host in (False, True):
+        sk = m.Sketcher(A.shape[1], 40, variant, alpha=0.2, n_shards=P)
+        src = torch.from_numpy(A).pin_memory() if host else torch.from_numpy(A).cuda()
+        o = 0
+        for a in apps:
+            sk.append(src[o:o + a])
+            o += a
+        B, st = sk.sketch()
+        outs.append((B.cpu().numpy(), st))
+        sk.close()
+    assert np.array_equal(outs[0][0], outs[1][0]), variant
+    assert outs[0][1] == outs[1][1], variant
+    r = oracle.sketch(A, 40, variant, alpha=0.2, n_shards=P, appends=apps)
+    Bg = outs[0][0].astype(np.float64)
+    assert spec_norm(Bg.T @ Bg - r.B.T @ r.B) <= SKETCH_TOL * r.frob_sq
+    assert outs[0][1]["n_shrinks"] == r.n_shrinks
+
+
+def test_proj_err_rank_deficient_A_is_an_error():
+    """||A - A_k||_F = 0 (rank A <= k): proj-err is undefined -> FdError (ZERO_NORM)."""
+    m = fd()
+    rng = np.random.default_rng(1)
+    A = (rng.standard_normal((200, 3)) @ rng.standard_normal((3, 24))).astype(np.float32)
+    B = rng.standard_normal((6, 24)).astype(np.float32)
+    with pytest.raises(m.FdError):
+        m.proj_err(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), k=5)
