@@ -65,12 +65,16 @@ def build_libfd(force=False):
     cu = [s for s in srcs if s.endswith((".cu", ".cpp"))]
     if not cu:
         return None
-    if force or _stale(out, srcs):
-        extra = os.environ.get("FD_NVCC_EXTRA", "").split()   # e.g. -DFD_INV_ITERS=2 (A/B builds)
+    extra = os.environ.get("FD_NVCC_EXTRA", "").split()   # e.g. -DFD_INV_ITERS=2 (A/B builds)
+    stamp = out + ".flags"
+    prev = open(stamp).read() if os.path.exists(stamp) else ""
+    if force or _stale(out, srcs) or prev != " ".join(extra):
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
               "-Xptxas", "-v" if os.environ.get("FD_PTXAS_V") else "-O3",
               "-I", os.path.join(ROOT, "include"), "-I", os.path.join(pkg, "csrc"), *extra,
               "-o", out, *cu])
+        with open(stamp, "w") as f:
+            f.write(" ".join(extra))
     return out
 
 

@@ -537,7 +537,10 @@ cudaError_t launch_recon(const Prob* dev_probs, int count, int nmax, const Param
 // problems), precision T, max size NM.
 // ============================================================================
 constexpr int kNW = kEigThreads / 32;  // 16 warps
-constexpr int kEigPreCtasPerSM = 4;     // resident CTAs of the lean (tridiagonal-input) variant
+#ifndef FD_EIG_CTAS
+#define FD_EIG_CTAS 4
+#endif
+constexpr int kEigPreCtasPerSM = FD_EIG_CTAS;     // resident CTAs of the lean (tridiagonal-input) variant
 constexpr int kSmallCl = 8;             // clusters up to this size: warp MGS; larger: block CGS2
 #ifndef FD_INV_ITERS
 #define FD_INV_ITERS 2
