@@ -538,7 +538,7 @@ cudaError_t launch_recon(const Prob* dev_probs, int count, int nmax, const Param
 // ============================================================================
 constexpr int kNW = kEigThreads / 32;  // 16 warps
 #ifndef FD_EIG_CTAS
-#define FD_EIG_CTAS 4
+#define FD_EIG_CTAS 3
 #endif
 constexpr int kEigPreCtasPerSM = FD_EIG_CTAS;     // resident CTAs of the lean (tridiagonal-input) variant
 constexpr int kSmallCl = 8;             // clusters up to this size: warp MGS; larger: block CGS2
@@ -547,7 +547,7 @@ constexpr int kSmallCl = 8;             // clusters up to this size: warp MGS; l
 #endif
 constexpr int kInvIters = FD_INV_ITERS;
 #ifndef FD_SOLVE_BATCH
-#define FD_SOLVE_BATCH 8
+#define FD_SOLVE_BATCH 4
 #endif
 constexpr int kSB = FD_SOLVE_BATCH;   // rows per load batch of the twisted solves  // inverse-iteration sweeps (2: same parity as 3)
 
