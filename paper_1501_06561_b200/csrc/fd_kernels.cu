@@ -409,8 +409,15 @@ __global__ void __launch_bounds__(256, 2) recon_pipe_kernel(const Prob* __restri
 // Default reconstruct: CTA tile 128 (j) x 256 (n), thread tile 16 x 8 (rows ty + 8 i,
 // columns 4 lane + 128 h), 256 threads / 255 registers, one CTA per SM; the same
 // 4-stage cp.async pipeline (recon_pipe_kernel, 8 x 8 tiles, is FD_RECON1=1).
+#ifndef FD_RC2_BK
+#define FD_RC2_BK 32
+#endif
+#ifndef FD_RC2_STAGES
+#define FD_RC2_STAGES 4
+#endif
+constexpr int kRc2BK = FD_RC2_BK, kRc2Stages = FD_RC2_STAGES, kRc2ALd = kRc2BK + 4;
 constexpr int kRc2BLd = 256;
-constexpr int kRc2StageFloats = 128 * kRcALd + kRcBK * kRc2BLd;
+constexpr int kRc2StageFloats = 128 * kRc2ALd + kRc2BK * kRc2BLd;
 
 __global__ void __launch_bounds__(256, 1) recon_pipe2_kernel(const Prob* __restrict__ probs, Params p) {
   const Prob P = probs[blockIdx.z];
@@ -421,20 +428,21 @@ __global__ void __launch_bounds__(256, 1) recon_pipe2_kernel(const Prob* __restr
   extern __shared__ __align__(16) float rsm[];
   const float* Wt = static_cast<const float*>(P.Wt);
   const int tid = threadIdx.x, lane = tid & 31, ty = tid >> 5;
-  const int nk = (N + kRcBK - 1) / kRcBK;
+  const int nk = (N + kRc2BK - 1) / kRc2BK;
   auto issue = [&](int kt) {
-    float* As = rsm + (kt % kRcStages) * kRc2StageFloats;
-    float* Bs = As + 128 * kRcALd;
-    const int k0 = kt * kRcBK;
+    float* As = rsm + (kt % kRc2Stages) * kRc2StageFloats;
+    float* Bs = As + 128 * kRc2ALd;
+    const int k0 = kt * kRc2BK;
+    constexpr int kQ = kRc2BK / 4;            // 16-byte chunks per A row
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int m = (tid >> 2) + 64 * h, kq = 4 * (tid & 3), k = k0 + kq, j = j0 + m;
+    for (int h = 0; h < 128 * kQ / 256; ++h) {
+      const int e = tid + 256 * h, m = e / kQ, kq = 4 * (e % kQ), k = k0 + kq, j = j0 + m;
       const int bytes = (j < jrows && k < N) ? 4 * min(4, N - k) : 0;
       const float* src = bytes ? Wt + (int64_t)j * p.ldg + k : Wt;
-      cp_async16(As + m * kRcALd + kq, src, bytes);
+      cp_async16(As + m * kRc2ALd + kq, src, bytes);
     }
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
+    for (int h = 0; h < kRc2BK / 4; ++h) {
       const int kr = (tid >> 6) + 4 * h, nq = 4 * (tid & 63), k = k0 + kr, n = n0 + nq;
       const bool ok = k < N && n < p.ldb;
       const float* src = ok ? prob_row(P, k, p.ldb) + n : Wt;
@@ -447,22 +455,22 @@ __global__ void __launch_bounds__(256, 1) recon_pipe2_kernel(const Prob* __restr
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
 #pragma unroll
-  for (int st = 0; st < kRcStages - 1; ++st) {
+  for (int st = 0; st < kRc2Stages - 1; ++st) {
     if (st < nk) issue(st);
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
-    cp_async_wait<kRcStages - 2>();
+    cp_async_wait<kRc2Stages - 2>();
     __syncthreads();
-    if (kt + kRcStages - 1 < nk) issue(kt + kRcStages - 1);
+    if (kt + kRc2Stages - 1 < nk) issue(kt + kRc2Stages - 1);
     cp_async_commit();
-    const float* As = rsm + (kt % kRcStages) * kRc2StageFloats;
-    const float* Bs = As + 128 * kRcALd;
+    const float* As = rsm + (kt % kRc2Stages) * kRc2StageFloats;
+    const float* Bs = As + 128 * kRc2ALd;
 #pragma unroll
-    for (int kk = 0; kk < kRcBK; kk += 2) {
+    for (int kk = 0; kk < kRc2BK; kk += 2) {
       float2 a[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) a[i] = *reinterpret_cast<const float2*>(&As[(ty + 8 * i) * kRcALd + kk]);
+      for (int i = 0; i < 16; ++i) a[i] = *reinterpret_cast<const float2*>(&As[(ty + 8 * i) * kRc2ALd + kk]);
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const float4 b0 = *reinterpret_cast<const float4*>(&Bs[(kk + u) * kRc2BLd + 4 * lane]);
@@ -498,7 +506,7 @@ cudaError_t launch_recon(const Prob* dev_probs, int count, int nmax, const Param
   if (count <= 0) return cudaSuccess;
   (void)nmax;
   if (!p.f64 && (p.ldg % 4) == 0 && (p.ldb % 4) == 0 && !getenv("FD_RECON1") && !getenv("FD_RECON128")) {
-    constexpr int dyn = kRcStages * kRc2StageFloats * (int)sizeof(float);
+    constexpr int dyn = kRc2Stages * kRc2StageFloats * (int)sizeof(float);
     static bool attr2 = false;
     if (!attr2) {
       cudaError_t e = cudaFuncSetAttribute(recon_pipe2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
