@@ -20,7 +20,14 @@ namespace fdk {
 
 namespace {
 
-constexpr int kHashCols = 64;
+#ifndef FD_HASH_COLS
+#define FD_HASH_COLS 64
+#endif
+#ifndef FD_HASH_CTAS
+#define FD_HASH_CTAS 3
+#endif
+constexpr int kHashCols = FD_HASH_COLS;   // columns per CTA (a multiple of 32)
+constexpr int kHashCtas = FD_HASH_CTAS;   // CTAs per SM the row ranges are sized for
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   x += 0x9E3779B97F4A7C15ull;
@@ -76,13 +83,13 @@ __global__ void __launch_bounds__(512) hash_kernel(const float* __restrict__ A, 
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         const int cd = __shfl_sync(0xffffffffu, code, base + q);
-        my[(cd >> 1) << 6] += (cd & 1) ? -(double)cur[q] : (double)cur[q];
+        my[(cd >> 1) * kHashCols] += (cd & 1) ? -(double)cur[q] : (double)cur[q];
       }
     } else {
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         const int cd = __shfl_sync(0xffffffffu, code, base + q);
-        if (k + q < nrows) my[(cd >> 1) << 6] += (cd & 1) ? -(double)cur[q] : (double)cur[q];
+        if (k + q < nrows) my[(cd >> 1) * kHashCols] += (cd & 1) ? -(double)cur[q] : (double)cur[q];
       }
     }
 #pragma unroll
@@ -111,7 +118,7 @@ __global__ void hash_reduce_kernel(const double* __restrict__ partials, int R, i
 // row ranges per column slice: one wave of 3 CTAs per SM (64 KiB of fp64 buckets each at ell = 128)
 int hash_ranges(int64_t d) {
   const int nslices = (int)((d + kHashCols - 1) / kHashCols);
-  return std::max(1, (3 * kNumSMs) / nslices);
+  return std::max(1, (kHashCtas * kNumSMs) / nslices);
 }
 
 bool hash_supported(int ell, int s) {
