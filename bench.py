@@ -257,7 +257,7 @@ def run_ours(args):
     if P % world:
         raise SystemExit(f"P_total={P} not divisible by world={world}")
     w = fdgen.config(cfgname)
-    r0, r1 = local_range(w.n, rank, world)
+    r0, r1 = local_range(w.n, rank, world, P)
     nloc = r1 - r0
     gen = fdgen.DeviceGenerator(w, device=dev)
     A = torch.empty((nloc, w.d), dtype=torch.float32, device=dev)

@@ -59,20 +59,35 @@ def build_oracle(force=False):
 
 
 def build_libfd(force=False):
+    """Each translation unit is compiled to an object in parallel (build/libfd/), then
+    linked; a unit is recompiled when it, any header or the extra flags changed."""
+    import concurrent.futures as cf
     pkg = os.path.join(ROOT, "paper_1501_06561_b200")
     out = os.path.join(pkg, "libfd.so")
     srcs = _glob("paper_1501_06561_b200/csrc", (".cu", ".cuh", ".cpp", ".h")) + _glob("include", (".h",))
     cu = [s for s in srcs if s.endswith((".cu", ".cpp"))]
+    hdr = [s for s in srcs if not s.endswith((".cu", ".cpp"))]
     if not cu:
         return None
     extra = os.environ.get("FD_NVCC_EXTRA", "").split()   # e.g. -DFD_INV_ITERS=2 (A/B builds)
     stamp = out + ".flags"
     prev = open(stamp).read() if os.path.exists(stamp) else ""
-    if force or _stale(out, srcs) or prev != " ".join(extra):
-        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+    flags_changed = prev != " ".join(extra)
+    objdir = os.path.join(ROOT, "build", "libfd")
+    os.makedirs(objdir, exist_ok=True)
+    common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-Xptxas", "-v" if os.environ.get("FD_PTXAS_V") else "-O3",
-              "-I", os.path.join(ROOT, "include"), "-I", os.path.join(pkg, "csrc"), *extra,
-              "-o", out, *cu])
+              "-I", os.path.join(ROOT, "include"), "-I", os.path.join(pkg, "csrc"), *extra]
+    objs, todo = [], []
+    for src in cu:
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        objs.append(obj)
+        if force or flags_changed or _stale(obj, [src] + hdr):
+            todo.append((src, obj))
+    with cf.ThreadPoolExecutor(max(1, min(len(todo), os.cpu_count() or 1))) as ex:
+        list(ex.map(lambda so: _run(common + ["-c", "-o", so[1], so[0]]), todo))
+    if todo or _stale(out, objs):
+        _run([NVCC, *ARCH, "-shared", "-o", out, *objs])
         with open(stamp, "w") as f:
             f.write(" ".join(extra))
     return out

@@ -195,6 +195,12 @@ fd_status fd_cov_err_from_gram(const double* AtA, const float* B, int32_t ell, i
                                double* err, double* lam_max, double* lam_min,
                                void* ws, size_t ws_bytes, void* cuda_stream);
 
+/* frob_sq [host] = trace(AtA) = ||A||_F^2 (PAPER.md:57's denominator) of AtA
+ * [device] (d x d fp64 from fd_cov_gram_partial, summed over ranks): the d
+ * diagonal entries are copied to the host and summed in index order.
+ * Synchronises the stream.  Errors: INVALID_ARG, CUDA. */
+fd_status fd_cov_frob_from_gram(const double* AtA, int64_t d, double* frob_sq, void* cuda_stream);
+
 /* Single-GPU convenience: AtA from A, then fd_cov_err_from_gram with
  * frob_sq = trace(A^T A).  A, B [device]. */
 fd_status fd_cov_err(const float* A, int64_t n, int64_t ld, const float* B, int32_t ell, int64_t d,

@@ -16,7 +16,7 @@ import ctypes
 
 from ._lib import FD_MAX_N, VARIANT, FdConfig, FdError, FdStats, check, lib
 
-__all__ = ["Sketcher", "cov_err", "cov_gram_partial", "cov_err_from_gram", "proj_err", "proj_err_from_gram", "hash_sketch", "FdError", "VARIANT", "FD_MAX_N",
+__all__ = ["Sketcher", "cov_err", "cov_gram_partial", "cov_err_from_gram", "cov_frob_from_gram", "proj_err", "proj_err_from_gram", "hash_sketch", "FdError", "VARIANT", "FD_MAX_N",
            "is_batched"]
 
 
@@ -119,13 +119,16 @@ class Sketcher:
     def reset(self):
         """Start a fresh stream with the same handle and workspace."""
         check(lib().fd_reset(self.h))
-        self._keep.clear()
+        if self._keep:
+            # the last staged host->device copies may still read the pinned inputs
+            self.stream.synchronize()
+            self._keep.clear()
         return self
 
     def profile(self, enable=True):
         check(lib().fd_profile(self.h, 1 if enable else 0))
 
-    KERNELS = ("ingest", "gram", "eig", "recon", "trd", "bt")
+    KERNELS = ("ingest", "gram", "eig", "recon", "trd", "bt", "perrow")
 
     def profile_read(self):
         """{kernel: (total_ms, launches)} since the last read (synchronises)."""
@@ -164,6 +167,15 @@ def cov_gram_partial(A, AtA, stream=None):
     check(lib().fd_cov_gram_partial(A.data_ptr(), A.shape[0], A.stride(0), A.shape[1], AtA.data_ptr(), None, 0,
                                     s.cuda_stream))
     return AtA
+
+
+def cov_frob_from_gram(AtA, stream=None):
+    """||A||_F^2 = trace(AtA) of a d x d fp64 cuda Gram (fd_cov_frob_from_gram; synchronises)."""
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream(AtA.device)
+    out = ctypes.c_double()
+    check(lib().fd_cov_frob_from_gram(AtA.data_ptr(), AtA.shape[0], ctypes.byref(out), s.cuda_stream))
+    return out.value
 
 
 def cov_err_from_gram(AtA, B, frob_sq, stream=None):

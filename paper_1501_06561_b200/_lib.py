@@ -24,7 +24,7 @@ FD_MAX_N = 416
 # every symbol include/fd.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "fd_workspace_bytes", "fd_create", "fd_append_rows", "fd_host_stage_bytes", "fd_append_rows_host", "fd_sketch", "fd_merge", "fd_shard_sketch",
-    "fd_destroy", "fd_reset", "fd_profile", "fd_profile_read", "fd_cov_workspace_bytes", "fd_cov_gram_partial", "fd_cov_err_from_gram", "fd_cov_err",
+    "fd_destroy", "fd_reset", "fd_profile", "fd_profile_read", "fd_cov_workspace_bytes", "fd_cov_gram_partial", "fd_cov_err_from_gram", "fd_cov_frob_from_gram", "fd_cov_err",
     "fd_proj_workspace_bytes", "fd_proj_err_from_gram", "fd_proj_err", "fd_hash_workspace_bytes", "fd_hash_sketch",
     "fd_last_error", "fd_version",
 ]
@@ -79,6 +79,7 @@ def lib():
         L.fd_cov_workspace_bytes.restype = sz
         L.fd_cov_gram_partial.argtypes = [vp, i64, i64, i64, vp, vp, sz, vp]
         L.fd_cov_err_from_gram.argtypes = [vp, vp, i32, i64, dbl, dp, dp, dp, vp, sz, vp]
+        L.fd_cov_frob_from_gram.argtypes = [vp, i64, dp, vp]
         L.fd_cov_err.argtypes = [vp, i64, i64, vp, i32, i64, dp, dp, dp, vp, sz, vp]
         L.fd_proj_workspace_bytes.argtypes = [i64, i32, i32]
         L.fd_proj_workspace_bytes.restype = sz
@@ -89,7 +90,7 @@ def lib():
         L.fd_hash_sketch.argtypes = [vp, i64, i64, i64, i32, i32, ctypes.c_uint64, i64, vp, vp, sz, vp]
         for f in ("fd_create", "fd_append_rows", "fd_append_rows_host", "fd_sketch", "fd_merge", "fd_shard_sketch", "fd_destroy",
                   "fd_reset", "fd_profile",
-                  "fd_cov_gram_partial", "fd_cov_err_from_gram", "fd_cov_err", "fd_proj_err_from_gram", "fd_proj_err", "fd_hash_sketch"):
+                  "fd_cov_gram_partial", "fd_cov_err_from_gram", "fd_cov_frob_from_gram", "fd_cov_err", "fd_proj_err_from_gram", "fd_proj_err", "fd_hash_sketch"):
             getattr(L, f).restype = ctypes.c_int
         L.fd_last_error.restype = ctypes.c_char_p
         L.fd_version.restype = ctypes.c_char_p

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <limits>
 #include <string>
 #include <vector>
 
@@ -45,8 +46,18 @@ constexpr size_t kArenaHalf = 8u << 20;       // descriptor arena half (bytes)
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Every handle entry point runs on the handle's device and restores the caller's.
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int dev) {
+    int cur = 0;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+  }
+  ~DevGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
 struct Layout {
-  size_t buf0, buf1, nodes, G, Wt, stats, flag, eig, arena, total;
+  size_t buf0, buf1, nodes, G, Wt, stats, flag, eig, arena, state, total;
   int nnodes, nslots;
 };
 
@@ -57,6 +68,7 @@ struct Derived {
   int t;         // delta = lambda_t (ell; paper-literal Fast alpha-FD: ell - ceil(alpha ell/2))
   bool cfd;      // Compensative FD: lazy ReduceRank + compensated final step (reading C27)
   bool perrow;   // Alg. 1 per-row chain (buffer L = ell)
+  bool prk;      // per-row chain on the persistent per-row kernel (fd_perrow.cu, fp64 state)
   size_t gbytes; // element size of the Gram / Wt scratch
 };
 
@@ -105,6 +117,11 @@ bool derive(const fd_config* c, Derived* D, std::string* why) {
   D->nmax = std::max(D->L, 2 * D->R);
   if (c->n_shards == 1) D->nmax = D->L;  // merges only via fd_merge (checked there)
   D->ldg = (std::max(D->nmax, 2 * D->R) + 3) / 4 * 4;
+  {
+    Params q{};
+    q.d = D->d; q.ell = D->ell; q.ret = D->R; q.tdel = D->t;
+    D->prk = D->perrow && fdk::perrow_supported(D->ell, D->d, q);
+  }
   return true;
 }
 
@@ -129,6 +146,7 @@ Layout layout(const Derived& D) {
   Lo.flag = take(sizeof(int) * 4);
   Lo.eig = take(fdk::eig_scratch_bytes(D.ldg));
   Lo.arena = take(2 * kArenaHalf);
+  Lo.state = D.prk ? take((size_t)D.P * D.ell * D.ldb * sizeof(double)) : 0;   // fp64 per-row state
   Lo.total = off;
   return Lo;
 }
@@ -150,6 +168,7 @@ struct fd_handle {
   Stats* stats;       // [P] shard stats, then [nnodes] node stats
   int* flag;
   double* eig;
+  double* state;      // fp64 per-row state (D.prk): P x ell x ldb
   char* arena;        // device descriptor arena (2 halves)
   char* host_arena;   // pinned host mirror
   cudaEvent_t ev[2];
@@ -157,6 +176,7 @@ struct fd_handle {
   cudaEvent_t ev_copied[2], ev_consumed[2];
   int half;
   size_t half_used;
+  size_t max_pitch;   // cudaDevAttrMaxPitch: larger 2-D copy pitches fall back to 1-D copies
   std::vector<int> occ, cur;
   int64_t rows_seen;
   bool dead;
@@ -198,7 +218,7 @@ fd_status push_desc(fd_handle* h, const std::vector<T>& v, const T** out) {
   return FD_OK;
 }
 
-enum { K_INGEST = 0, K_GRAM = 1, K_EIG = 2, K_RECON = 3, K_TRD = 4, K_BT = 5, K_COUNT = 6 };
+enum { K_INGEST = 0, K_GRAM = 1, K_EIG = 2, K_RECON = 3, K_TRD = 4, K_BT = 5, K_PERROW = 6, K_COUNT = 7 };
 
 cudaEvent_t get_event(fd_handle* h) {
   if (!h->pool.empty()) {
@@ -415,6 +435,7 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
   h->stats = reinterpret_cast<Stats*>(h->ws + Lo.stats);
   h->flag = reinterpret_cast<int*>(h->ws + Lo.flag);
   h->eig = reinterpret_cast<double*>(h->ws + Lo.eig);
+  h->state = D.prk ? reinterpret_cast<double*>(h->ws + Lo.state) : nullptr;
   h->arena = h->ws + Lo.arena;
   h->half = 0;
   h->half_used = 0;
@@ -423,7 +444,10 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
   h->rows_seen = 0;
   h->dead = false;
   h->prof = false;
-  cudaError_t e = cudaSetDevice(h->device);
+  DevGuard guard(h->device);
+  int pitch = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&pitch, cudaDevAttrMaxPitch, h->device);
+  h->max_pitch = pitch > 0 ? (size_t)pitch : ((size_t)1 << 31);
   if (e == cudaSuccess) e = cudaMallocHost(&h->host_arena, 2 * kArenaHalf);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev[0], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev[1], cudaEventDisableTiming);
@@ -447,6 +471,82 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
   return FD_OK;
 }
 
+// Rows a per-row chain keeps in its state after n more rows (slot semantics, C6):
+// Alg. 1 reduces when the buffer fills (occupancy ell -> ell-1); Compensative FD
+// reduces lazily, when the next row arrives at a full buffer (reading C27).
+static int perrow_occ_after(const Derived& D, int occ, int64_t n) {
+  if (n <= 0) return occ;
+  if (D.cfd) return (int)std::min<int64_t>((int64_t)occ + n, D.L);
+  return (int)std::min<int64_t>((int64_t)occ + n, D.L - 1);
+}
+
+// Rows per shard per staging round of a host-input per-row append.
+static int64_t perrow_stage_rows(const Derived& D) { return std::max<int64_t>(D.L, 16384 / D.P); }
+
+// Per-row variants on the persistent per-row kernel: one launch per call (device
+// rows) or per staged chunk (host rows, double-buffered copies on the copy stream).
+static fd_status append_perrow(fd_handle* h, const float* rows, int64_t n_rows, int64_t ld, bool host, float* stage,
+                               size_t stage_bytes) {
+  const int P = h->D.P;
+  const int64_t q = n_rows / P, r = n_rows % P;
+  std::vector<int64_t> start(P), rem(P);
+  int64_t off = 0;
+  for (int s = 0; s < P; ++s) {
+    start[s] = off;
+    rem[s] = q + (s < r ? 1 : 0);
+    off += rem[s];
+  }
+  const int64_t CH = host ? perrow_stage_rows(h->D) : std::numeric_limits<int64_t>::max();
+  const size_t slot_floats = (size_t)P * (size_t)std::min<int64_t>(CH, std::max<int64_t>(q + 1, 1)) * ld;
+  if (host && (!stage || stage_bytes < 2 * (size_t)P * CH * ld * sizeof(float)))
+    return fail(FD_ERR_WORKSPACE, "host staging buffer smaller than fd_host_stage_bytes()");
+  (void)slot_floats;
+  std::vector<fdk::RowJob> jobs;
+  for (int round = 0;; ++round) {
+    jobs.clear();
+    const int slot = round & 1;
+    float* base = host ? stage + (size_t)slot * P * CH * ld : nullptr;
+    if (host) FD_CUDA(cudaStreamWaitEvent(h->copy_stream, h->ev_consumed[slot], 0));
+    for (int s = 0; s < P; ++s) {
+      if (rem[s] == 0) continue;
+      const int64_t c = std::min(CH, rem[s]);
+      fdk::RowJob J{};
+      if (host) {
+        float* dstp = base + (size_t)s * CH * ld;
+        FD_CUDA(cudaMemcpyAsync(dstp, rows + start[s] * ld, (size_t)c * ld * sizeof(float), cudaMemcpyHostToDevice,
+                                h->copy_stream));
+        J.src = dstp;
+      } else {
+        J.src = rows + start[s] * ld;
+      }
+      J.ld = ld;
+      J.nrows = c;
+      J.state = h->state + (size_t)s * h->D.ell * h->D.ldb;
+      J.dst = shard_buf(h, s, h->cur[s]);
+      J.stats = h->stats + s;
+      J.k_in = h->occ[s];
+      jobs.push_back(J);
+      h->occ[s] = perrow_occ_after(h->D, h->occ[s], c);
+      start[s] += c;
+      rem[s] -= c;
+    }
+    if (jobs.empty()) break;
+    if (host) {
+      FD_CUDA(cudaEventRecord(h->ev_copied[slot], h->copy_stream));
+      FD_CUDA(cudaStreamWaitEvent(h->stream, h->ev_copied[slot], 0));
+    }
+    const fdk::RowJob* dj = nullptr;
+    fd_status st = push_desc(h, jobs, &dj);
+    if (st != FD_OK) return st;
+    const int nj = (int)jobs.size();
+    cudaError_t e = timed(h, K_PERROW, [&] { return fdk::launch_perrow(dj, nj, h->prm, h->D.cfd ? 1 : 0, h->flag, h->stream); });
+    if (e != cudaSuccess) return cuda_fail(e, "perrow");
+    if (host) FD_CUDA(cudaEventRecord(h->ev_consumed[slot], h->stream));
+  }
+  h->rows_seen += n_rows;
+  return FD_OK;
+}
+
 // Round loop shared by the device- and host-input appends.  Every call's rows are
 // split into P contiguous ranges (reading C10); each round ingests the next
 // min(L - occ, remaining) rows of every shard, then runs one batched ReduceRank
@@ -461,6 +561,8 @@ static fd_status append_impl(fd_handle* h, const float* rows, int64_t n_rows, in
   if (n_rows == 0) return FD_OK;
   if (!rows) return fail(FD_ERR_INVALID_ARG, "rows is NULL");
   if (ld < h->D.d) return fail(FD_ERR_SHAPE, "ld < d");
+  DevGuard guard(h->device);
+  if (h->D.prk) return append_perrow(h, rows, n_rows, ld, host, stage, stage_bytes);
   const int P = h->D.P, L = h->D.L, ell = h->D.ell;
   const size_t slot_floats = (size_t)P * L * ld;
   if (host && (!stage || stage_bytes < 2 * slot_floats * sizeof(float)))
@@ -502,8 +604,16 @@ static fd_status append_impl(fd_handle* h, const float* rows, int64_t n_rows, in
       const size_t cnt = j - i;
       const size_t width = (size_t)ch[i].c * ld * sizeof(float);
       const size_t spitch = (cnt > 1) ? (size_t)delta * ld * sizeof(float) : width;
-      FD_CUDA(cudaMemcpy2DAsync(base + i * (size_t)maxc * ld, (size_t)maxc * ld * sizeof(float), rows + ch[i].row * ld,
-                                spitch, width, cnt, cudaMemcpyHostToDevice, h->copy_stream));
+      const size_t dpitch = (size_t)maxc * ld * sizeof(float);
+      if (cnt > 1 && (spitch > h->max_pitch || dpitch > h->max_pitch)) {
+        // pitches beyond the device's 2-D copy limit: one 1-D copy per chunk
+        for (size_t k = i; k < j; ++k)
+          FD_CUDA(cudaMemcpyAsync(base + k * (size_t)maxc * ld, rows + ch[k].row * ld, width, cudaMemcpyHostToDevice,
+                                  h->copy_stream));
+      } else {
+        FD_CUDA(cudaMemcpy2DAsync(base + i * (size_t)maxc * ld, dpitch, rows + ch[i].row * ld, spitch, width, cnt,
+                                  cudaMemcpyHostToDevice, h->copy_stream));
+      }
       i = j;
     }
     FD_CUDA(cudaEventRecord(h->ev_copied[slot], h->copy_stream));
@@ -594,6 +704,7 @@ size_t fd_host_stage_bytes(const fd_config* cfg, int64_t ld) {
   Derived D;
   std::string why;
   if (!derive(cfg, &D, &why) || ld < D.d) return 0;
+  if (D.prk) return 2 * (size_t)D.P * perrow_stage_rows(D) * ld * sizeof(float);
   return 2 * (size_t)D.P * D.L * ld * sizeof(float);
 }
 
@@ -605,6 +716,7 @@ fd_status fd_append_rows_host(fd_handle* h, const float* host_rows, int64_t n_ro
 fd_status fd_sketch(fd_handle* h, float* B_out, fd_stats* st) {
   if (!h || !B_out) return fail(FD_ERR_INVALID_ARG, "NULL argument");
   if (h->dead) return fail(FD_ERR_STATE, "handle refuses work after a sticky error");
+  DevGuard guard(h->device);
   const bool cfd = h->D.cfd;
   fd_status s = finalize_shards(h, 0, h->D.P, cfd && h->D.P == 1);
   if (s != FD_OK) return s;
@@ -623,6 +735,7 @@ fd_status fd_merge(fd_handle* h, const float* sketches, int32_t count, float* B_
   if (count < 1 || count > kMergeMax) return fail(FD_ERR_INVALID_ARG, "count must be in [1, 64]");
   if (h->D.cfd)
     return fail(FD_ERR_UNSUPPORTED, "Compensative FD sketches are final (compensated); merge the handle's shards via fd_sketch");
+  DevGuard guard(h->device);
   const int ell = h->D.ell;
   FD_CUDA(cudaMemcpy2DAsync(node_buf(h, 0), h->D.ldb * sizeof(float), sketches, h->D.d * sizeof(float),
                             h->D.d * sizeof(float), (size_t)count * ell, cudaMemcpyDeviceToDevice, h->stream));
@@ -631,7 +744,7 @@ fd_status fd_merge(fd_handle* h, const float* sketches, int32_t count, float* B_
     FD_CUDA(cudaMemset2DAsync(node_buf(h, 0) + h->D.d, h->D.ldb * sizeof(float), 0,
                               (h->D.ldb - h->D.d) * sizeof(float), (size_t)count * ell, h->stream));
   }
-  FD_CUDA(cudaMemsetAsync(node_stats(h, 0), 0, sizeof(Stats) * (2 * count), h->stream));
+  FD_CUDA(cudaMemsetAsync(node_stats(h, 0), 0, sizeof(Stats) * (2 * count - 1), h->stream));
   int root = 0;
   fd_status s = run_tree(h, count, &root);
   if (s != FD_OK) return s;
@@ -650,6 +763,7 @@ fd_status fd_shard_sketch(fd_handle* h, int32_t shard, float* B_out) {
   if (!h || !B_out) return fail(FD_ERR_INVALID_ARG, "NULL argument");
   if (shard < 0 || shard >= h->D.P) return fail(FD_ERR_INVALID_ARG, "shard out of range");
   if (h->dead) return fail(FD_ERR_STATE, "handle refuses work after a sticky error");
+  DevGuard guard(h->device);
   fd_status s = finalize_shards(h, shard, shard + 1);
   if (s != FD_OK) return s;
   FD_CUDA(cudaMemcpy2DAsync(B_out, h->D.d * sizeof(float), node_buf(h, shard), h->D.ldb * sizeof(float),
@@ -659,6 +773,7 @@ fd_status fd_shard_sketch(fd_handle* h, int32_t shard, float* B_out) {
 
 fd_status fd_reset(fd_handle* h) {
   if (!h) return fail(FD_ERR_INVALID_ARG, "handle is NULL");
+  DevGuard guard(h->device);
   std::fill(h->occ.begin(), h->occ.end(), 0);
   std::fill(h->cur.begin(), h->cur.end(), 0);
   h->rows_seen = 0;
@@ -696,6 +811,7 @@ int32_t fd_profile_read(fd_handle* h, double* ms, int64_t* launches, int32_t max
 
 fd_status fd_destroy(fd_handle* h) {
   if (!h) return FD_OK;
+  DevGuard guard(h->device);
   cudaStreamSynchronize(h->stream);
   for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : h->pool) cudaEventDestroy(e);
@@ -766,6 +882,20 @@ fd_status fd_cov_err_from_gram(const double* AtA, const float* B, int32_t ell, i
   return FD_OK;
 }
 
+fd_status fd_cov_frob_from_gram(const double* AtA, int64_t d, double* frob_sq, void* cuda_stream) {
+  if (!AtA || !frob_sq || d < 1) return fail(FD_ERR_INVALID_ARG, "bad argument");
+  cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+  std::vector<double> diag(d);
+  cudaError_t e = cudaMemcpy2DAsync(diag.data(), sizeof(double), AtA, (d + 1) * sizeof(double), sizeof(double), d,
+                                    cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "trace");
+  double frob = 0.0;
+  for (double x : diag) frob += x;
+  *frob_sq = frob;
+  return FD_OK;
+}
+
 fd_status fd_cov_err(const float* A, int64_t n, int64_t ld, const float* B, int32_t ell, int64_t d, double* err,
                      double* lam_max, double* lam_min, void* ws, size_t ws_bytes, void* cuda_stream) {
   if (!ws || ws_bytes < fd_cov_workspace_bytes(d)) return fail(FD_ERR_WORKSPACE, "evaluator workspace too small");
@@ -776,14 +906,9 @@ fd_status fd_cov_err(const float* A, int64_t n, int64_t ld, const float* B, int3
   if (e != cudaSuccess) return cuda_fail(e, "memset");
   fd_status st = fd_cov_gram_partial(A, n, ld, d, AtA, ws, ws_bytes, cuda_stream);
   if (st != FD_OK) return st;
-  // frob = trace(A^T A)
-  std::vector<double> diag(d);
-  e = cudaMemcpy2DAsync(diag.data(), sizeof(double), AtA, (d + 1) * sizeof(double), sizeof(double), d,
-                        cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return cuda_fail(e, "trace");
   double frob = 0.0;
-  for (double x : diag) frob += x;
+  st = fd_cov_frob_from_gram(AtA, d, &frob, cuda_stream);
+  if (st != FD_OK) return st;
   return fd_cov_err_from_gram(AtA, B, ell, d, frob, err, lam_max, lam_min, ws, ws_bytes, cuda_stream);
 }
 
@@ -860,13 +985,9 @@ fd_status fd_proj_err(const float* A, int64_t n, int64_t ld, const float* B, int
   if (e != cudaSuccess) return cuda_fail(e, "memset");
   fd_status st = fd_cov_gram_partial(A, n, ld, d, AtA, nullptr, 0, cuda_stream);
   if (st != FD_OK) return st;
-  std::vector<double> diag(d);
-  e = cudaMemcpy2DAsync(diag.data(), sizeof(double), AtA, (d + 1) * sizeof(double), sizeof(double), d,
-                        cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return cuda_fail(e, "trace");
   double frob = 0.0;
-  for (double x : diag) frob += x;
+  st = fd_cov_frob_from_gram(AtA, d, &frob, cuda_stream);
+  if (st != FD_OK) return st;
   return fd_proj_err_from_gram(AtA, B, ell, d, frob, k, proj_err, nullptr, nullptr, ws, pb, cuda_stream);
 }
 

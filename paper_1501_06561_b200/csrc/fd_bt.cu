@@ -264,12 +264,8 @@ bool bt_supported(int nmax, const Params& p) { return p.pretrd && nmax <= kMaxNS
 cudaError_t launch_bt(const Prob* dev_probs, int count, const Params& p, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
   const int dyn = (int)bt_smem_bytes();
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(bt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static AttrOnce once;
+  if (cudaError_t e = once.ensure(bt_kernel, dyn); e != cudaSuccess) return e;
   const int grid = count < kNumSMs ? count : kNumSMs;
   bt_kernel<<<grid, kBtThreads, dyn, s>>>(dev_probs, count, p);
   return cudaGetLastError();

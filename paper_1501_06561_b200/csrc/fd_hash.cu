@@ -131,11 +131,9 @@ cudaError_t launch_hash(const float* A, int64_t n, int64_t ld, int64_t d, int el
   const int R = hash_ranges(d);
   const int64_t rpr = (n + R - 1) / R;
   const int smem = ell * kHashCols * (int)sizeof(double);
-  static int attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(hash_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
+  static AttrOnce once;
+  if (smem > 48 * 1024) {
+    if (cudaError_t e = once.ensure(hash_kernel, smem); e != cudaSuccess) return e;
   }
   if (n > 0) {
     hash_kernel<<<dim3((unsigned)nslices, (unsigned)R), kHashCols * s, smem, st>>>(A, n, ld, d, ell, s, seed, row0,

@@ -36,6 +36,22 @@ struct Prob {
   const Stats* child1;
 };
 
+// One shard stream's rows of an append call for the persistent per-row kernel
+// (fd_perrow.cu): rows src[0 .. nrows) (stride ld) in stream order, the fp64 state
+// (ell rows, stride Params.ldb doubles) carried across calls, its fp32 copy for
+// fd_sketch's final ReduceRank (the shard buffer), and the shard's statistics.
+struct RowJob {
+  const float* src;
+  int64_t ld;
+  int64_t nrows;
+  double* state;
+  float* dst;
+  Stats* stats;
+  int k_in;       // rows in the state at entry (occupancy)
+  int pad;
+};
+constexpr size_t kPrSmemMax = 200 * 1024;
+
 // Ingest of one shard in one round: copy nrows rows of the user's A into the
 // shard buffer (row stride ldb, zero-padded to ldb columns), accumulate ||a||^2.
 struct Ingest {
@@ -64,6 +80,23 @@ struct Params {
   long long* dbg;  // optional phase clock trace of problem 0 (FD_DEBUG_EIG), else null
 };
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) applies to the current device
+// only: remember, per kernel launcher, the device ordinals it was set on.
+struct AttrOnce {
+  unsigned long long done = 0;   // bit per device ordinal (< 64)
+  int bytes[64] = {};
+  template <typename K>
+  cudaError_t ensure(K kernel, int nbytes) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 64 && ((done >> dev) & 1ull) && bytes[dev] >= nbytes) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, nbytes);
+    if (e == cudaSuccess && dev < 64) { done |= 1ull << dev; bytes[dev] = nbytes; }
+    return e;
+  }
+};
+
 // All launchers return cudaGetLastError() after enqueueing.
 cudaError_t launch_ingest(const Ingest* dev_desc, int count, const Params& p, int* nonfinite, cudaStream_t s);
 cudaError_t launch_gram(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s);
@@ -81,6 +114,14 @@ cudaError_t launch_recon_tc(const Prob* dev_probs, int count, int nmax, const Pa
 cudaError_t launch_trd(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s);
 // Blocked (compact WY) back-transform + Wt = diag(w) U^T (fd_bt.cu), after eig when p.pretrd.
 cudaError_t launch_bt(const Prob* dev_probs, int count, const Params& p, cudaStream_t s);
+
+// Persistent per-row kernel (fd_perrow.cu): every row of an append call,
+// one thread-block cluster per shard stream, fp64 state, arrowhead eigen-updates.
+bool perrow_supported(int ell, int64_t d, const Params& p);
+int perrow_cluster(int ell, int64_t d);
+size_t perrow_smem_bytes(int ell, int64_t d, int C);
+cudaError_t launch_perrow(const RowJob* dev_jobs, int count, const Params& p, int lazy, int* nonfinite,
+                          cudaStream_t s);
 
 // Evaluator.
 cudaError_t launch_syrk_f64(const float* A, int64_t n, int64_t ld, int64_t d, double* AtA, cudaStream_t s);

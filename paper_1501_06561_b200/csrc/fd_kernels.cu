@@ -225,94 +225,8 @@ __global__ void __launch_bounds__(256) recon_kernel(const Prob* __restrict__ pro
   }
 }
 
-// fp32 reconstruct, register-blocked SGEMM: one CTA per (128-column tile of d,
-// 128-row block of Wt, problem); 256 threads, 8 x 8 outputs each; K (= buffer rows)
-// in steps of 8, double-buffered through registers.  A = Wt (rows j, contiguous
-// k) is transposed into As[k][j] on the store; B = Bf rows (contiguous n).
-__global__ void __launch_bounds__(256, 2) recon128_kernel(const Prob* __restrict__ probs, Params p) {
-  const Prob P = probs[blockIdx.z];
-  const int N = P.rows0 + P.rows1;
-  const int n0 = blockIdx.x * 128, j0 = blockIdx.y * 128;
-  const int jrows = p.ret;
-  if (j0 >= p.ell) return;
-  __shared__ __align__(16) float As[2][8][128 + 4];
-  __shared__ __align__(16) float Bs[2][8][128 + 4];
-  const float* Wt = static_cast<const float*>(P.Wt);
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  // loaders: A: row j0 + (tid >> 1), k-quad 4 * (tid & 1); B: k-row tid >> 5, columns 4 * (tid & 31)
-  const int aj = tid >> 1, ak = 4 * (tid & 1);
-  const int bk = tid >> 5, bn = 4 * (tid & 31);
-  const int ja = j0 + aj;
-  float acc[8][8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
-  auto load = [&](int k0, float4& av, float4& bv) {
-    av = make_float4(0.f, 0.f, 0.f, 0.f);
-    bv = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int ka = k0 + ak;
-    if (ja < jrows && ka < N) {
-      av = *reinterpret_cast<const float4*>(Wt + (int64_t)ja * p.ldg + ka);
-      if (ka + 1 >= N) av.y = 0.f;
-      if (ka + 2 >= N) av.z = 0.f;
-      if (ka + 3 >= N) av.w = 0.f;
-    }
-    const int kb = k0 + bk, nb = n0 + bn;
-    if (kb < N && nb < p.ldb) bv = __ldg(reinterpret_cast<const float4*>(prob_row(P, kb, p.ldb) + nb));
-  };
-  auto store = [&](int b, const float4& av, const float4& bv) {
-    As[b][ak + 0][aj] = av.x; As[b][ak + 1][aj] = av.y; As[b][ak + 2][aj] = av.z; As[b][ak + 3][aj] = av.w;
-    *reinterpret_cast<float4*>(&Bs[b][bk][bn]) = bv;
-  };
-  float4 av, bv;
-  load(0, av, bv);
-  store(0, av, bv);
-  __syncthreads();
-  const int nk = (N + 7) / 8;
-  for (int kt = 0; kt < nk; ++kt) {
-    const int b = kt & 1;
-    if (kt + 1 < nk) load(8 * (kt + 1), av, bv);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float4 a0 = *reinterpret_cast<const float4*>(&As[b][k][8 * ty]);
-      const float4 a1 = *reinterpret_cast<const float4*>(&As[b][k][8 * ty + 4]);
-      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[b][k][8 * tx]);
-      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[b][k][8 * tx + 4]);
-      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], bb[j], acc[i][j]);
-    }
-    if (kt + 1 < nk) store(b ^ 1, av, bv);
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int j = j0 + 8 * ty + i;
-    if (j >= p.ell) continue;
-    const int c = n0 + 8 * tx;
-    float* dst = P.dst + (int64_t)j * p.ldb + c;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (c + 4 * h >= p.ldb) continue;
-      const float4 o = (j < jrows) ? make_float4(acc[i][4 * h], acc[i][4 * h + 1], acc[i][4 * h + 2], acc[i][4 * h + 3])
-                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-      *reinterpret_cast<float4*>(dst + 4 * h) = o;
-    }
-  }
-}
-
-// Reconstruct, pipelined variant (fp32, ldg % 4 == 0, ldb % 4 == 0): same product as
-// recon128_kernel with a 4-stage cp.async pipeline (BK = 16).  A keeps its [j][k]
-// layout in shared memory and is read as k-pairs; thread rows are ty + 16 i and
-// columns 4 tx + 64 h, so every shared-memory read is conflict-free.
+// cp.async helpers of the pipelined reconstruct
 namespace {
-constexpr int kRcBK = 16, kRcStages = 4, kRcALd = 20, kRcBLd = 128;
-constexpr int kRcStageFloats = 128 * kRcALd + kRcBK * kRcBLd;
-
 __device__ __forceinline__ void cp_async16(float* dst, const float* src, int bytes) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes) : "memory");
@@ -322,93 +236,10 @@ template <int K>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory"); }
 }  // namespace
 
-__global__ void __launch_bounds__(256, 2) recon_pipe_kernel(const Prob* __restrict__ probs, Params p) {
-  const Prob P = probs[blockIdx.z];
-  const int N = P.rows0 + P.rows1;
-  const int n0 = blockIdx.x * 128, j0 = blockIdx.y * 128;
-  const int jrows = p.ret;
-  if (j0 >= p.ell) return;
-  extern __shared__ __align__(16) float rsm[];
-  const float* Wt = static_cast<const float*>(P.Wt);
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int nk = (N + kRcBK - 1) / kRcBK;
-  // loader: A chunks (row tid >> 2 and 64 + (tid >> 2), k-quad tid & 3); B chunks
-  // (k-row tid >> 5 and 8 + (tid >> 5), column quad tid & 31)
-  auto issue = [&](int kt) {
-    float* As = rsm + (kt % kRcStages) * kRcStageFloats;
-    float* Bs = As + 128 * kRcALd;
-    const int k0 = kt * kRcBK;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int m = (tid >> 2) + 64 * h, kq = 4 * (tid & 3), k = k0 + kq, j = j0 + m;
-      const int bytes = (j < jrows && k < N) ? 4 * min(4, N - k) : 0;
-      const float* src = bytes ? Wt + (int64_t)j * p.ldg + k : Wt;
-      cp_async16(As + m * kRcALd + kq, src, bytes);
-    }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int kr = (tid >> 5) + 8 * h, nq = 4 * (tid & 31), k = k0 + kr, n = n0 + nq;
-      const bool ok = k < N && n < p.ldb;
-      const float* src = ok ? prob_row(P, k, p.ldb) + n : Wt;
-      cp_async16(Bs + kr * kRcBLd + nq, src, ok ? 16 : 0);
-    }
-  };
-  float acc[8][8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
-#pragma unroll
-  for (int st = 0; st < kRcStages - 1; ++st) {
-    if (st < nk) issue(st);
-    cp_async_commit();
-  }
-  for (int kt = 0; kt < nk; ++kt) {
-    cp_async_wait<kRcStages - 2>();
-    __syncthreads();
-    if (kt + kRcStages - 1 < nk) issue(kt + kRcStages - 1);
-    cp_async_commit();
-    const float* As = rsm + (kt % kRcStages) * kRcStageFloats;
-    const float* Bs = As + 128 * kRcALd;
-#pragma unroll
-    for (int kk = 0; kk < kRcBK; kk += 2) {
-      float2 a[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float2*>(&As[(ty + 16 * i) * kRcALd + kk]);
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const float4 b0 = *reinterpret_cast<const float4*>(&Bs[(kk + u) * kRcBLd + 4 * tx]);
-        const float4 b1 = *reinterpret_cast<const float4*>(&Bs[(kk + u) * kRcBLd + 64 + 4 * tx]);
-        const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float av = u ? a[i].y : a[i].x;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av, bb[j], acc[i][j]);
-        }
-      }
-    }
-  }
-  cp_async_wait<0>();
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int j = j0 + ty + 16 * i;
-    if (j >= p.ell) continue;
-    float* dst = P.dst + (int64_t)j * p.ldb + n0;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int c = 64 * h + 4 * tx;
-      if (n0 + c >= p.ldb) continue;
-      const float4 o = (j < jrows) ? make_float4(acc[i][4 * h], acc[i][4 * h + 1], acc[i][4 * h + 2], acc[i][4 * h + 3])
-                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-      *reinterpret_cast<float4*>(dst + c) = o;
-    }
-  }
-}
-
-// Default reconstruct: CTA tile 128 (j) x 256 (n), thread tile 16 x 8 (rows ty + 8 i,
-// columns 4 lane + 128 h), 256 threads / 255 registers, one CTA per SM; the same
-// 4-stage cp.async pipeline (recon_pipe_kernel, 8 x 8 tiles, is FD_RECON1=1).
+// Default fp32 reconstruct: CTA tile 128 (j) x 256 (n), thread tile 16 x 8 (rows ty + 8 i,
+// columns 4 lane + 128 h), 256 threads / 255 registers, one CTA per SM, 4-stage
+// cp.async pipeline (BK = 32); A keeps its [j][k] layout in shared memory and is
+// read as broadcast k-pairs, B rows as conflict-free float4 runs.
 #ifndef FD_RC2_BK
 #define FD_RC2_BK 32
 #endif
@@ -505,38 +336,16 @@ __global__ void __launch_bounds__(256, 1) recon_pipe2_kernel(const Prob* __restr
 cudaError_t launch_recon(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
   (void)nmax;
-  if (!p.f64 && (p.ldg % 4) == 0 && (p.ldb % 4) == 0 && !getenv("FD_RECON1") && !getenv("FD_RECON128")) {
+  if (!p.f64) {   // ldg and ldb are multiples of 4 by construction (fd_api.cpp derive)
     constexpr int dyn = kRc2Stages * kRc2StageFloats * (int)sizeof(float);
-    static bool attr2 = false;
-    if (!attr2) {
-      cudaError_t e = cudaFuncSetAttribute(recon_pipe2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-      if (e != cudaSuccess) return e;
-      attr2 = true;
-    }
+    static AttrOnce once;
+    if (cudaError_t e = once.ensure(recon_pipe2_kernel, dyn); e != cudaSuccess) return e;
     dim3 grid((unsigned)((p.ldb + 255) / 256), (unsigned)((p.ell + 127) / 128), count);
     recon_pipe2_kernel<<<grid, 256, dyn, s>>>(dev_probs, p);
     return cudaGetLastError();
   }
-  if (!p.f64 && (p.ldg % 4) == 0 && (p.ldb % 4) == 0 && !getenv("FD_RECON128")) {
-    constexpr int dyn = kRcStages * kRcStageFloats * (int)sizeof(float);
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(recon_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
-    dim3 grid((unsigned)((p.ldb + 127) / 128), (unsigned)((p.ell + 127) / 128), count);
-    recon_pipe_kernel<<<grid, 256, dyn, s>>>(dev_probs, p);
-    return cudaGetLastError();
-  }
-  if (!p.f64 && (p.ldg % 4) == 0) {
-    dim3 grid((unsigned)((p.ldb + 127) / 128), (unsigned)((p.ell + 127) / 128), count);
-    recon128_kernel<<<grid, 256, 0, s>>>(dev_probs, p);
-    return cudaGetLastError();
-  }
   dim3 grid((unsigned)((p.ldb + 63) / 64), (unsigned)((p.ell + 63) / 64), count);
-  if (p.f64) recon_kernel<double><<<grid, 256, 0, s>>>(dev_probs, p);
-  else recon_kernel<float><<<grid, 256, 0, s>>>(dev_probs, p);
+  recon_kernel<double><<<grid, 256, 0, s>>>(dev_probs, p);
   return cudaGetLastError();
 }
 
@@ -1694,13 +1503,8 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
 template <typename T, int NM, bool GAPK, bool PRE = false, bool BIG = false>
 static cudaError_t launch_eig_t(const Prob* dev_probs, int count, const Params& p, double* scratch, cudaStream_t s) {
   using C = EigCfg<T, NM, GAPK, PRE>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(eig_kernel<T, NM, GAPK, PRE, BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)C::kBytes);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static AttrOnce once;
+  if (cudaError_t e = once.ensure(eig_kernel<T, NM, GAPK, PRE, BIG>, (int)C::kBytes); e != cudaSuccess) return e;
   const int slots = kNumSMs * (PRE ? kEigPreCtasPerSM : 1);
   const int grid = count < slots ? count : slots;
   eig_kernel<T, NM, GAPK, PRE, BIG><<<grid, PRE ? 256 : kEigThreads, C::kBytes, s>>>(dev_probs, count, p, scratch);

@@ -1,0 +1,660 @@
+// fd_perrow.cu — persistent per-row Frequent Directions kernel:
+// Alg. 1's row loop for the per-row variants FD,
+// alpha-FD (Alg. 2), iSVD, SpaceSaving Directions
+// (Alg. 3) and Compensative FD's lazy stream,
+// one thread-block cluster per shard stream, every row of an append call in one
+// launch, the sketch state in fp64.
+//
+// Row step.  After every step the state rows b_1..b_k are mutually orthogonal
+// (B' = diag(w) U^T Bf has orthogonal rows: u_j^T G u_i = lambda_j delta_ij), so the
+// Gram of [B; a] is the arrowhead
+//       H = [[ D, z ], [ z^T, rho ]],  D = diag(||b_j||^2), z_j = b_j . a, rho = ||a||^2
+// (the neglected b_i . b_j, i != j, are fp64 rounding, ~1e-16 ||B||^2).  Its
+// eigenvalues are the roots of the secular equation
+//       f(lambda) = lambda - rho - sum_j z_j^2 / (lambda - d_j) = 0,
+// one in each interval between consecutive poles (interlacing), after deflating
+// z_j ~ 0 and coincident poles (Givens).  Eigenvectors come from Loewner's formula
+// (Gu-Eisenstat): z^_i^2 = -prod_m (d_i - lambda_m) / prod_{j != i} (d_i - d_j) is the
+// z for which the computed lambdas are exact, and u_m ~ [z^/(lambda_m - D); 1], so the
+// vectors are numerically orthogonal.  When the buffer is full (k + 1 = ell) the
+// variant's ReduceRank rule picks delta and sigma'^2 exactly as the batched path
+// (eig_kernel) and the oracle do; otherwise (the first ell - 1 rows; Compensative
+// FD's pending row) the step only rotates: B' = U^T Bf keeps every row (B'^T B' =
+// Bf^T Bf; the oracle keeps those rows unrotated: the same covariance).
+//
+// Work split: CTA r of a cluster of C owns the column slice [r dc, (r+1) dc) of the
+// state (fp64, resident in shared memory for the whole call).  Per row: (1) the
+// slice's partial dots b_j . a, ||b_j||^2, ||a||^2 (thread tile 8 rows x 4 columns,
+// 16-lane reduce-scatter); (2) cluster barrier, every CTA sums the C partial vectors
+// from distributed shared memory in the same order (bit-identical inputs, so every
+// CTA takes the same decisions); (3) the secular roots are split over the cluster
+// (warp per root, lanes over the terms) and gathered after a second barrier; (4)
+// Loewner vectors and the rule, redundantly in every CTA; (5) the slice's
+// reconstruct B'[:, slice] = W^T [B; a][:, slice] (fp64 register tiles 8 x 4) into
+// the other state buffer.  fp64 throughout.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include <float.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "fd_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace fdk {
+
+namespace {
+
+constexpr int kPrThreads = 256;
+constexpr int kPrMaxRows = 128;           // state rows the register tiles cover (16 groups x 8)
+constexpr int kPrColsPass = 64;           // columns per tile pass (16 lanes x 4)
+constexpr int kPL = 2 * kPrMaxRows + 2;   // partial vector: c[128], nrm[128], ||a||^2
+constexpr unsigned kFull = 0xffffffffu;
+
+struct PrLayout {
+  int ellp;       // state rows allocated (ell rounded up to 8)
+  int dcp;        // state row stride (doubles), multiple of 4, >= dc
+  int ws;         // WtT row stride (doubles): ellp + 2
+  size_t S0, S1, arow, part, full, rp, rt, dsort, zsort, dpol, z2, zhat, lam, wout, scl, sclo, rc, rs, WtT, ints,
+      total;
+};
+
+__host__ __device__ inline size_t pr_align(size_t x) { return (x + 15) & ~(size_t)15; }
+
+__host__ __device__ inline PrLayout pr_layout(int ell, int dc) {
+  PrLayout L;
+  L.ellp = (ell + 7) / 8 * 8;
+  L.dcp = (dc + 3) / 4 * 4;
+  L.ws = L.ellp + 2;
+  const size_t v = (size_t)(ell + 2) * 8;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = pr_align(off + bytes); return o; };
+  L.S0 = take((size_t)L.ellp * L.dcp * 8);
+  L.S1 = take((size_t)L.ellp * L.dcp * 8);
+  L.arow = take((size_t)L.dcp * 8);
+  L.part = take((size_t)2 * kPL * 8);     // double-buffered across rows (DSMEM readers)
+  L.full = take((size_t)kPL * 8);
+  L.rp = take(v);                          // roots: nearer pole p and offset tau (lambda = p + tau)
+  L.rt = take(v);
+  L.dsort = take(v);                       // arrowhead diagonal, sorted (coordinate order)
+  L.zsort = take(v);
+  L.dpol = take(v);                        // non-deflated poles (secular equation)
+  L.z2 = take(v);
+  L.zhat = take(v);                        // Loewner z^
+  L.lam = take(v);                         // eigenvalue of each eigen slot
+  L.wout = take(v);                        // rule weight of each output row
+  L.scl = take(v);                         // pre-scale of each state row (CFD pending shrink)
+  L.sclo = take(v);                        // final scale of each output column (weight / norm)
+  L.rc = take(v);                          // Givens deflations
+  L.rs = take(v);
+  L.WtT = take((size_t)(ell + 1) * L.ws * 8);   // rows: Bf rows (state rows, then a); cols: outputs
+  L.ints = take((size_t)9 * (ell + 2) * 4 + 16 * 4);
+  L.total = off;
+  return L;
+}
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// One secular root (whole warp; lanes over the terms).  Poles dp[0..K-1] strictly
+// decreasing, z2 = z^2 > 0, tip rho, zn = ||z||.  Root m lies in (dp[m], dp[m-1])
+// (dp[-1] = +inf, dp[K] = -inf).  Returns lambda = p + tau with p the nearer pole
+// (tau then carries the root's distance to it to full relative accuracy).
+// Safeguarded Newton on g(tau) = tau f(p + tau), which has no pole at tau = 0,
+// started from the root of the model with the other poles frozen; bisection on the
+// bracket (sign of f) whenever a step leaves it.
+__device__ void secular_root(int m, int K, const double* dp, const double* z2, double rho, double zn, int lane,
+                             double& p_out, double& t_out) {
+  int ip;
+  double p, lo, hi;
+  if (m == 0) {
+    ip = 0;
+    p = dp[0];
+    lo = 0.0;
+    hi = (fmax(rho - p, 0.0) + zn) * (1.0 + 8.0 * DBL_EPSILON) + DBL_MIN;
+  } else if (m == K) {
+    ip = K - 1;
+    p = dp[K - 1];
+    hi = 0.0;
+    lo = -(fmax(p - rho, 0.0) + zn) * (1.0 + 8.0 * DBL_EPSILON) - DBL_MIN;
+  } else {
+    const double a = dp[m], b = dp[m - 1];
+    const double mid = 0.5 * (a + b);
+    double s = 0.0;
+    for (int i = lane; i < K; i += 32) s += z2[i] / (mid - dp[i]);
+    s = wsum(s);
+    if (mid - rho - s >= 0.0) { ip = m; p = a; lo = 0.0; hi = mid - a; }
+    else { ip = m - 1; p = b; lo = mid - b; hi = 0.0; }
+  }
+  double s0 = 0.0;
+  for (int i = lane; i < K; i += 32)
+    if (i != ip) s0 += z2[i] / (p - dp[i]);
+  s0 = wsum(s0);
+  const double zp = z2[ip];
+  const double B = p - rho - s0;          // f(p + t) ~ t + B - zp / t
+  const double disc = sqrt(B * B + 4.0 * zp);
+  double t;
+  if (hi > 0.0) t = (B <= 0.0) ? 0.5 * (disc - B) : 2.0 * zp / (B + disc);
+  else t = (B >= 0.0) ? -0.5 * (B + disc) : -2.0 * zp / (disc - B);
+  if (!(t > lo && t < hi)) t = 0.5 * (lo + hi);
+  for (int it = 0; it < 80; ++it) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int i = lane; i < K; i += 32) {
+      if (i == ip) continue;
+      const double r = 1.0 / (t - (dp[i] - p));
+      const double q = z2[i] * r;
+      s1 += q;
+      s2 = fma(q, r, s2);
+    }
+    s1 = wsum(s1);
+    s2 = wsum(s2);
+    const double f = (p + t - rho) - zp / t - s1;
+    if (f < 0.0) lo = t; else hi = t;
+    const double g = t * (p + t - rho) - zp - t * s1;
+    const double gp = (p + 2.0 * t - rho) - s1 + t * s2;
+    double tn = t - g / gp;
+    if (!(tn > lo && tn < hi)) tn = 0.5 * (lo + hi);
+    const double step = fabs(tn - t);
+    t = tn;
+    if (f == 0.0 || step <= 2.0 * DBL_EPSILON * fabs(t) || hi - lo <= 4.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)))
+      break;
+  }
+  p_out = p;
+  t_out = t;
+}
+
+// block-wide sum of one double per thread (kPrThreads), result in every thread
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  v = wsum(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int w = 0; w < kPrThreads / 32; ++w) s += red[w];
+  return s;
+}
+
+}  // namespace
+
+size_t perrow_smem_bytes(int ell, int64_t d, int C) {
+  const int dc = (int)((d + C - 1) / C);
+  return pr_layout(ell, dc).total;
+}
+
+// Cluster size of a per-row stream: enough CTAs that the state slice fits in shared
+// memory and the per-row reconstruct (~ell^2 dc fp64 FMAs per CTA) stays short.
+int perrow_cluster(int ell, int64_t d) {
+  const double work = (double)ell * ell * (double)d;
+  int C = 1;
+  while (C < 8 && (work / C > 65536.0 || perrow_smem_bytes(ell, d, C) > kPrSmemMax)) C *= 2;
+  if (perrow_smem_bytes(ell, d, C) > kPrSmemMax) return 0;
+  return C;
+}
+
+bool perrow_supported(int ell, int64_t d, const Params& p) {
+  return ell >= 2 && ell < kPrMaxRows && p.ret == ell - 1 && p.tdel == ell && perrow_cluster(ell, d) > 0;
+}
+
+__global__ void __launch_bounds__(kPrThreads, 1)
+perrow_kernel(const RowJob* __restrict__ jobs, Params p, int C, int lazy, int* __restrict__ nonfinite) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank();
+  const RowJob J = jobs[blockIdx.x / C];
+  const int ell = p.ell, d = (int)p.d;
+  const int dc = (d + C - 1) / C;
+  const int c0 = crank * dc, c1 = min(d, c0 + dc), ncol = max(0, c1 - c0);
+  const PrLayout Lo = pr_layout(ell, dc);
+  extern __shared__ __align__(16) unsigned char smem[];
+  auto D_ = [&](size_t o) { return reinterpret_cast<double*>(smem + o); };
+  double* Sbuf[2] = {D_(Lo.S0), D_(Lo.S1)};
+  double *arow = D_(Lo.arow), *part = D_(Lo.part), *full = D_(Lo.full), *rp = D_(Lo.rp), *rt = D_(Lo.rt);
+  double *dsort = D_(Lo.dsort), *zsort = D_(Lo.zsort), *dpol = D_(Lo.dpol), *z2 = D_(Lo.z2), *zhat = D_(Lo.zhat);
+  double *lam = D_(Lo.lam), *wout = D_(Lo.wout), *scl = D_(Lo.scl), *sclo = D_(Lo.sclo), *rc = D_(Lo.rc);
+  double *rs = D_(Lo.rs), *WtT = D_(Lo.WtT);
+  int* ib = reinterpret_cast<int*>(smem + Lo.ints);
+  const int E = ell + 2;
+  int* perm = ib;              // sorted coordinate -> state row
+  int* dflag = ib + E;         // coordinate deflated?
+  int* pidx = ib + 2 * E;      // coordinate -> pole index (non-deflated) or -1
+  int* coord = ib + 3 * E;     // pole index -> coordinate
+  int* slot_src = ib + 4 * E;  // eigen slot -> root m (>= 0) or ~coordinate (deflated)
+  int* order = ib + 5 * E;     // sorted position -> eigen slot
+  int* out_src = ib + 6 * E;   // output row -> eigen slot
+  int* rot_a = ib + 7 * E;     // Givens deflation pairs (coordinates)
+  int* rot_b = ib + 8 * E;
+  int* misc = ib + 9 * E;      // [0] K  [1] nrot  [2] close pair found
+  __shared__ double s_red[kPrThreads / 32];
+  __shared__ double s_stat[4];  // frob, delta, removed, shrinks of this call (CTA-local copy)
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cgp = lane & 15, rg = (lane >> 4) + 2 * warp;   // tile: rows 8 rg .. +7, cols 4 cgp .. +3
+  const int lds = Lo.dcp, ws = Lo.ws;
+
+  // ---- load the state slice (fp64, persistent across calls) ----
+  int k = J.k_in;
+  int cur = 0;
+  for (int e = tid; e < Lo.ellp * lds; e += kPrThreads) {
+    const int r = e / lds, c = e - r * lds;
+    Sbuf[0][e] = (r < k && c < ncol) ? J.state[(int64_t)r * p.ldb + c0 + c] : 0.0;
+    Sbuf[1][e] = 0.0;
+  }
+  if (tid < 4) s_stat[tid] = 0.0;
+  for (int e = tid; e < 2 * kPL; e += kPrThreads) part[e] = 0.0;
+  if (tid < 16) misc[tid] = 0;
+  __syncthreads();
+  if (C > 1) cluster.sync();
+
+  const double eps = DBL_EPSILON;
+  int bad = 0;
+  float pre = 0.f;                      // prefetched element (column c0 + tid) of the next row
+  if (J.nrows > 0 && tid < ncol) pre = J.src[c0 + tid];
+
+  for (int64_t t = 0; t < J.nrows; ++t) {
+    const double* S = Sbuf[cur];
+    double* Sn = Sbuf[cur ^ 1];
+    double* pt = part + (t & 1) * kPL;
+    // ---- the row's slice (fp64) into shared memory; prefetch the next row ----
+    if (tid < lds) arow[tid] = (tid < ncol) ? (double)pre : 0.0;
+    for (int c = tid + kPrThreads; c < lds; c += kPrThreads)
+      arow[c] = (c < ncol) ? (double)J.src[t * J.ld + c0 + c] : 0.0;
+    if (tid < ncol) bad |= !isfinite(pre);
+    if (t + 1 < J.nrows && tid < ncol) pre = J.src[(t + 1) * J.ld + c0 + tid];
+    __syncthreads();
+    // ---- (1) slice partials: c_j = b_j . a, n_j = ||b_j||^2, ||a||^2 ----
+    {
+      double v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = 0.0;
+      if (8 * rg < k) {
+        for (int cb = 0; cb < lds; cb += kPrColsPass) {
+          const int c = cb + 4 * cgp;
+          if (c >= lds) break;
+          const double2 a01 = *reinterpret_cast<const double2*>(arow + c);
+          const double2 a23 = *reinterpret_cast<const double2*>(arow + c + 2);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const double* row = S + (8 * rg + q) * lds + c;
+            const double2 b01 = *reinterpret_cast<const double2*>(row);
+            const double2 b23 = *reinterpret_cast<const double2*>(row + 2);
+            v[q] = fma(b01.x, a01.x, fma(b01.y, a01.y, fma(b23.x, a23.x, fma(b23.y, a23.y, v[q]))));
+            v[8 + q] = fma(b01.x, b01.x, fma(b01.y, b01.y, fma(b23.x, b23.x, fma(b23.y, b23.y, v[8 + q]))));
+          }
+        }
+      }
+      // reduce-scatter over the 16 column lanes: lane cgp ends with value cgp's total
+#pragma unroll
+      for (int lvl = 0; lvl < 4; ++lvl) {
+        const int half = 8 >> lvl;
+        const bool up = (cgp >> (3 - lvl)) & 1;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (q < half) {
+            const double snd = up ? v[q] : v[q + half];
+            const double kp = up ? v[q + half] : v[q];
+            v[q] = kp + __shfl_xor_sync(kFull, snd, half);
+          }
+        }
+      }
+      if (8 * rg < kPrMaxRows) pt[(cgp < 8 ? 0 : kPrMaxRows) + 8 * rg + (cgp & 7)] = v[0];
+      if (warp == 0) {
+        double na = 0.0;
+        for (int c = lane; c < lds; c += 32) na = fma(arow[c], arow[c], na);
+        na = wsum(na);
+        if (lane == 0) pt[2 * kPrMaxRows] = na;
+      }
+    }
+    // ---- (2) cluster-wide sums, fixed order (identical in every CTA) ----
+    if (C > 1) cluster.sync(); else __syncthreads();
+    for (int e = tid; e <= 2 * kPrMaxRows; e += kPrThreads) {
+      const bool used = (e < k) || (e >= kPrMaxRows && e < kPrMaxRows + k) || e == 2 * kPrMaxRows;
+      double s = 0.0;
+      if (used)
+        for (int r = 0; r < C; ++r) s += (r == crank ? pt : cluster.map_shared_rank(pt, r))[e];
+      full[e] = s;
+    }
+    __syncthreads();
+    const double rho = full[2 * kPrMaxRows];
+    if (tid == 0) s_stat[0] += rho;
+    // ---- (3) Compensative FD: ReduceRank of the full pending buffer first (C27).  Its
+    //      Gram is diag(||b_j||^2); the FD rule gives every state row a weight ----
+    if (tid <= ell) scl[tid] = 1.0;
+    const bool full_pend = lazy && (k == ell);
+    if (full_pend) {
+      if (tid < k) {
+        const double dv = fmax(full[kPrMaxRows + tid], 0.0);
+        int rk = 0;
+        for (int j = 0; j < k; ++j) {
+          const double dj = fmax(full[kPrMaxRows + j], 0.0);
+          rk += (dj > dv) || (dj == dv && j < tid);
+        }
+        order[rk] = tid;
+        lam[rk] = dv;
+      }
+      __syncthreads();
+      const double delta = lam[ell - 1];
+      double rem = 0.0;
+      if (tid < ell) {
+        const double lj = lam[tid];
+        double sp2 = 0.0;
+        if (tid < ell - 1) sp2 = (tid < ell - p.m) ? lj : fmax(lj - delta, 0.0);
+        rem = lj - sp2;
+        scl[order[tid]] = (lj > 0.0) ? sqrt(sp2) / sqrt(lj) : 0.0;
+      }
+      rem = block_sum(rem, s_red);
+      if (tid == 0) { s_stat[1] += delta; s_stat[2] += rem; s_stat[3] += 1.0; }
+    }
+    __syncthreads();
+    // the pending shrink frees the slot of the smallest direction (slot semantics, C6):
+    // that row leaves the arrowhead; kc state coordinates + the new row remain
+    const int drop = full_pend ? order[ell - 1] : -1;
+    const int kc = full_pend ? k - 1 : k;
+    const int n = kc + 1;
+    const bool shrink = !lazy && (n == ell);
+    // ---- (4) arrowhead coordinates: D' = scl^2 D sorted descending (ties by row) ----
+    if (tid < k && tid != drop) {
+      const double sc = scl[tid];
+      const double dv = sc * sc * fmax(full[kPrMaxRows + tid], 0.0);
+      int rk = 0;
+      for (int j = 0; j < k; ++j) {
+        if (j == drop) continue;
+        const double sj = scl[j];
+        const double dj = sj * sj * fmax(full[kPrMaxRows + j], 0.0);
+        rk += (dj > dv) || (dj == dv && j < tid);
+      }
+      perm[rk] = tid;
+      dsort[rk] = dv;
+      zsort[rk] = sc * full[tid];
+    }
+    __syncthreads();
+    double zz = 0.0;
+    if (tid < kc) zz = zsort[tid] * zsort[tid];
+    zz = block_sum(zz, s_red);
+    const double znorm = sqrt(zz);
+    const double tol = 8.0 * eps * (fmax((kc > 0) ? dsort[0] : 0.0, rho) + znorm);
+    if (tid < kc) dflag[tid] = fabs(zsort[tid]) <= tol;
+    __syncthreads();
+    // coincident poles (parallel detection; the chain is resolved serially, rarely)
+    if (tid < kc && !dflag[tid] && tid > 0) {
+      int j = tid - 1;
+      while (j >= 0 && dflag[j]) --j;
+      if (j >= 0 && dsort[j] - dsort[tid] <= tol) misc[2] = 1;
+    }
+    __syncthreads();
+    if (misc[2]) {
+      if (tid == 0) {
+        int prev = -1, nrot = 0;
+        for (int i = 0; i < kc; ++i) {
+          if (dflag[i]) continue;
+          if (prev >= 0 && dsort[prev] - dsort[i] <= tol) {
+            const double zp = zsort[prev], zi = zsort[i];
+            const double r = hypot(zp, zi);
+            rc[nrot] = zp / r;
+            rs[nrot] = zi / r;
+            rot_a[nrot] = prev;
+            rot_b[nrot] = i;
+            ++nrot;
+            zsort[prev] = r;
+            zsort[i] = 0.0;
+            dflag[i] = 1;
+          } else {
+            prev = i;
+          }
+        }
+        misc[1] = nrot;
+        misc[2] = 0;
+      }
+    } else if (tid == 0) {
+      misc[1] = 0;
+    }
+    __syncthreads();
+    // pole indices (prefix count of the non-deflated coordinates)
+    if (tid < kc) {
+      int q = 0;
+      for (int j = 0; j < tid; ++j) q += !dflag[j];
+      pidx[tid] = dflag[tid] ? -1 : q;
+      if (!dflag[tid]) {
+        coord[q] = tid;
+        dpol[q] = dsort[tid];
+        z2[q] = zsort[tid] * zsort[tid];
+      }
+      if (tid == kc - 1) misc[0] = q + !dflag[tid];
+    }
+    if (kc == 0 && tid == 0) misc[0] = 0;
+    __syncthreads();
+    const int K = misc[0];
+    const int nrot = misc[1];
+    // ---- (5) secular roots, split over the cluster: root m -> CTA m % C ----
+    {
+      const int nroots = K + 1;
+      if (K == 0) {
+        if (tid == 0) { rp[0] = rho; rt[0] = 0.0; }
+      } else {
+        double zs = 0.0;
+        if (tid < K) zs = z2[tid];
+        zs = block_sum(zs, s_red);
+        const double zn = sqrt(zs);
+        for (int m = crank + C * warp; m < nroots; m += C * (kPrThreads / 32)) {
+          double pp, tt;
+          secular_root(m, K, dpol, z2, rho, zn, lane, pp, tt);
+          if (lane == 0) { rp[m] = pp; rt[m] = tt; }
+        }
+      }
+      if (C > 1) {
+        cluster.sync();
+        if (K > 0)
+          for (int m = tid; m < nroots; m += kPrThreads) {
+            const int own = m % C;
+            if (own != crank) {
+              rp[m] = cluster.map_shared_rank(rp, own)[m];
+              rt[m] = cluster.map_shared_rank(rt, own)[m];
+            }
+          }
+      }
+      __syncthreads();
+    }
+    // ---- (6) Loewner z^_q = sign(z_q) sqrt(-(d_q - l_q)(d_q - l_K) prod_{m != q} (d_q - l_m)/(d_q - d_m)) ----
+    if (tid < K) {
+      const double di = dpol[tid];
+      double prod = -((di - rp[tid]) - rt[tid]) * ((di - rp[K]) - rt[K]);
+      for (int m = 0; m < K; ++m)
+        if (m != tid) prod *= ((di - rp[m]) - rt[m]) / (di - dpol[m]);
+      zhat[tid] = copysign(sqrt(fmax(prod, 0.0)), zsort[coord[tid]]);
+    }
+    // eigen slots: roots 0..K, then the deflated coordinates (prefix count)
+    if (tid <= K) { slot_src[tid] = tid; lam[tid] = fmax(rp[tid] + rt[tid], 0.0); }
+    if (tid < kc && dflag[tid]) {
+      int q = 0;
+      for (int j = 0; j < tid; ++j) q += dflag[j];
+      slot_src[K + 1 + q] = ~tid;
+      lam[K + 1 + q] = fmax(dsort[tid], 0.0);
+    }
+    __syncthreads();
+    // eigenvalues sorted descending, ties by slot
+    if (tid < n) {
+      const double lv = lam[tid];
+      int rk = 0;
+      for (int j = 0; j < n; ++j) rk += (lam[j] > lv) || (lam[j] == lv && j < tid);
+      order[rk] = tid;
+    }
+    __syncthreads();
+    // ---- (7) the ReduceRank rule ----
+    int kept = n;
+    if (!shrink) {
+      if (tid < n) { out_src[tid] = order[tid]; wout[tid] = 1.0; }
+    } else {
+      kept = ell - 1;
+      const double l0 = lam[order[0]], lm1 = lam[order[ell - 1]];
+      double delta = lm1;
+      int src_last = -1;
+      if (p.rule == RULE_SS) {
+        delta = 0.0;
+        if (lm1 > 1e-12 * l0) { delta = lam[order[ell - 2]]; src_last = ell - 1; }
+      }
+      double rem = 0.0;
+      if (tid < n) {
+        const int j = tid;
+        const double lj = lam[order[j]];
+        double sp2;
+        if (p.rule == RULE_SS) {
+          if (src_last >= 0) sp2 = (j < ell - 2) ? lj : (j == ell - 1 ? lj + delta : 0.0);
+          else sp2 = (j < ell - 1) ? lj : 0.0;
+        } else if (j >= ell - 1) {
+          sp2 = 0.0;
+        } else if (p.rule == RULE_ISVD || j < ell - p.m) {
+          sp2 = lj;
+        } else {
+          sp2 = fmax(lj - delta, 0.0);
+        }
+        rem = lj - sp2;
+        int orow = j;
+        if (src_last >= 0) orow = (j == ell - 1) ? ell - 2 : (j == ell - 2 ? -1 : j);
+        if (orow >= 0 && orow < kept) {
+          out_src[orow] = order[j];
+          wout[orow] = (lj > 0.0) ? sqrt(sp2) / sqrt(lj) : 0.0;
+        }
+      }
+      rem = block_sum(rem, s_red);
+      if (tid == 0) { s_stat[1] += delta; s_stat[2] += rem; s_stat[3] += 1.0; }
+    }
+    __syncthreads();
+    // ---- (8) W^T (rows: Bf rows = state rows, then the new row k; cols: outputs) ----
+    for (int e = tid; e < n * kept; e += kPrThreads) {
+      const int j = e % kept, ci = e / kept;          // ci: sorted coordinate, or kc (the tip)
+      const int src = slot_src[out_src[j]];
+      double x;
+      if (src >= 0) {
+        if (ci == kc) x = 1.0;
+        else if (pidx[ci] < 0) x = 0.0;
+        else {
+          const int q = pidx[ci];
+          x = zhat[q] / (rt[src] - (dpol[q] - rp[src]));   // z^_q / (lambda_m - d_q)
+        }
+      } else {
+        x = (ci == ~src) ? 1.0 : 0.0;
+      }
+      const int row = (ci == kc) ? k : perm[ci];
+      WtT[row * ws + j] = x;
+    }
+    if (drop >= 0)
+      for (int j = tid; j < kept; j += kPrThreads) WtT[drop * ws + j] = 0.0;
+    __syncthreads();
+    // Givens deflations (reverse order), the output norms and scales: thread per output
+    if (tid < kept) {
+      const int j = tid;
+      for (int r = nrot - 1; r >= 0; --r) {
+        double* xa = &WtT[perm[rot_a[r]] * ws + j];
+        double* xb = &WtT[perm[rot_b[r]] * ws + j];
+        const double a = *xa, b = *xb, c = rc[r], s = rs[r];
+        *xa = c * a - s * b;
+        *xb = s * a + c * b;
+      }
+      double nn = 0.0;
+      for (int r = 0; r <= k; ++r) nn = fma(WtT[r * ws + j], WtT[r * ws + j], nn);
+      sclo[j] = (nn > 0.0) ? wout[j] / sqrt(nn) : 0.0;
+    }
+    __syncthreads();
+    // the CFD pending-shrink weights scale the state rows
+    if (lazy)
+      for (int e = tid; e < k * kept; e += kPrThreads) {
+        const int r = e / kept, j = e % kept;
+        WtT[r * ws + j] *= scl[r];
+      }
+    __syncthreads();
+    // ---- (9) reconstruct the slice: Sn[j][c] = sclo_j sum_r WtT[r][j] Bf[r][c] ----
+    for (int cb = 0; cb < lds; cb += kPrColsPass) {
+      const int c = cb + 4 * cgp;
+      if (c >= lds || 8 * rg >= Lo.ellp) continue;
+      double acc[8][4];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int h = 0; h < 4; ++h) acc[q][h] = 0.0;
+      if (8 * rg < kept) {
+        for (int r = 0; r <= k; ++r) {
+          const double* br = (r < k) ? (S + r * lds + c) : (arow + c);
+          const double2 b01 = *reinterpret_cast<const double2*>(br);
+          const double2 b23 = *reinterpret_cast<const double2*>(br + 2);
+          const double* wr = WtT + r * ws + 8 * rg;
+#pragma unroll
+          for (int q2 = 0; q2 < 4; ++q2) {
+            const double2 w = *reinterpret_cast<const double2*>(wr + 2 * q2);
+            acc[2 * q2][0] = fma(w.x, b01.x, acc[2 * q2][0]);
+            acc[2 * q2][1] = fma(w.x, b01.y, acc[2 * q2][1]);
+            acc[2 * q2][2] = fma(w.x, b23.x, acc[2 * q2][2]);
+            acc[2 * q2][3] = fma(w.x, b23.y, acc[2 * q2][3]);
+            acc[2 * q2 + 1][0] = fma(w.y, b01.x, acc[2 * q2 + 1][0]);
+            acc[2 * q2 + 1][1] = fma(w.y, b01.y, acc[2 * q2 + 1][1]);
+            acc[2 * q2 + 1][2] = fma(w.y, b23.x, acc[2 * q2 + 1][2]);
+            acc[2 * q2 + 1][3] = fma(w.y, b23.y, acc[2 * q2 + 1][3]);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int j = 8 * rg + q;
+        const double sc = (j < kept) ? sclo[j] : 0.0;
+        double* o = Sn + j * lds + c;
+        *reinterpret_cast<double2*>(o) = make_double2(sc * acc[q][0], sc * acc[q][1]);
+        *reinterpret_cast<double2*>(o + 2) = make_double2(sc * acc[q][2], sc * acc[q][3]);
+      }
+    }
+    __syncthreads();
+    k = kept;
+    cur ^= 1;
+  }
+  // ---- write back: fp64 state, its fp32 copy (the shard buffer fd_sketch reads), stats ----
+  const double* S = Sbuf[cur];
+  for (int e = tid; e < ell * lds; e += kPrThreads) {
+    const int r = e / lds, c = e - r * lds;
+    if (c >= ncol) continue;
+    const double v = (r < k) ? S[e] : 0.0;
+    J.state[(int64_t)r * p.ldb + c0 + c] = v;
+    J.dst[(int64_t)r * p.ldb + c0 + c] = (float)v;
+  }
+  if (crank == C - 1)   // padding columns d..ldb-1 of the fp32 rows stay zero
+    for (int e = tid; e < ell * (int)(p.ldb - d); e += kPrThreads) {
+      const int r = e / (int)(p.ldb - d), c = d + e % (int)(p.ldb - d);
+      J.dst[(int64_t)r * p.ldb + c] = 0.f;
+    }
+  bad = __syncthreads_or(bad);
+  if (tid == 0) {
+    if (bad) atomicOr(nonfinite, 1);
+    if (crank == 0) {
+      J.stats->frob += s_stat[0];
+      J.stats->delta += s_stat[1];
+      J.stats->removed += s_stat[2];
+      J.stats->shrinks += s_stat[3];
+    }
+  }
+  if (C > 1) cluster.sync();   // no CTA exits while a peer may still read its shared memory
+}
+
+cudaError_t launch_perrow(const RowJob* dev_jobs, int count, const Params& p, int lazy, int* nonfinite,
+                          cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  const int C = perrow_cluster(p.ell, p.d);
+  if (C <= 0) return cudaErrorInvalidValue;
+  const int smem = (int)perrow_smem_bytes(p.ell, p.d, C);
+  static AttrOnce once;
+  if (cudaError_t e = once.ensure(perrow_kernel, smem); e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(count * C));
+  cfg.blockDim = dim3(kPrThreads);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, perrow_kernel, dev_jobs, p, C, lazy, nonfinite);
+}
+
+}  // namespace fdk

@@ -169,12 +169,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) gram_tc_kernel(const Prob* __re
 template <int NP>
 static cudaError_t launch_gram_tc_t(const Prob* dev_probs, int count, const Params& p, cudaStream_t s) {
   constexpr int dyn = 4 * kTile + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gram_tc_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static AttrOnce once;
+  if (cudaError_t e = once.ensure(gram_tc_kernel<NP>, dyn); e != cudaSuccess) return e;
   const int grid = count < kNumSMs ? count : kNumSMs;
   gram_tc_kernel<NP><<<grid, kTcThreads, dyn, s>>>(dev_probs, count, p);
   return cudaGetLastError();
@@ -369,12 +365,8 @@ cudaError_t launch_recon_tc(const Prob* dev_probs, int count, int nmax, const Pa
   (void)nmax;
   if (count <= 0) return cudaSuccess;
   constexpr int dyn = 2 * kRStage + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(recon_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static AttrOnce once;
+  if (cudaError_t e = once.ensure(recon_tc_kernel, dyn); e != cudaSuccess) return e;
   const int grid = count < kNumSMs ? count : kNumSMs;
   recon_tc_kernel<<<grid, kTcThreads, dyn, s>>>(dev_probs, count, p);
   return cudaGetLastError();

@@ -395,12 +395,8 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
 template <int NM>
 static cudaError_t launch_trd_t(const Prob* dev_probs, int count, const Params& p, cudaStream_t s) {
   constexpr int dyn = TrdCfg<NM>::NB * 32 * 32 * (int)sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(trd_kernel<NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static AttrOnce once;
+  if (cudaError_t e = once.ensure(trd_kernel<NM>, dyn); e != cudaSuccess) return e;
   const int grid = count < kNumSMs ? count : kNumSMs;
   trd_kernel<NM><<<grid, TrdCfg<NM>::kThreads, dyn, s>>>(dev_probs, count, p);
   return cudaGetLastError();

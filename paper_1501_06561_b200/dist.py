@@ -15,11 +15,20 @@ import torch.distributed as dist
 STAT_KEYS = ("frob_sq", "delta_total", "removed_mass", "n_shrinks", "rows_seen")
 
 
-def local_range(n: int, rank: int, world: int):
-    """Contiguous row range of `rank` (sizes floor(n/world) + (rank < n mod world))."""
-    q, r = divmod(n, world)
-    start = rank * q + min(rank, r)
-    return start, start + q + (1 if rank < r else 0)
+def local_range(n: int, rank: int, world: int, n_shards_total: int | None = None):
+    """Contiguous row range of `rank`: the rows of the global shards
+    [rank P_local, (rank+1) P_local), P_local = P_total / world, with the global
+    shard sizes floor(n/P_total) + (s < n mod P_total) of reading C10.  The rank's
+    fd_append_rows then splits its range into exactly those P_local shards, so the
+    g-rank DAG is the 1-GPU DAG at the same P_total for every n (not only when
+    P_total divides n).  P_total defaults to world (one shard per rank)."""
+    P = world if n_shards_total is None else int(n_shards_total)
+    if P < 1 or P % world:
+        raise ValueError(f"P_total={P} must be a positive multiple of world={world}")
+    q, r = divmod(n, P)
+    pl = P // world
+    s0, s1 = rank * pl, (rank + 1) * pl
+    return s0 * q + min(s0, r), s1 * q + min(s1, r)
 
 
 def gather_and_merge(B_local, stats_local: dict, merge_fn, group=None):
@@ -53,12 +62,15 @@ def dist_sketch(sketcher, group=None):
     return gather_and_merge(B_local, st, lambda S: sketcher.merge(S, stats=True), group)
 
 
-def reduce_gram(AtA, group=None):
+def reduce_gram(AtA, group=None, frob_fn=None):
     """Sum the per-rank d x d fp64 partial Grams in place (one all_reduce);
-    returns (AtA, ||A||_F^2 = trace(AtA))."""
+    returns (AtA, ||A||_F^2 = trace(AtA)).  `frob_fn` computes the trace (libfd's
+    fd_cov_frob_from_gram for device Grams; the CPU gloo tests pass their own)."""
     if dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(AtA, group=group)
-    return AtA, float(torch.diagonal(AtA).sum().item())
+    if frob_fn is None:
+        from . import cov_frob_from_gram as frob_fn
+    return AtA, float(frob_fn(AtA))
 
 
 def dist_cov_err(A_local, B, group=None, proj_k=0):

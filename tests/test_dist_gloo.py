@@ -34,7 +34,7 @@ def _worker(rank, port, P_total, ell, variant, out_dir):
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
     try:
         A = fdgen.host_rows(fdgen.config("c1"))
-        r0, r1 = local_range(A.shape[0], rank, WORLD)
+        r0, r1 = local_range(A.shape[0], rank, WORLD, P_total)
         # per-rank sketch of its rows with P_total / world shards (oracle stands in
         # for fd_append_rows + fd_sketch on the GPU)
         r = oracle.sketch(A[r0:r1], ell, variant, n_shards=P_total // WORLD)
@@ -47,7 +47,7 @@ def _worker(rank, port, P_total, ell, variant, out_dir):
 
         B, tot = gather_and_merge(torch.from_numpy(r.B), st, merge_fn)
         AtA_p, _ = oracle.gram(A[r0:r1])
-        AtA, frob = reduce_gram(torch.from_numpy(AtA_p))
+        AtA, frob = reduce_gram(torch.from_numpy(AtA_p), frob_fn=lambda G: torch.diagonal(G).sum().item())
         np.save(os.path.join(out_dir, f"B{rank}.npy"), B.numpy())
         np.save(os.path.join(out_dir, f"G{rank}.npy"), AtA.numpy())
         np.save(os.path.join(out_dir, f"s{rank}.npy"),
@@ -66,9 +66,35 @@ def test_local_range_partition():
             assert max(b - a for a, b in rs) - min(b - a for a, b in rs) <= 1
 
 
+def _split(n, P):
+    q, r = divmod(n, P)
+    return [q + (1 if s < r else 0) for s in range(P)]
+
+
+@pytest.mark.parametrize("n,P,g", [(8388608, 2368, 8), (8388608, 2368, 2), (2003, 4, 2), (60000, 296, 8),
+                                   (7, 8, 4), (1000, 24, 3)])
+def test_local_range_is_shard_aligned(n, P, g):
+    """Each rank's rows are exactly the global shards [r P/g, (r+1) P/g) of the
+    1-GPU split (reading C10), and fd_append_rows' split of the rank's range into
+    P/g shards reproduces their sizes: the g-rank DAG is the 1-GPU DAG at P_total
+    also when P_total does not divide n."""
+    glob = _split(n, P)
+    off = 0
+    for r in range(g):
+        a, b = local_range(n, r, g, P)
+        assert a == off
+        loc = _split(b - a, P // g)
+        assert loc == glob[r * (P // g):(r + 1) * (P // g)]
+        off = b
+    assert off == n
+    with pytest.raises(ValueError):
+        local_range(n, 0, g, P + 1 if (P + 1) % g else P + 2)
+
+
 @pytest.mark.parametrize("variant", ["fast_fd", "alpha_fd"])
-def test_two_rank_gloo_matches_single_process(tmp_path, variant):
-    P_total, ell = 4, 16
+@pytest.mark.parametrize("P_total", [4, 6])
+def test_two_rank_gloo_matches_single_process(tmp_path, variant, P_total):
+    ell = 16
     mp.start_processes(_worker, args=(_port(), P_total, ell, variant, str(tmp_path)), nprocs=WORLD,
                        start_method="spawn", join=True)
     A = fdgen.host_rows(fdgen.config("c1"))
