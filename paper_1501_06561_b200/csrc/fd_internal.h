@@ -50,7 +50,7 @@ struct RowJob {
   int k_in;       // rows in the state at entry (occupancy)
   int pad;
 };
-constexpr size_t kPrSmemMax = 200 * 1024;
+constexpr size_t kPrSmemMax = 225 * 1024;
 
 // Ingest of one shard in one round: copy nrows rows of the user's A into the
 // shard buffer (row stride ldb, zero-padded to ldb columns), accumulate ||a||^2.

@@ -100,71 +100,124 @@ __device__ __forceinline__ double wsum(double v) {
   return v;
 }
 
-// One secular root (whole warp; lanes over the terms).  Poles dp[0..K-1] strictly
-// decreasing, z2 = z^2 > 0, tip rho, zn = ||z||.  Root m lies in (dp[m], dp[m-1])
-// (dp[-1] = +inf, dp[K] = -inf).  Returns lambda = p + tau with p the nearer pole
-// (tau then carries the root's distance to it to full relative accuracy).
-// Safeguarded Newton on g(tau) = tau f(p + tau), which has no pole at tau = 0,
-// started from the root of the model with the other poles frozen; bisection on the
-// bracket (sign of f) whenever a step leaves it.
-__device__ void secular_root(int m, int K, const double* dp, const double* z2, double rho, double zn, int lane,
-                             double& p_out, double& t_out) {
-  int ip;
-  double p, lo, hi;
-  if (m == 0) {
-    ip = 0;
-    p = dp[0];
-    lo = 0.0;
-    hi = (fmax(rho - p, 0.0) + zn) * (1.0 + 8.0 * DBL_EPSILON) + DBL_MIN;
-  } else if (m == K) {
-    ip = K - 1;
-    p = dp[K - 1];
-    hi = 0.0;
-    lo = -(fmax(p - rho, 0.0) + zn) * (1.0 + 8.0 * DBL_EPSILON) - DBL_MIN;
-  } else {
-    const double a = dp[m], b = dp[m - 1];
-    const double mid = 0.5 * (a + b);
-    double s = 0.0;
-    for (int i = lane; i < K; i += 32) s += z2[i] / (mid - dp[i]);
-    s = wsum(s);
-    if (mid - rho - s >= 0.0) { ip = m; p = a; lo = 0.0; hi = mid - a; }
-    else { ip = m - 1; p = b; lo = mid - b; hi = 0.0; }
+// 1/x in fp64: the hardware approximation (rcp.approx.ftz.f64) + two Newton steps
+// (quadratic: ~2^-20 -> 2^-40 -> full precision); x is never 0 here (the poles and
+// roots are separated by the deflation tolerance).
+__device__ __forceinline__ double rcp64(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// sum over the LW lanes of a lane group (xor butterfly: every lane gets the same bits)
+template <int LW>
+__device__ __forceinline__ double gsum(double v) {
+#pragma unroll
+  for (int o = LW / 2; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// Secular roots, one per group of LW lanes (the lanes split the terms).  Poles
+// dp[0..K-1] strictly decreasing, z2 = z^2 > 0, tip rho, zn = ||z||.  Root m lies in
+// (dp[m], dp[m-1]) (dp[-1] = +inf, dp[K] = -inf); groups with has == false idle.
+// Returns lambda = p + tau with p the nearer pole (tau then carries the root's
+// distance to it to full relative accuracy).  Safeguarded Newton on
+// g(tau) = tau f(p + tau), which has no pole at tau = 0, started from the root of the
+// model with the other poles frozen; bisection on the bracket (sign of f) whenever a
+// step leaves it.  The whole warp iterates until its last group has converged.
+template <int LW>
+__device__ void secular_roots(int m, bool has, int K, const double* dp, const double* z2, double rho, double zn,
+                              int gl, double& p_out, double& t_out) {
+  int ip = 0;
+  double p = 0.0, lo = 0.0, hi = 0.0;
+  const bool interior = has && m > 0 && m < K;
+  const double mid = interior ? 0.5 * (dp[m] + dp[m - 1]) : 0.0;
+  double sm = 0.0;
+  if (interior)
+    for (int i = gl; i < K; i += LW) sm = fma(z2[i], rcp64(mid - dp[i]), sm);
+  sm = gsum<LW>(sm);
+  if (has) {
+    if (m == 0) {
+      ip = 0; p = dp[0]; lo = 0.0;
+      hi = (fmax(rho - p, 0.0) + zn) * (1.0 + 8.0 * DBL_EPSILON) + DBL_MIN;
+    } else if (m == K) {
+      ip = K - 1; p = dp[K - 1]; hi = 0.0;
+      lo = -(fmax(p - rho, 0.0) + zn) * (1.0 + 8.0 * DBL_EPSILON) - DBL_MIN;
+    } else if (mid - rho - sm >= 0.0) {
+      ip = m; p = dp[m]; lo = 0.0; hi = mid - p;
+    } else {
+      ip = m - 1; p = dp[m - 1]; lo = mid - p; hi = 0.0;
+    }
   }
   double s0 = 0.0;
-  for (int i = lane; i < K; i += 32)
-    if (i != ip) s0 += z2[i] / (p - dp[i]);
-  s0 = wsum(s0);
-  const double zp = z2[ip];
-  const double B = p - rho - s0;          // f(p + t) ~ t + B - zp / t
-  const double disc = sqrt(B * B + 4.0 * zp);
-  double t;
-  if (hi > 0.0) t = (B <= 0.0) ? 0.5 * (disc - B) : 2.0 * zp / (B + disc);
-  else t = (B >= 0.0) ? -0.5 * (B + disc) : -2.0 * zp / (disc - B);
-  if (!(t > lo && t < hi)) t = 0.5 * (lo + hi);
+  if (has)
+    for (int i = gl; i < K; i += LW)
+      if (i != ip) s0 = fma(z2[i], rcp64(p - dp[i]), s0);
+  s0 = gsum<LW>(s0);
+  double t = 0.0;
+  bool done = !has;
+  double zp = 0.0;
+  if (has) {
+    zp = z2[ip];
+    const double B = p - rho - s0;          // f(p + t) ~ t + B - zp / t
+    const double disc = sqrt(B * B + 4.0 * zp);
+    if (hi > 0.0) t = (B <= 0.0) ? 0.5 * (disc - B) : 2.0 * zp / (B + disc);
+    else t = (B >= 0.0) ? -0.5 * (B + disc) : -2.0 * zp / (disc - B);
+    if (!(t > lo && t < hi)) t = 0.5 * (lo + hi);
+  }
   for (int it = 0; it < 80; ++it) {
+    if (!__any_sync(kFull, !done)) break;
     double s1 = 0.0, s2 = 0.0;
-    for (int i = lane; i < K; i += 32) {
-      if (i == ip) continue;
-      const double r = 1.0 / (t - (dp[i] - p));
-      const double q = z2[i] * r;
-      s1 += q;
-      s2 = fma(q, r, s2);
-    }
-    s1 = wsum(s1);
-    s2 = wsum(s2);
+    if (!done)
+      for (int i = gl; i < K; i += LW) {
+        if (i == ip) continue;
+        const double r = rcp64(t - (dp[i] - p));
+        const double q = z2[i] * r;
+        s1 += q;
+        s2 = fma(q, r, s2);
+      }
+    s1 = gsum<LW>(s1);
+    s2 = gsum<LW>(s2);
+    if (done) continue;
     const double f = (p + t - rho) - zp / t - s1;
+    if (f == 0.0) { done = true; continue; }   // t is a root
     if (f < 0.0) lo = t; else hi = t;
     const double g = t * (p + t - rho) - zp - t * s1;
     const double gp = (p + 2.0 * t - rho) - s1 + t * s2;
-    double tn = t - g / gp;
-    if (!(tn > lo && tn < hi)) tn = 0.5 * (lo + hi);
-    const double step = fabs(tn - t);
-    t = tn;
-    if (f == 0.0 || step <= 2.0 * DBL_EPSILON * fabs(t) || hi - lo <= 4.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)))
-      break;
+    const double dt = g / gp;
+    const double tn = t - dt;
+    if (fabs(dt) <= 2.0 * DBL_EPSILON * fabs(t)) {   // converged (a last step may round onto the bracket)
+      if (tn > lo && tn < hi) t = tn;
+      done = true;
+      continue;
+    }
+    t = (tn > lo && tn < hi) ? tn : 0.5 * (lo + hi);
+    if (hi - lo <= 4.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi))) done = true;
   }
   p_out = p;
   t_out = t;
+}
+
+// the roots of one CTA (m = crank, crank + C, ...), LW lanes per root
+template <int LW>
+__device__ void cta_roots(int K, int C, int crank, const double* dp, const double* z2, double rho, double zn,
+                          double* rp, double* rt) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int G = 32 / LW;                          // groups per warp
+  const int nloc = (K + 1 - crank + C - 1) / C;       // roots this CTA owns
+  const int grp = warp * G + lane / LW;
+  for (int base = 0; base < nloc; base += (kPrThreads / 32) * G) {
+    if (base + warp * G >= nloc) break;               // warp-uniform
+    const int li = base + grp;
+    const bool has = li < nloc;
+    const int m = crank + C * li;
+    double pp, tt;
+    secular_roots<LW>(has ? m : 0, has, K, dp, z2, rho, zn, lane % LW, pp, tt);
+    if (has && lane % LW == 0) { rp[m] = pp; rt[m] = tt; }
+  }
 }
 
 // block-wide sum of one double per thread (kPrThreads), result in every thread
@@ -254,6 +307,11 @@ perrow_kernel(const RowJob* __restrict__ jobs, Params p, int C, int lazy, int* _
   float pre = 0.f;                      // prefetched element (column c0 + tid) of the next row
   if (J.nrows > 0 && tid < ncol) pre = J.src[c0 + tid];
 
+  const bool tr = p.dbg && blockIdx.x == 0 && tid == 0;   // phase clocks (FD_DEBUG_EIG)
+  long long t_ph = tr ? clock64() : 0;
+  auto phase = [&](int i) {
+    if (tr) { const long long c = clock64(); p.dbg[i] += c - t_ph; t_ph = c; }
+  };
   for (int64_t t = 0; t < J.nrows; ++t) {
     const double* S = Sbuf[cur];
     double* Sn = Sbuf[cur ^ 1];
@@ -308,18 +366,24 @@ perrow_kernel(const RowJob* __restrict__ jobs, Params p, int C, int lazy, int* _
         if (lane == 0) pt[2 * kPrMaxRows] = na;
       }
     }
+    phase(0);
     // ---- (2) cluster-wide sums, fixed order (identical in every CTA) ----
     if (C > 1) cluster.sync(); else __syncthreads();
+    phase(1);
     for (int e = tid; e <= 2 * kPrMaxRows; e += kPrThreads) {
       const bool used = (e < k) || (e >= kPrMaxRows && e < kPrMaxRows + k) || e == 2 * kPrMaxRows;
+      double v[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) v[r] = (used && r < C) ? (r == crank ? pt : cluster.map_shared_rank(pt, r))[e] : 0.0;
       double s = 0.0;
-      if (used)
-        for (int r = 0; r < C; ++r) s += (r == crank ? pt : cluster.map_shared_rank(pt, r))[e];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) s += v[r];
       full[e] = s;
     }
     __syncthreads();
     const double rho = full[2 * kPrMaxRows];
     if (tid == 0) s_stat[0] += rho;
+    phase(2);
     // ---- (3) Compensative FD: ReduceRank of the full pending buffer first (C27).  Its
     //      Gram is diag(||b_j||^2); the FD rule gives every state row a weight ----
     if (tid <= ell) scl[tid] = 1.0;
@@ -428,6 +492,7 @@ perrow_kernel(const RowJob* __restrict__ jobs, Params p, int C, int lazy, int* _
     __syncthreads();
     const int K = misc[0];
     const int nrot = misc[1];
+    phase(3);
     // ---- (5) secular roots, split over the cluster: root m -> CTA m % C ----
     {
       const int nroots = K + 1;
@@ -438,12 +503,12 @@ perrow_kernel(const RowJob* __restrict__ jobs, Params p, int C, int lazy, int* _
         if (tid < K) zs = z2[tid];
         zs = block_sum(zs, s_red);
         const double zn = sqrt(zs);
-        for (int m = crank + C * warp; m < nroots; m += C * (kPrThreads / 32)) {
-          double pp, tt;
-          secular_root(m, K, dpol, z2, rho, zn, lane, pp, tt);
-          if (lane == 0) { rp[m] = pp; rt[m] = tt; }
-        }
+        if (K <= 16) cta_roots<4>(K, C, crank, dpol, z2, rho, zn, rp, rt);
+        else if (K <= 32) cta_roots<8>(K, C, crank, dpol, z2, rho, zn, rp, rt);
+        else if (K <= 64) cta_roots<16>(K, C, crank, dpol, z2, rho, zn, rp, rt);
+        else cta_roots<32>(K, C, crank, dpol, z2, rho, zn, rp, rt);
       }
+      phase(4);
       if (C > 1) {
         cluster.sync();
         if (K > 0)
@@ -457,13 +522,19 @@ perrow_kernel(const RowJob* __restrict__ jobs, Params p, int C, int lazy, int* _
       }
       __syncthreads();
     }
+    phase(5);
     // ---- (6) Loewner z^_q = sign(z_q) sqrt(-(d_q - l_q)(d_q - l_K) prod_{m != q} (d_q - l_m)/(d_q - d_m)) ----
-    if (tid < K) {
-      const double di = dpol[tid];
-      double prod = -((di - rp[tid]) - rt[tid]) * ((di - rp[K]) - rt[K]);
-      for (int m = 0; m < K; ++m)
-        if (m != tid) prod *= ((di - rp[m]) - rt[m]) / (di - dpol[m]);
-      zhat[tid] = copysign(sqrt(fmax(prod, 0.0)), zsort[coord[tid]]);
+    {   // two threads per pole (even / odd m), combined by one shuffle
+      const int q = tid >> 1, h = tid & 1;
+      double prod = 1.0;
+      if (q < K) {
+        const double di = dpol[q];
+        if (h == 0) prod = -((di - rp[q]) - rt[q]) * ((di - rp[K]) - rt[K]);
+        for (int m = h; m < K; m += 2)
+          if (m != q) prod *= ((di - rp[m]) - rt[m]) * rcp64(di - dpol[m]);
+      }
+      prod *= __shfl_xor_sync(kFull, prod, 1);
+      if (q < K && h == 0) zhat[q] = copysign(sqrt(fmax(prod, 0.0)), zsort[coord[q]]);
     }
     // eigen slots: roots 0..K, then the deflated coordinates (prefix count)
     if (tid <= K) { slot_src[tid] = tid; lam[tid] = fmax(rp[tid] + rt[tid], 0.0); }
@@ -522,6 +593,7 @@ perrow_kernel(const RowJob* __restrict__ jobs, Params p, int C, int lazy, int* _
       if (tid == 0) { s_stat[1] += delta; s_stat[2] += rem; s_stat[3] += 1.0; }
     }
     __syncthreads();
+    phase(6);
     // ---- (8) W^T (rows: Bf rows = state rows, then the new row k; cols: outputs) ----
     for (int e = tid; e < n * kept; e += kPrThreads) {
       const int j = e % kept, ci = e / kept;          // ci: sorted coordinate, or kc (the tip)
@@ -532,7 +604,7 @@ perrow_kernel(const RowJob* __restrict__ jobs, Params p, int C, int lazy, int* _
         else if (pidx[ci] < 0) x = 0.0;
         else {
           const int q = pidx[ci];
-          x = zhat[q] / (rt[src] - (dpol[q] - rp[src]));   // z^_q / (lambda_m - d_q)
+          x = zhat[q] * rcp64(rt[src] - (dpol[q] - rp[src]));   // z^_q / (lambda_m - d_q)
         }
       } else {
         x = (ci == ~src) ? 1.0 : 0.0;
@@ -565,6 +637,7 @@ perrow_kernel(const RowJob* __restrict__ jobs, Params p, int C, int lazy, int* _
         WtT[r * ws + j] *= scl[r];
       }
     __syncthreads();
+    phase(7);
     // ---- (9) reconstruct the slice: Sn[j][c] = sclo_j sum_r WtT[r][j] Bf[r][c] ----
     for (int cb = 0; cb < lds; cb += kPrColsPass) {
       const int c = cb + 4 * cgp;
@@ -604,6 +677,8 @@ perrow_kernel(const RowJob* __restrict__ jobs, Params p, int C, int lazy, int* _
       }
     }
     __syncthreads();
+    phase(8);
+    if (tr) p.dbg[9] += 1;
     k = kept;
     cur ^= 1;
   }

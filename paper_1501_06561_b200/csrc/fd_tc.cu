@@ -22,6 +22,7 @@ namespace {
 
 constexpr int kTcThreads = 256;
 constexpr int kTile = 256 * 128;   // bytes of one 256-row x 32-value SW128 tile
+constexpr int kAccs = 4;           // K-split accumulators of the NP = 128 Gram (4 x 128 TMEM columns)
 
 __device__ __forceinline__ const float* row_ptr(const Prob& P, int r, int64_t ldb) {
   if (r < P.rows0) return P.src0 + (int64_t)r * ldb;
@@ -105,12 +106,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) gram_tc_kernel(const Prob* __re
         const uint32_t hi = tc::smem_u32(sm + (2 * b) * kTile), lo = tc::smem_u32(sm + (2 * b + 1) * kTile);
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
-          const uint32_t acc = (kc > 0 || ks > 0) ? 1u : 0u;
+          // NP = 128: K-chunks rotate over kAccs accumulators (TMEM columns 128 a), summed
+          // in fp32 registers by the epilogue: each accumulates 1/kAccs of the K range, so
+          // the truncating fp32 accumulation of the MMAs (~0.5 ulp of the running sum per
+          // step) biases the Gram kAccs^2 times less per accumulator, kAccs times less in total
+          const uint32_t acc = ((NP == 128 ? kc >= kAccs : kc > 0) || ks > 0) ? 1u : 0u;
+          const uint32_t ta = (NP == 128) ? tbase + 128u * (uint32_t)(kc % kAccs) : tbase;
           const uint32_t ko = ks * 32;  // 8 tf32 = 32 bytes along K
           // tile 0: rows [0,128) x cols [0,128)
-          tc::mma_tf32(tbase, tc::desc_k_sw128(hi + ko), tc::desc_k_sw128(hi + ko), id0, acc);
-          tc::mma_tf32(tbase, tc::desc_k_sw128(hi + ko), tc::desc_k_sw128(lo + ko), id0, 1u);
-          tc::mma_tf32(tbase, tc::desc_k_sw128(lo + ko), tc::desc_k_sw128(hi + ko), id0, 1u);
+          tc::mma_tf32(ta, tc::desc_k_sw128(hi + ko), tc::desc_k_sw128(hi + ko), id0, acc);
+          tc::mma_tf32(ta, tc::desc_k_sw128(hi + ko), tc::desc_k_sw128(lo + ko), id0, 1u);
+          tc::mma_tf32(ta, tc::desc_k_sw128(lo + ko), tc::desc_k_sw128(hi + ko), id0, 1u);
           if (NP == 256) {  // tile 1: rows [128,256) x cols [0,256), TMEM columns [128, 384)
             tc::mma_tf32(tbase + 128, tc::desc_k_sw128(hi + 16384 + ko), tc::desc_k_sw128(hi + ko), id1, acc);
             tc::mma_tf32(tbase + 128, tc::desc_k_sw128(hi + 16384 + ko), tc::desc_k_sw128(lo + ko), id1, 1u);
@@ -151,6 +157,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) gram_tc_kernel(const Prob* __re
         for (int c0 = 0; c0 < ncols; c0 += 16) {
           float v[16];
           tc::tmem_ld16(lanebase + (t == 0 ? 0 : 128) + c0, v);
+          if (NP == 128) {
+            for (int a = 1; a < kAccs && a < nk; ++a) {
+              float u[16];
+              tc::tmem_ld16(lanebase + 128 * a + c0, u);
+#pragma unroll
+              for (int q = 0; q < 16; ++q) v[q] += u[q];
+            }
+          }
           if (row < N) {
             float* dst = G + (int64_t)row * p.ldg + c0;
 #pragma unroll
