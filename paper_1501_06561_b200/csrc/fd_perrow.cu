@@ -89,7 +89,7 @@ __host__ __device__ inline PrLayout pr_layout(int ell, int dc) {
   L.rc = take(v);                          // Givens deflations
   L.rs = take(v);
   L.WtT = take((size_t)(ell + 1) * L.ws * 8);   // rows: Bf rows (state rows, then a); cols: outputs
-  L.ints = take((size_t)9 * (ell + 2) * 4 + 16 * 4);
+  L.ints = take((size_t)9 * (ell + 2) * 4 + 32 * 4);
   L.total = off;
   return L;
 }
@@ -118,6 +118,15 @@ __device__ __forceinline__ double gsum(double v) {
 #pragma unroll
   for (int o = LW / 2; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
   return v;
+}
+template <int LW>
+__device__ __forceinline__ void gsum2(double& a, double& b) {
+#pragma unroll
+  for (int o = LW / 2; o > 0; o >>= 1) {
+    const double x = __shfl_xor_sync(kFull, a, o), y = __shfl_xor_sync(kFull, b, o);
+    a += x;
+    b += y;
+  }
 }
 
 // Secular roots, one per group of LW lanes (the lanes split the terms).  Poles
@@ -170,24 +179,35 @@ __device__ void secular_roots(int m, bool has, int K, const double* dp, const do
   }
   for (int it = 0; it < 80; ++it) {
     if (!__any_sync(kFull, !done)) break;
-    double s1 = 0.0, s2 = 0.0;
-    if (!done)
-      for (int i = gl; i < K; i += LW) {
-        if (i == ip) continue;
+    double s1 = 0.0, s2 = 0.0, s1b = 0.0, s2b = 0.0;
+    if (!done) {
+      int i = gl;
+      for (; i + LW < K; i += 2 * LW) {     // two independent reciprocal chains per step
+        const double ra = (i == ip) ? 0.0 : rcp64(t - (dp[i] - p));
+        const double rb = (i + LW == ip) ? 0.0 : rcp64(t - (dp[i + LW] - p));
+        const double qa = z2[i] * ra, qb = z2[i + LW] * rb;
+        s1 += qa;
+        s2 = fma(qa, ra, s2);
+        s1b += qb;
+        s2b = fma(qb, rb, s2b);
+      }
+      if (i < K && i != ip) {
         const double r = rcp64(t - (dp[i] - p));
         const double q = z2[i] * r;
         s1 += q;
         s2 = fma(q, r, s2);
       }
-    s1 = gsum<LW>(s1);
-    s2 = gsum<LW>(s2);
+      s1 += s1b;
+      s2 += s2b;
+    }
+    gsum2<LW>(s1, s2);
     if (done) continue;
-    const double f = (p + t - rho) - zp / t - s1;
+    const double f = (p + t - rho) - zp * rcp64(t) - s1;
     if (f == 0.0) { done = true; continue; }   // t is a root
     if (f < 0.0) lo = t; else hi = t;
     const double g = t * (p + t - rho) - zp - t * s1;
     const double gp = (p + 2.0 * t - rho) - s1 + t * s2;
-    const double dt = g / gp;
+    const double dt = g * rcp64(gp);
     const double tn = t - dt;
     if (fabs(dt) <= 2.0 * DBL_EPSILON * fabs(t)) {   // converged (a last step may round onto the bracket)
       if (tn > lo && tn < hi) t = tn;
@@ -280,7 +300,7 @@ perrow_kernel(const RowJob* __restrict__ jobs, Params p, int C, int lazy, int* _
   int* out_src = ib + 6 * E;   // output row -> eigen slot
   int* rot_a = ib + 7 * E;     // Givens deflation pairs (coordinates)
   int* rot_b = ib + 8 * E;
-  int* misc = ib + 9 * E;      // [0] K  [1] nrot  [2] close pair found
+  int* misc = ib + 9 * E;      // [0] K  [1] nrot  [4..11] / [12..19] per-warp ballot counts
   __shared__ double s_red[kPrThreads / 32];
   __shared__ double s_stat[4];  // frob, delta, removed, shrinks of this call (CTA-local copy)
 
@@ -298,7 +318,7 @@ perrow_kernel(const RowJob* __restrict__ jobs, Params p, int C, int lazy, int* _
   }
   if (tid < 4) s_stat[tid] = 0.0;
   for (int e = tid; e < 2 * kPL; e += kPrThreads) part[e] = 0.0;
-  if (tid < 16) misc[tid] = 0;
+  if (tid < 32) misc[tid] = 0;
   __syncthreads();
   if (C > 1) cluster.sync();
 
@@ -419,20 +439,31 @@ perrow_kernel(const RowJob* __restrict__ jobs, Params p, int C, int lazy, int* _
     const int kc = full_pend ? k - 1 : k;
     const int n = kc + 1;
     const bool shrink = !lazy && (n == ell);
-    // ---- (4) arrowhead coordinates: D' = scl^2 D sorted descending (ties by row) ----
-    if (tid < k && tid != drop) {
-      const double sc = scl[tid];
-      const double dv = sc * sc * fmax(full[kPrMaxRows + tid], 0.0);
-      int rk = 0;
-      for (int j = 0; j < k; ++j) {
-        if (j == drop) continue;
-        const double sj = scl[j];
-        const double dj = sj * sj * fmax(full[kPrMaxRows + j], 0.0);
-        rk += (dj > dv) || (dj == dv && j < tid);
+    // ---- (4) arrowhead coordinates: D' = scl^2 D sorted descending (ties by row).  The
+    //      state rows come out of the previous step sorted (sigma'^2 descending), so the
+    //      rank sort only runs when rounding (or CFD's pending shrink) broke the order ----
+    {
+      int unsorted = full_pend;
+      if (!full_pend && tid > 0 && tid < k)
+        unsorted = fmax(full[kPrMaxRows + tid - 1], 0.0) < fmax(full[kPrMaxRows + tid], 0.0);
+      unsorted = __syncthreads_or(unsorted);
+      if (tid < k && tid != drop) {
+        const double sc = scl[tid];
+        const double dv = sc * sc * fmax(full[kPrMaxRows + tid], 0.0);
+        int rk = tid;
+        if (unsorted) {
+          rk = 0;
+          for (int j = 0; j < k; ++j) {
+            if (j == drop) continue;
+            const double sj = scl[j];
+            const double dj = sj * sj * fmax(full[kPrMaxRows + j], 0.0);
+            rk += (dj > dv) || (dj == dv && j < tid);
+          }
+        }
+        perm[rk] = tid;
+        dsort[rk] = dv;
+        zsort[rk] = sc * full[tid];
       }
-      perm[rk] = tid;
-      dsort[rk] = dv;
-      zsort[rk] = sc * full[tid];
     }
     __syncthreads();
     double zz = 0.0;
@@ -440,16 +471,17 @@ perrow_kernel(const RowJob* __restrict__ jobs, Params p, int C, int lazy, int* _
     zz = block_sum(zz, s_red);
     const double znorm = sqrt(zz);
     const double tol = 8.0 * eps * (fmax((kc > 0) ? dsort[0] : 0.0, rho) + znorm);
-    if (tid < kc) dflag[tid] = fabs(zsort[tid]) <= tol;
+    // deflation (|z| <= tol); coincident poles: parallel detection, serial resolution (rare)
+    int dfl = (tid < kc) ? (fabs(zsort[tid]) <= tol) : 0;
+    if (tid < kc) dflag[tid] = dfl;
     __syncthreads();
-    // coincident poles (parallel detection; the chain is resolved serially, rarely)
-    if (tid < kc && !dflag[tid] && tid > 0) {
+    int close = 0;
+    if (tid < kc && !dfl && tid > 0) {
       int j = tid - 1;
       while (j >= 0 && dflag[j]) --j;
-      if (j >= 0 && dsort[j] - dsort[tid] <= tol) misc[2] = 1;
+      close = (j >= 0) && (dsort[j] - dsort[tid] <= tol);
     }
-    __syncthreads();
-    if (misc[2]) {
+    if (__syncthreads_or(close)) {
       if (tid == 0) {
         int prev = -1, nrot = 0;
         for (int i = 0; i < kc; ++i) {
@@ -470,25 +502,38 @@ perrow_kernel(const RowJob* __restrict__ jobs, Params p, int C, int lazy, int* _
           }
         }
         misc[1] = nrot;
-        misc[2] = 0;
       }
+      __syncthreads();
+      dfl = (tid < kc) ? dflag[tid] : 0;
     } else if (tid == 0) {
       misc[1] = 0;
     }
-    __syncthreads();
-    // pole indices (prefix count of the non-deflated coordinates)
-    if (tid < kc) {
-      int q = 0;
-      for (int j = 0; j < tid; ++j) q += !dflag[j];
-      pidx[tid] = dflag[tid] ? -1 : q;
-      if (!dflag[tid]) {
-        coord[q] = tid;
-        dpol[q] = dsort[tid];
-        z2[q] = zsort[tid] * zsort[tid];
+    // pole index / deflated index of every coordinate (ballot prefix counts)
+    {
+      const unsigned live = __ballot_sync(kFull, tid < kc && !dfl);
+      const unsigned dead = __ballot_sync(kFull, tid < kc && dfl);
+      if (lane == 0) { ib[9 * E + 4 + warp] = __popc(live); ib[9 * E + 12 + warp] = __popc(dead); }
+      __syncthreads();
+      int ol = 0, od = 0;
+      for (int w = 0; w < warp; ++w) { ol += ib[9 * E + 4 + w]; od += ib[9 * E + 12 + w]; }
+      const unsigned lt = (1u << lane) - 1u;
+      const int q = ol + __popc(live & lt), qd = od + __popc(dead & lt);
+      if (tid < kc) {
+        if (!dfl) {
+          pidx[tid] = q;
+          coord[q] = tid;
+          dpol[q] = dsort[tid];
+          z2[q] = zsort[tid] * zsort[tid];
+        } else {
+          pidx[tid] = -1 - qd;          // deflated: -1 - (its index among the deflated)
+        }
       }
-      if (tid == kc - 1) misc[0] = q + !dflag[tid];
+      if (tid == 0) {
+        int K = 0;
+        for (int w = 0; w < kPrThreads / 32; ++w) K += ib[9 * E + 4 + w];
+        misc[0] = K;
+      }
     }
-    if (kc == 0 && tid == 0) misc[0] = 0;
     __syncthreads();
     const int K = misc[0];
     const int nrot = misc[1];
@@ -536,20 +581,29 @@ perrow_kernel(const RowJob* __restrict__ jobs, Params p, int C, int lazy, int* _
       prod *= __shfl_xor_sync(kFull, prod, 1);
       if (q < K && h == 0) zhat[q] = copysign(sqrt(fmax(prod, 0.0)), zsort[coord[q]]);
     }
-    // eigen slots: roots 0..K, then the deflated coordinates (prefix count)
+    // eigen slots: roots 0..K (descending by interlacing), then the deflated coordinates
+    // (descending: a subsequence of the sorted diagonal)
     if (tid <= K) { slot_src[tid] = tid; lam[tid] = fmax(rp[tid] + rt[tid], 0.0); }
-    if (tid < kc && dflag[tid]) {
-      int q = 0;
-      for (int j = 0; j < tid; ++j) q += dflag[j];
-      slot_src[K + 1 + q] = ~tid;
-      lam[K + 1 + q] = fmax(dsort[tid], 0.0);
+    if (tid < kc && pidx[tid] < 0) {
+      const int qd = -1 - pidx[tid];
+      slot_src[K + 1 + qd] = ~tid;
+      lam[K + 1 + qd] = fmax(dsort[tid], 0.0);
     }
     __syncthreads();
-    // eigenvalues sorted descending, ties by slot
+    // merge of the two descending lists by binary search (ties: roots first)
     if (tid < n) {
+      const int nd = n - (K + 1);
       const double lv = lam[tid];
-      int rk = 0;
-      for (int j = 0; j < n; ++j) rk += (lam[j] > lv) || (lam[j] == lv && j < tid);
+      int rk;
+      if (tid <= K) {            // roots: + #deflated strictly greater
+        int lo = 0, hi = nd;
+        while (lo < hi) { const int md = (lo + hi) >> 1; if (lam[K + 1 + md] > lv) lo = md + 1; else hi = md; }
+        rk = tid + lo;
+      } else {                   // deflated: + #roots >= value
+        int lo = 0, hi = K + 1;
+        while (lo < hi) { const int md = (lo + hi) >> 1; if (lam[md] >= lv) lo = md + 1; else hi = md; }
+        rk = (tid - (K + 1)) + lo;
+      }
       order[rk] = tid;
     }
     __syncthreads();
@@ -594,48 +648,52 @@ perrow_kernel(const RowJob* __restrict__ jobs, Params p, int C, int lazy, int* _
     }
     __syncthreads();
     phase(6);
-    // ---- (8) W^T (rows: Bf rows = state rows, then the new row k; cols: outputs) ----
-    for (int e = tid; e < n * kept; e += kPrThreads) {
-      const int j = e % kept, ci = e / kept;          // ci: sorted coordinate, or kc (the tip)
-      const int src = slot_src[out_src[j]];
-      double x;
-      if (src >= 0) {
-        if (ci == kc) x = 1.0;
-        else if (pidx[ci] < 0) x = 0.0;
-        else {
-          const int q = pidx[ci];
-          x = zhat[q] * rcp64(rt[src] - (dpol[q] - rp[src]));   // z^_q / (lambda_m - d_q)
-        }
-      } else {
-        x = (ci == ~src) ? 1.0 : 0.0;
-      }
-      const int row = (ci == kc) ? k : perm[ci];
-      WtT[row * ws + j] = x;
-    }
-    if (drop >= 0)
-      for (int j = tid; j < kept; j += kPrThreads) WtT[drop * ws + j] = 0.0;
-    __syncthreads();
-    // Givens deflations (reverse order), the output norms and scales: thread per output
-    if (tid < kept) {
-      const int j = tid;
-      for (int r = nrot - 1; r >= 0; --r) {
-        double* xa = &WtT[perm[rot_a[r]] * ws + j];
-        double* xb = &WtT[perm[rot_b[r]] * ws + j];
-        const double a = *xa, b = *xb, c = rc[r], s = rs[r];
-        *xa = c * a - s * b;
-        *xb = s * a + c * b;
-      }
+    // ---- (8) W^T (rows: Bf rows = state rows, then the new row k; cols: outputs), two
+    //      threads per output column (coordinates split by parity), fused column norms;
+    //      CFD's pending-shrink weights scale the state rows ----
+    {
+      const int j = tid >> 1, h = tid & 1;
       double nn = 0.0;
-      for (int r = 0; r <= k; ++r) nn = fma(WtT[r * ws + j], WtT[r * ws + j], nn);
-      sclo[j] = (nn > 0.0) ? wout[j] / sqrt(nn) : 0.0;
-    }
-    __syncthreads();
-    // the CFD pending-shrink weights scale the state rows
-    if (lazy)
-      for (int e = tid; e < k * kept; e += kPrThreads) {
-        const int r = e / kept, j = e % kept;
-        WtT[r * ws + j] *= scl[r];
+      if (j < kept) {
+        const int src = slot_src[out_src[j]];
+        if (src >= 0) {
+          const double pm = rp[src], tm = rt[src];
+          for (int ci = h; ci < kc; ci += 2) {
+            const int q = pidx[ci];
+            double x = 0.0;
+            if (q >= 0) x = zhat[q] * rcp64(tm - (dpol[q] - pm));   // z^_q / (lambda_m - d_q)
+            nn = fma(x, x, nn);
+            const int row = perm[ci];
+            WtT[row * ws + j] = x * scl[row];
+          }
+          if (h == 0) { WtT[k * ws + j] = 1.0; nn += 1.0; }
+        } else {
+          const int c0d = ~src;
+          for (int ci = h; ci < kc; ci += 2) {
+            const int row = perm[ci];
+            WtT[row * ws + j] = (ci == c0d) ? scl[row] : 0.0;
+          }
+          if (h == 0) { WtT[k * ws + j] = 0.0; nn = 1.0; }
+        }
+        if (h == 0 && drop >= 0) WtT[drop * ws + j] = 0.0;
       }
+      nn += __shfl_xor_sync(kFull, nn, 1);
+      __syncwarp();
+      if (j < kept && h == 0) {
+        // Givens deflations, reverse order (rows perm[a], perm[b]; scl is 1 outside CFD's
+        // pending shrink, and then the rotated pair shares ... scl applied per row above)
+        for (int r = nrot - 1; r >= 0; --r) {
+          const int ra = perm[rot_a[r]], rb = perm[rot_b[r]];
+          const double sa = scl[ra], sb = scl[rb];
+          const double xa = (sa != 0.0) ? WtT[ra * ws + j] / sa : 0.0;
+          const double xb = (sb != 0.0) ? WtT[rb * ws + j] / sb : 0.0;
+          const double c = rc[r], sn = rs[r];
+          WtT[ra * ws + j] = (c * xa - sn * xb) * sa;
+          WtT[rb * ws + j] = (sn * xa + c * xb) * sb;
+        }
+        sclo[j] = (nn > 0.0) ? wout[j] / sqrt(nn) : 0.0;
+      }
+    }
     __syncthreads();
     phase(7);
     // ---- (9) reconstruct the slice: Sn[j][c] = sclo_j sum_r WtT[r][j] Bf[r][c] ----
