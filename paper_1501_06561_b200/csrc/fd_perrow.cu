@@ -138,8 +138,8 @@ __device__ __forceinline__ void gsum2(double& a, double& b) {
 // model with the other poles frozen; bisection on the bracket (sign of f) whenever a
 // step leaves it.  The whole warp iterates until its last group has converged.
 template <int LW>
-__device__ void secular_roots(int m, bool has, int K, const double* dp, const double* z2, double rho, double zn,
-                              int gl, double& p_out, double& t_out) {
+__device__ int secular_roots(int m, bool has, int K, const double* dp, const double* z2, double rho, double zn,
+                             int gl, double& p_out, double& t_out) {
   int ip = 0;
   double p = 0.0, lo = 0.0, hi = 0.0;
   const bool interior = has && m > 0 && m < K;
@@ -177,7 +177,8 @@ __device__ void secular_roots(int m, bool has, int K, const double* dp, const do
     else t = (B >= 0.0) ? -0.5 * (B + disc) : -2.0 * zp / (disc - B);
     if (!(t > lo && t < hi)) t = 0.5 * (lo + hi);
   }
-  for (int it = 0; it < 80; ++it) {
+  int it = 0;
+  for (; it < 80; ++it) {
     if (!__any_sync(kFull, !done)) break;
     double s1 = 0.0, s2 = 0.0, s1b = 0.0, s2b = 0.0;
     if (!done) {
@@ -219,12 +220,14 @@ __device__ void secular_roots(int m, bool has, int K, const double* dp, const do
   }
   p_out = p;
   t_out = t;
+  return it;
 }
 
 // the roots of one CTA (m = crank, crank + C, ...), LW lanes per root
 template <int LW>
-__device__ void cta_roots(int K, int C, int crank, const double* dp, const double* z2, double rho, double zn,
-                          double* rp, double* rt) {
+__device__ int cta_roots(int K, int C, int crank, const double* dp, const double* z2, double rho, double zn,
+                         double* rp, double* rt) {
+  int iters = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int G = 32 / LW;                          // groups per warp
   const int nloc = (K + 1 - crank + C - 1) / C;       // roots this CTA owns
@@ -235,9 +238,10 @@ __device__ void cta_roots(int K, int C, int crank, const double* dp, const doubl
     const bool has = li < nloc;
     const int m = crank + C * li;
     double pp, tt;
-    secular_roots<LW>(has ? m : 0, has, K, dp, z2, rho, zn, lane % LW, pp, tt);
+    iters += secular_roots<LW>(has ? m : 0, has, K, dp, z2, rho, zn, lane % LW, pp, tt);
     if (has && lane % LW == 0) { rp[m] = pp; rt[m] = tt; }
   }
+  return iters;
 }
 
 // block-wide sum of one double per thread (kPrThreads), result in every thread
@@ -548,10 +552,12 @@ perrow_kernel(const RowJob* __restrict__ jobs, Params p, int C, int lazy, int* _
         if (tid < K) zs = z2[tid];
         zs = block_sum(zs, s_red);
         const double zn = sqrt(zs);
-        if (K <= 16) cta_roots<4>(K, C, crank, dpol, z2, rho, zn, rp, rt);
-        else if (K <= 32) cta_roots<8>(K, C, crank, dpol, z2, rho, zn, rp, rt);
-        else if (K <= 64) cta_roots<16>(K, C, crank, dpol, z2, rho, zn, rp, rt);
-        else cta_roots<32>(K, C, crank, dpol, z2, rho, zn, rp, rt);
+        int its;
+        if (K <= 16) its = cta_roots<4>(K, C, crank, dpol, z2, rho, zn, rp, rt);
+        else if (K <= 32) its = cta_roots<8>(K, C, crank, dpol, z2, rho, zn, rp, rt);
+        else if (K <= 64) its = cta_roots<16>(K, C, crank, dpol, z2, rho, zn, rp, rt);
+        else its = cta_roots<32>(K, C, crank, dpol, z2, rho, zn, rp, rt);
+        if (tr) { p.dbg[10] += its; p.dbg[11] = max(p.dbg[11], (long long)its); p.dbg[12] += K; }
       }
       phase(4);
       if (C > 1) {

@@ -22,5 +22,6 @@ for cfg, ell, v in [("c1", 16, "fd"), ("c2", 20, "fd"), ("c2", 100, "fd"), ("c5"
     rows = max(1, tr[9])
     tot = sum(tr[i] for i in range(9))
     print(f"{cfg} ell={ell} {v}: {tot / rows:.0f} cycles/row over {rows} rows; " +
-          ", ".join(f"{names[i]} {tr[i] / rows:.0f}" for i in range(9)), flush=True)
+          ", ".join(f"{names[i]} {tr[i] / rows:.0f}" for i in range(9)) +
+          f"; warp-0 secular iterations/row {tr[10] / rows:.1f} (max {tr[11]}), K/row {tr[12] / rows:.1f}", flush=True)
     sk.close()
