@@ -31,10 +31,21 @@ sys.path.insert(0, ROOT)
 
 METRIC = "rows/sec sketched (fp32, ell given) at 1/2/4/8 B200 + % roofline; cov err"
 WORKLOADS = {
-    # name: (fdgen config, ell, default variant, P_total)
+    # name: (fdgen config, ell, default variant, P_total) -- one per BASELINE.json config.
+    # Per-row variants default to P_total = 1, the paper-exact single stream (reading C10);
+    # the batched configs use the shard counts of the cached oracle parity runs.
+    "c1": ("c1", 16, "fd", 1),
+    "c2": ("c2", 100, "fd", 1),
+    "c3": ("c3", 100, "fast_fd", 296),
     "c4": ("c4", 128, "fast_fd", 2368),
-    "c2": ("c2", 100, "fast_fd", 8),
-    "c1": ("c1", 16, "fast_fd", 8),
+    "c5": ("c5", 32, "fd", 1),
+}
+GEN = {
+    "c1": "noisy low-rank n=2000 d=64 k=8 zeta=10",
+    "c2": "noisy low-rank n=10000 d=500 k=50 zeta=10",
+    "c3": "image-like n=60000 d=3072 (rank-100 signal, [0,255] pixels / 255)",
+    "c4": "noisy low-rank n=8388608 d=1024 k=64 zeta=10",
+    "c5": "drifting subspaces n=200000 d=256 (20 blocks of 8-dim subspaces, fixed e every 100th row)",
 }
 
 
@@ -46,6 +57,13 @@ def peaks():
         with open(f) as fh:
             p.update(json.load(fh))
         p["source"] = "measured (MEASURED_PEAKS.json)"
+    # our own microbenchmarks (tools/micro/peaks.cu) for the pipes MEASURED_PEAKS.json lacks
+    g = os.path.join(ROOT, "profiles", "round2_peaks_microbench.json")
+    if os.path.exists(g):
+        with open(g) as fh:
+            m = json.load(fh)
+        p.update({k: m[k] for k in ("ffma_tflops", "dfma_tflops", "tf32_tcgen05_tflops") if k in m})
+        p["micro_source"] = "measured (profiles/round2_peaks_microbench.json, tools/micro/peaks.cu)"
     return p
 
 
@@ -91,9 +109,24 @@ def algorithmic_work(ell, d, N, R=None, t=None):
     }
 
 
-def fp32_simt_peak_tflops(mhz):
+def fp32_simt_peak_tflops(mhz, pk=None):
+    # measured FFMA throughput (tools/micro/peaks.cu) if present, else
     # 148 SMs x 128 FP32 lanes x 2 flops (FFMA) x clock
+    if pk and "ffma_tflops" in pk:
+        return pk["ffma_tflops"]
     return 148 * 128 * 2 * mhz * 1e6 / 1e12
+
+
+def tf32x3_peak_tflops(pk):
+    # measured tcgen05 kind::tf32 throughput / 3 (3xTF32) if present, else bf16 / 2 / 3
+    if "tf32_tcgen05_tflops" in pk:
+        return pk["tf32_tcgen05_tflops"] / 3.0
+    return pk["bf16_tflops"] / 2.0 / 3.0
+
+
+def fp64_peak_tflops(pk):
+    # measured DFMA throughput if present, else 148 SMs x 64 FP64 lanes x 2 x clock
+    return pk.get("dfma_tflops", 148 * 64 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12)
 
 
 class ClockSampler:
@@ -157,7 +190,8 @@ def dist_env():
 # ---------------------------------------------------------------------------
 # CPU oracle timing (cpu_baseline and the --impl reference arm)
 # ---------------------------------------------------------------------------
-def oracle_sample(wl, rows_per_shard=None, nshards=None, variant=None, alpha=0.2):
+def oracle_sample(wl, rows_per_shard=None, nshards=None, variant=None, alpha=0.2, ell_override=None,
+                  shards_override=None):
     """Time the oracle (as it stands) on a bounded sample of the workload: `nshards`
     shard streams of the bench DAG (one thread each, all host cores)."""
     import numpy as np  # noqa: F401
@@ -165,10 +199,24 @@ def oracle_sample(wl, rows_per_shard=None, nshards=None, variant=None, alpha=0.2
     import fdgen
     import oracle
     cfgname, ell, v0, P = WORKLOADS[wl]
+    ell = ell_override or ell
+    P = shards_override or P
     variant = variant or v0
     w = fdgen.config(cfgname)
+    if w.kind == fdgen.KIND_IMAGE:
+        w.xminmax = fdgen.host_minmax(w)
     cores = os.cpu_count() or 1
-    nshards = nshards or cores
+    if P == 1:
+        # one dependent stream: the oracle (one thread) on a prefix of it
+        nr = min(w.n, rows_per_shard or 4000)
+        A = fdgen.host_rows(w, 0, nr)
+        t0 = time.perf_counter()
+        oracle.sketch(A, ell, variant, alpha=alpha, nthreads=1)
+        dt = time.perf_counter() - t0
+        return {"value": nr / dt, "unit": "rows/s", "cores": 1, "kind": "oracle",
+                "sample": f"first {nr} rows of the single {wl} stream (P_total = 1), fp64 oracle, one thread, "
+                          f"{dt:.1f} s"}
+    nshards = nshards or min(cores, P)
     q, r = divmod(w.n, P)
     picks = [int(s * P / nshards) for s in range(nshards)]
     jobs = []
@@ -197,11 +245,14 @@ def run_reference(args):
     wl = args.workload
     cfgname, ell, variant, P = WORKLOADS[wl]
     variant = args.variant or variant
-    rows_per_shard = 2064 if wl == "c4" else None  # 256 + 14*129 rows: 15 ReduceRanks per shard
+    ell = args.ell or ell
+    P = args.shards or P
+    rows_per_shard = sample_rows(wl, P)
     times = []
     res = None
     for i in range(args.warmup + args.steps):
-        res = oracle_sample(wl, rows_per_shard=rows_per_shard, variant=variant, alpha=args.alpha)
+        res = oracle_sample(wl, rows_per_shard=rows_per_shard, variant=variant, alpha=args.alpha,
+                            ell_override=ell, shards_override=P)
         if i >= args.warmup:
             times.append(res)
     vals = [t["value"] for t in times]
@@ -211,7 +262,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.median(ms) if ms else None,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(wl, variant, P, world, args.alpha),
+        "config": config_dict(wl, variant, P, world, args.alpha, ell),
         "cpu_baseline": {"value": value, "unit": "rows/s", "cores": res["cores"], "kind": "oracle",
                          "sample": res["sample"]},
         "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -220,14 +271,26 @@ def run_reference(args):
     return 0
 
 
-def config_dict(wl, variant, P, world, alpha=None):
-    cfgname, ell, _, _ = WORKLOADS[wl]
+def sample_rows(wl, P):
+    """Rows per shard of the oracle's timed sample (about 10-30 s of one core per shard)."""
+    if wl == "c4":
+        return 2064          # 256 + 14*129 rows: 15 ReduceRanks per shard
+    if P == 1:
+        return {"c1": 2000, "c2": 1500, "c5": 20000}.get(wl, 4000)
+    return None
+
+
+def config_dict(wl, variant, P, world, alpha=None, ell=None):
+    cfgname, ell0, _, _ = WORKLOADS[wl]
+    ell = ell or ell0
     import fdgen
     w = fdgen.config(cfgname)
     va = f"{variant} alpha={alpha}" if (alpha is not None and "alpha" in variant) else variant
-    out = {"workload": f"{wl}: noisy low-rank n={w.n} d={w.d} k={w.k} zeta=10 fp32, ell={ell}, {va}",
+    l2 = ("inputs larger than L2 (A is streamed from HBM every step)" if w.n * w.d * 4 > 126e6 else
+          "A fits in L2 (126 MB); per-row steps are latency-bound, not memory-bound")
+    out = {"workload": f"{wl}: {GEN[wl]} fp32, ell={ell}, {va}, P_total={P}",
            "n": w.n, "d": w.d, "ell": ell, "variant": variant, "n_shards_total": P,
-           "parallelism": f"rows dp{world}", "l2": "inputs larger than L2 (A is streamed from HBM every step)"}
+           "parallelism": f"rows dp{world}", "l2": l2}
     if alpha is not None and "alpha" in variant:
         out["alpha"] = alpha
     return out
@@ -253,6 +316,7 @@ def run_ours(args):
     wl = args.workload
     cfgname, ell, variant, P = WORKLOADS[wl]
     variant = args.variant or variant
+    ell = args.ell or ell
     P = args.shards or P
     if P % world:
         raise SystemExit(f"P_total={P} not divisible by world={world}")
@@ -315,16 +379,23 @@ def run_ours(args):
     sk.append(A)
     Bst, st = sk.sketch(stats=True)
     shrinks_per_step = st["n_shrinks"]
-    simt_peak = fp32_simt_peak_tflops(pk.get("sm_max_mhz", 1965.0))
-    tf32_peak = pk["bf16_tflops"] / 2.0          # nominal tf32 = bf16 / 2 (B200_PROFILING.md)
+    simt_peak = fp32_simt_peak_tflops(pk.get("sm_max_mhz", 1965.0), pk)
+    tf32x3 = tf32x3_peak_tflops(pk)
     dom = max(kern, key=lambda k: kern[k][0])
     dom_ms = kern[dom][0] / args.steps
-    if dom == "ingest":
+    perrow = dom == "perrow"
+    if perrow:
+        # per-row chain: f_row = 2 ell^2 d + 2 ell d flops per row (reconstruct +
+        # dots), in fp64 on the FP64 pipe; latency-bound by design (n - ell + 1 dependent steps)
+        flops_step = (2.0 * ell * ell * w.d + 2.0 * ell * w.d) * nloc
+        roof = {"bound": "alu", "achieved": flops_step / (dom_ms / 1e3) / 1e12, "peak": fp64_peak_tflops(pk),
+                "unit": "TFLOP/s"}
+    elif dom == "ingest":
         bytes_step = 2.0 * nloc * w.d * 4
         roof = {"bound": "hbm", "achieved": bytes_step / (dom_ms / 1e3) / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s"}
     elif dom == "gram":
         flops_step = work["gram"] * shrinks_per_step
-        roof = {"bound": "tensor", "achieved": flops_step / (dom_ms / 1e3) / 1e12, "peak": tf32_peak / 3.0,
+        roof = {"bound": "tensor", "achieved": flops_step / (dom_ms / 1e3) / 1e12, "peak": tf32x3,
                 "unit": "TFLOP/s"}
     else:
         flops_step = work[dom] * shrinks_per_step
@@ -335,9 +406,13 @@ def run_ours(args):
     roof["per_kernel_ms_per_step"] = {k: v[0] / args.steps for k, v in kern.items()}
     roof["launches_per_step"] = {k: v[1] / args.steps for k, v in kern.items()}
     roof["problems_per_step"] = shrinks_per_step
+    micro = pk.get("micro_source")
     roof["peak_source"] = {
-        "alu": f"FP32 SIMT: 148 SM x 128 lanes x 2 flop x {pk.get('sm_max_mhz', 1965.0):.0f} MHz (derived, DESIGN.md §5)",
-        "tensor": f"3xTF32 = (bf16_tflops {pk['bf16_tflops']} / 2) / 3, {pk['source']}",
+        "alu": (f"FP64 DFMA, {micro}" if perrow else
+                (f"FP32 FFMA, {micro}" if micro else
+                 f"FP32 SIMT: 148 SM x 128 lanes x 2 flop x {pk.get('sm_max_mhz', 1965.0):.0f} MHz (derived)")),
+        "tensor": (f"tcgen05 kind::tf32 / 3 (3xTF32), {micro}" if micro else
+                   f"3xTF32 = (bf16_tflops {pk['bf16_tflops']} / 2) / 3, {pk['source']}"),
         "hbm": f"hbm_gbs {pk['source']}"}[roof["bound"]]
     traffic_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     roof["traffic"] = None
@@ -351,18 +426,26 @@ def run_ours(args):
     # north_star roofline: slower of HBM (4d bytes/row) and the Gram + reconstruct flops
     # on the pipes this build uses (Gram: tcgen05 3xTF32; reconstruct: FP32 SIMT)
     n_rows = w.n / world
-    gram_s = work["gram"] * shrinks_per_step / (tf32_peak / 3.0 * 1e12)
-    recon_s = work["recon"] * shrinks_per_step / (simt_peak * 1e12)
     hbm_s = n_rows * 4 * w.d / (pk["hbm_gbs"] * 1e9)
-    t_roof = max(hbm_s, gram_s + recon_s)
-    roof["north_star"] = {
-        "R_roof_rows_per_s_per_gpu": n_rows / t_roof, "t_roof_ms": t_roof * 1e3,
-        "pipes": "Gram tcgen05 3xTF32 (bf16/6), reconstruct FP32 SIMT", "hbm_ms": hbm_s * 1e3,
-        "frac": (value / world) / (n_rows / t_roof)}
-    eig_flops = (work["trd"] + work["bt"]) * shrinks_per_step
-    roof["eigensolver_inclusive"] = {
-        "t_roof_ms": (t_roof + eig_flops / (simt_peak * 1e12)) * 1e3,
-        "frac": (ms_step / 1e3) and ((t_roof + eig_flops / (simt_peak * 1e12)) / (ms_step / 1e3))}
+    if perrow:
+        t_roof = max(hbm_s, flops_step / (fp64_peak_tflops(pk) * 1e12))
+        roof["north_star"] = {
+            "R_roof_rows_per_s_per_gpu": n_rows / t_roof, "t_roof_ms": t_roof * 1e3,
+            "pipes": "per-row fp64 (f_row = 2 ell^2 d + 2 ell d on the FP64 pipe, all SMs)", "hbm_ms": hbm_s * 1e3,
+            "frac": (value / world) / (n_rows / t_roof),
+            "note": f"{P} dependent stream(s): at most {P} x C of 148 SMs busy; latency-bound by design"}
+    else:
+        gram_s = work["gram"] * shrinks_per_step / (tf32x3 * 1e12)
+        recon_s = work["recon"] * shrinks_per_step / (simt_peak * 1e12)
+        t_roof = max(hbm_s, gram_s + recon_s)
+        roof["north_star"] = {
+            "R_roof_rows_per_s_per_gpu": n_rows / t_roof, "t_roof_ms": t_roof * 1e3,
+            "pipes": "Gram tcgen05 3xTF32, reconstruct FP32 SIMT", "hbm_ms": hbm_s * 1e3,
+            "frac": (value / world) / (n_rows / t_roof)}
+        eig_flops = (work["trd"] + work["bt"]) * shrinks_per_step
+        roof["eigensolver_inclusive"] = {
+            "t_roof_ms": (t_roof + eig_flops / (simt_peak * 1e12)) * 1e3,
+            "frac": (ms_step / 1e3) and ((t_roof + eig_flops / (simt_peak * 1e12)) / (ms_step / 1e3))}
 
     gpu_launches = int(sum(v[1] for v in kern.values()))
 
@@ -408,9 +491,11 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32 (Gram: 3xTF32 tensor cores, fp32-accurate)",
+        "vs_baseline": None,
+        "dtype": ("f64 (per-row state and arithmetic)" if fd.is_batched(variant) is False and variant in PERROW
+                  else "f32 (Gram: 3xTF32 tensor cores, fp32-accurate)"),
         "data": "synthetic (seeded fdgen, generated on device)",
-        "config": config_dict(wl, variant, P, world, args.alpha),
+        "config": config_dict(wl, variant, P, world, args.alpha, ell),
         "roofline": roof,
         "gpu_launches": gpu_launches,
         "clocks": {"sm_mhz": clk["sm_mhz"], "sm_max_mhz": clk["sm_max_mhz"], "reasons": clk["reasons"]},
@@ -418,8 +503,8 @@ def run_ours(args):
         "e2e": e2e,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = oracle_sample(wl, rows_per_shard=2064 if wl == "c4" else None, variant=variant,
-                                             alpha=args.alpha)
+        line["cpu_baseline"] = oracle_sample(wl, rows_per_shard=sample_rows(wl, P), variant=variant,
+                                             alpha=args.alpha, ell_override=ell, shards_override=P)
     if rank == 0:
         print(json.dumps(line), flush=True)
     sk.close()
@@ -432,6 +517,7 @@ def run_ours(args):
 # Hashing / OSNAP arm: --variant osnap | hashing
 # ---------------------------------------------------------------------------
 HASH_S = {"osnap": 4, "hashing": 1}
+PERROW = ("fd", "alpha_fd", "isvd", "ssd", "cfd")
 
 
 def hash_oracle_sample(wl, s, ell, rows=1_000_000):
@@ -607,6 +693,7 @@ def main():
     ap.add_argument("--variant", default=None)
     ap.add_argument("--alpha", type=float, default=0.2, help="alpha of the alpha-FD variants")
     ap.add_argument("--shards", type=int, default=None, help="P_total shard streams (default: the workload's)")
+    ap.add_argument("--ell", type=int, default=None, help="sketch size (default: the workload's)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -1,0 +1,102 @@
+// Peak microbenchmarks for the roofline denominators: FP32 FFMA,
+// FP64 DFMA and tcgen05 kind::tf32 dense MMA throughput on all 148 SMs, timed with
+// CUDA events.  Output: one JSON object (TFLOP/s, measured at the clock the run saw).
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "fd_tc.cuh"
+using namespace fdk;
+
+template <typename T>
+__global__ void __launch_bounds__(1024) fma_kernel(T* out, int iters) {
+  T a[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = (T)(threadIdx.x + j);
+  const T b = (T)0.999999, c = (T)1e-7;
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = fma(a[j], b, c);
+  T s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += a[j];
+  if (s == (T)-1) out[0] = s;
+}
+
+// one CTA per SM; one thread issues M=128 x N=256 x K=8 tf32 MMAs back to back from
+// resident SW128 smem tiles into TMEM, committing every 32 MMAs to an mbarrier
+__global__ void __launch_bounds__(128, 1) tf32_kernel(int iters, int* sink) {
+  extern __shared__ unsigned char raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t s_tmem;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < (128 + 256) * 32; i += blockDim.x) reinterpret_cast<float*>(sm)[i] = 0.5f;
+  if (warp == 0) tc::tmem_alloc(&s_tmem, 512);
+  if (tid == 0) { tc::mbar_init(&mbar, 1); tc::fence_mbar_init(); }
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tb = s_tmem;
+  if (tid == 0) {
+    const uint32_t a = tc::smem_u32(sm), b = tc::smem_u32(sm + 128 * 128);
+    const uint32_t id = tc::idesc_tf32(128, 256, 0, 0);
+    uint32_t ph = 0;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const uint32_t ko = (q & 3) * 32;
+        tc::mma_tf32(tb + (q & 1) * 256, tc::desc_k_sw128(a + ko), tc::desc_k_sw128(b + ko), id, 1u);
+      }
+      tc::commit(&mbar);
+      tc::mbar_wait(&mbar, ph);
+      ph ^= 1;
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  if (warp == 0) tc::tmem_dealloc(tb, 512);
+  if (tid == 0 && iters < 0) sink[0] = 1;
+}
+
+int main() {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float ms;
+  void* out;
+  cudaMalloc(&out, 64);
+  const int sms = 148;
+  // FFMA: 8 resident 1024-thread... use 2 x 1024 threads per SM
+  const int it = 1 << 16;
+  fma_kernel<float><<<sms * 2, 1024>>>((float*)out, 16);
+  cudaEventRecord(e0);
+  fma_kernel<float><<<sms * 2, 1024>>>((float*)out, it);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double ffma = 2.0 * 8 * it * (double)sms * 2 * 1024 / (ms * 1e-3) / 1e12;
+  fma_kernel<double><<<sms * 2, 1024>>>((double*)out, 16);
+  cudaEventRecord(e0);
+  fma_kernel<double><<<sms * 2, 1024>>>((double*)out, it / 8);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double dfma = 2.0 * 8 * (it / 8) * (double)sms * 2 * 1024 / (ms * 1e-3) / 1e12;
+  const int smem = (128 + 256) * 128 + 1024;
+  cudaFuncSetAttribute(tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  tf32_kernel<<<sms, 128, smem>>>(16, (int*)out);
+  const int ti = 4096;
+  cudaEventRecord(e0);
+  tf32_kernel<<<sms, 128, smem>>>(ti, (int*)out);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double tf32 = 2.0 * 128 * 256 * 8 * 32.0 * ti * sms / (ms * 1e-3) / 1e12;
+  cudaError_t err = cudaGetLastError();
+  printf("{\"ffma_tflops\": %.2f, \"dfma_tflops\": %.2f, \"tf32_tcgen05_tflops\": %.2f, \"tf32x3_tflops\": %.2f, "
+         "\"error\": \"%s\", \"how\": \"tools/micro/peaks.cu: 296x1024 threads x 8 independent FMA chains (FFMA, DFMA); "
+         "148 CTAs each issuing back-to-back tcgen05.mma.kind::tf32 M128 N256 K8 from resident smem tiles, CUDA events\"}\n",
+         ffma, dfma, tf32, tf32 / 3.0, cudaGetErrorString(err));
+  return 0;
+}
