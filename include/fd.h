@@ -178,9 +178,15 @@ fd_status fd_destroy(fd_handle* h);
 /* Workspace bytes for the evaluator functions at dimension d. */
 size_t fd_cov_workspace_bytes(int64_t d);
 
+/* Scratch bytes fd_cov_gram_partial uses at (n, d) for its row-chunk partials (0: none). */
+size_t fd_cov_gram_workspace_bytes(int64_t n, int64_t d);
+
 /* AtA [device] (d x d fp64, row-major, full symmetric) += A^T A for the n rows
  * of A [device] (fp32, ld).  Products of fp32 values are exact in fp64 and the
- * accumulation is fp64 in a fixed order (deterministic).  Asynchronous. */
+ * accumulation is fp64 in a fixed order (deterministic).  ws [device] of at least
+ * fd_cov_gram_workspace_bytes(n, d) bytes lets the rows split into chunks that fill
+ * the GPU (their partials are summed in chunk order); ws = NULL runs one chunk.
+ * Asynchronous. */
 fd_status fd_cov_gram_partial(const float* A, int64_t n, int64_t ld, int64_t d, double* AtA,
                               void* ws, size_t ws_bytes, void* cuda_stream);
 

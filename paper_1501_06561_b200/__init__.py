@@ -164,8 +164,10 @@ def cov_gram_partial(A, AtA, stream=None):
     torch = _torch()
     A = _as_rows(A, AtA.shape[0])
     s = stream if stream is not None else torch.cuda.current_stream(A.device)
-    check(lib().fd_cov_gram_partial(A.data_ptr(), A.shape[0], A.stride(0), A.shape[1], AtA.data_ptr(), None, 0,
-                                    s.cuda_stream))
+    nb = lib().fd_cov_gram_workspace_bytes(A.shape[0], A.shape[1])
+    ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=A.device)
+    check(lib().fd_cov_gram_partial(A.data_ptr(), A.shape[0], A.stride(0), A.shape[1], AtA.data_ptr(),
+                                    ws.data_ptr() if nb else None, nb, s.cuda_stream))
     return AtA
 
 

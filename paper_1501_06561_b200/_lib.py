@@ -24,7 +24,7 @@ FD_MAX_N = 416
 # every symbol include/fd.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "fd_workspace_bytes", "fd_create", "fd_append_rows", "fd_host_stage_bytes", "fd_append_rows_host", "fd_sketch", "fd_merge", "fd_shard_sketch",
-    "fd_destroy", "fd_reset", "fd_profile", "fd_profile_read", "fd_cov_workspace_bytes", "fd_cov_gram_partial", "fd_cov_err_from_gram", "fd_cov_frob_from_gram", "fd_cov_err",
+    "fd_destroy", "fd_reset", "fd_profile", "fd_profile_read", "fd_cov_workspace_bytes", "fd_cov_gram_workspace_bytes", "fd_cov_gram_partial", "fd_cov_err_from_gram", "fd_cov_frob_from_gram", "fd_cov_err",
     "fd_proj_workspace_bytes", "fd_proj_err_from_gram", "fd_proj_err", "fd_hash_workspace_bytes", "fd_hash_sketch",
     "fd_last_error", "fd_version",
 ]
@@ -77,6 +77,8 @@ def lib():
         L.fd_profile_read.restype = ctypes.c_int32
         L.fd_cov_workspace_bytes.argtypes = [i64]
         L.fd_cov_workspace_bytes.restype = sz
+        L.fd_cov_gram_workspace_bytes.argtypes = [i64, i64]
+        L.fd_cov_gram_workspace_bytes.restype = sz
         L.fd_cov_gram_partial.argtypes = [vp, i64, i64, i64, vp, vp, sz, vp]
         L.fd_cov_err_from_gram.argtypes = [vp, vp, i32, i64, dbl, dp, dp, dp, vp, sz, vp]
         L.fd_cov_frob_from_gram.argtypes = [vp, i64, dp, vp]

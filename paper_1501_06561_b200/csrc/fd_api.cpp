@@ -829,26 +829,39 @@ fd_status fd_destroy(fd_handle* h) {
 // ---------------------------------------------------------------------------
 static int lanczos_k(int64_t d) { return (int)std::min<int64_t>(d, 512); }
 
-size_t fd_cov_workspace_bytes(int64_t d) {
-  if (d < 1) return 0;
+// bytes of the row-chunk partials of fd_cov_gram_partial at any n (the chunk count
+// saturates once n is large)
+static size_t syrk_part_max(int64_t d) { return fdk::syrk_partial_bytes(INT64_MAX / 4, d); }
+
+// evaluator workspace: [M][Q][work][out] (fd_cov_err_from_gram), then fd_cov_err's AtA,
+// then the SYRK row-chunk partials
+static size_t cov_base_bytes(int64_t d) {
   const int k = lanczos_k(d);
   size_t off = 0;
-  off = align_up(off + (size_t)d * d * sizeof(double), kAlign);                 // M / AtA scratch
+  off = align_up(off + (size_t)d * d * sizeof(double), kAlign);                 // M
   off = align_up(off + (size_t)(k + 1) * d * sizeof(double), kAlign);           // Q
   off = align_up(off + (size_t)(2 * k + 2 + d + k + 64) * sizeof(double), kAlign);  // work
   off = align_up(off + 4 * sizeof(double), kAlign);                             // out
-  off = align_up(off + (size_t)d * d * sizeof(double), kAlign);                 // AtA for fd_cov_err
   return off;
+}
+
+size_t fd_cov_workspace_bytes(int64_t d) {
+  if (d < 1) return 0;
+  return cov_base_bytes(d) + align_up((size_t)d * d * sizeof(double), kAlign) + align_up(syrk_part_max(d), kAlign);
+}
+
+size_t fd_cov_gram_workspace_bytes(int64_t n, int64_t d) {
+  if (d < 1 || n < 0) return 0;
+  return fdk::syrk_partial_bytes(n, d);
 }
 
 fd_status fd_cov_gram_partial(const float* A, int64_t n, int64_t ld, int64_t d, double* AtA, void* ws,
                               size_t ws_bytes, void* cuda_stream) {
-  (void)ws;
-  (void)ws_bytes;
   if (!AtA || (n > 0 && !A) || d < 1 || n < 0) return fail(FD_ERR_INVALID_ARG, "bad argument");
   if (ld < d) return fail(FD_ERR_SHAPE, "ld < d");
   if (n == 0) return FD_OK;
-  cudaError_t e = fdk::launch_syrk_f64(A, n, ld, d, AtA, static_cast<cudaStream_t>(cuda_stream));
+  cudaError_t e = fdk::launch_syrk_f64(A, n, ld, d, AtA, static_cast<double*>(ws), ws ? ws_bytes : 0,
+                                       static_cast<cudaStream_t>(cuda_stream));
   if (e != cudaSuccess) return cuda_fail(e, "syrk");
   return FD_OK;
 }
@@ -900,11 +913,12 @@ fd_status fd_cov_err(const float* A, int64_t n, int64_t ld, const float* B, int3
                      double* lam_max, double* lam_min, void* ws, size_t ws_bytes, void* cuda_stream) {
   if (!ws || ws_bytes < fd_cov_workspace_bytes(d)) return fail(FD_ERR_WORKSPACE, "evaluator workspace too small");
   cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
-  const size_t tot = fd_cov_workspace_bytes(d);
-  double* AtA = reinterpret_cast<double*>(static_cast<char*>(ws) + tot - align_up((size_t)d * d * sizeof(double), kAlign));
+  const size_t base = cov_base_bytes(d), atab = align_up((size_t)d * d * sizeof(double), kAlign);
+  double* AtA = reinterpret_cast<double*>(static_cast<char*>(ws) + base);
   cudaError_t e = cudaMemsetAsync(AtA, 0, (size_t)d * d * sizeof(double), s);
   if (e != cudaSuccess) return cuda_fail(e, "memset");
-  fd_status st = fd_cov_gram_partial(A, n, ld, d, AtA, ws, ws_bytes, cuda_stream);
+  fd_status st = fd_cov_gram_partial(A, n, ld, d, AtA, static_cast<char*>(ws) + base + atab, ws_bytes - base - atab,
+                                     cuda_stream);
   if (st != FD_OK) return st;
   double frob = 0.0;
   st = fd_cov_frob_from_gram(AtA, d, &frob, cuda_stream);

@@ -124,7 +124,12 @@ cudaError_t launch_perrow(const RowJob* dev_jobs, int count, const Params& p, in
                           cudaStream_t s);
 
 // Evaluator.
-cudaError_t launch_syrk_f64(const float* A, int64_t n, int64_t ld, int64_t d, double* AtA, cudaStream_t s);
+// AtA += A^T A (fp64); rows split into chunks whose partials (part, syrk_partial_bytes)
+// are summed in a fixed order; part == nullptr (or too small) -> one chunk, no partials
+int syrk_chunks(int64_t n, int64_t d);
+size_t syrk_partial_bytes(int64_t n, int64_t d);
+cudaError_t launch_syrk_f64(const float* A, int64_t n, int64_t ld, int64_t d, double* AtA, double* part,
+                            size_t part_bytes, cudaStream_t s);
 cudaError_t launch_sub_btb(double* M, const double* AtA, const float* B, int ell, int64_t d, cudaStream_t s);
 cudaError_t launch_lanczos(const double* M, int64_t d, int kmax, double* Q, double* work, double* out2,
                            cudaStream_t s, int ntop = 0, double* top = nullptr);

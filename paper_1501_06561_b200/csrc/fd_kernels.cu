@@ -15,6 +15,7 @@
 // iteration (with modified Gram-Schmidt inside eigenvalue clusters) for the
 // ell-1 retained eigenvectors, and a fp32 Householder back-transform.
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdlib>
 #include <float.h>
 #include <math.h>
@@ -1529,13 +1530,22 @@ cudaError_t launch_eig(const Prob* dev_probs, int count, const Params& p, double
 // Evaluator: AtA += A^T A (fp64 products / accumulation), one CTA per 64x64
 // lower tile, fixed row order -> deterministic.
 // ============================================================================
+// fp64 SYRK: 64 x 64 lower-triangular tiles of A^T A (products of fp32 values are
+// exact in fp64), rows split into `nch` contiguous chunks so every SM holds several
+// CTAs (d = 1024: 136 tiles x 7 chunks).  Chunk c of tile t writes its partial to
+// part[(c * ntiles + t) * 4096] (nch > 1) or adds straight into AtA (nch == 1); the
+// partials are summed in chunk order by syrk_reduce_kernel (deterministic).
 __global__ void __launch_bounds__(256) syrk_f64_kernel(const float* __restrict__ A, int64_t n, int64_t ld,
-                                                       int64_t d, double* __restrict__ AtA) {
+                                                       int64_t d, double* __restrict__ AtA, double* __restrict__ part,
+                                                       int nch) {
   int ti, tj;
   tri_index(blockIdx.x, ti, tj);
+  const int ntiles = gridDim.x, ch = blockIdx.y;
+  const int64_t rows_per = (n + nch - 1) / nch;
+  const int64_t rbeg = (int64_t)ch * rows_per, rend = min(n, rbeg + rows_per);
   const int64_t i0 = (int64_t)ti * 64, j0 = (int64_t)tj * 64;
-  __shared__ double As[16][65];
-  __shared__ double Bs[16][65];
+  __shared__ __align__(16) double As[16][68];
+  __shared__ __align__(16) double Bs[16][68];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   double acc[4][4];
 #pragma unroll
@@ -1543,26 +1553,48 @@ __global__ void __launch_bounds__(256) syrk_f64_kernel(const float* __restrict__
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
   const int lrow = threadIdx.x >> 4, lcol = (threadIdx.x & 15) * 4;
-  for (int64_t r0 = 0; r0 < n; r0 += 16) {
-    const int64_t r = r0 + lrow;
+  const bool vec = ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+  auto load = [&](int64_t r, int64_t c0, float (&v)[4]) {
+    if (r < rend && vec && c0 + 3 < d) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(A + r * ld + c0));
+      v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    } else {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int64_t ci = i0 + lcol + q, cj = j0 + lcol + q;
-      As[lrow][lcol + q] = (r < n && ci < d) ? (double)A[r * ld + ci] : 0.0;
-      Bs[lrow][lcol + q] = (r < n && cj < d) ? (double)A[r * ld + cj] : 0.0;
+      for (int q = 0; q < 4; ++q) v[q] = (r < rend && c0 + q < d) ? A[r * ld + c0 + q] : 0.f;
     }
+  };
+  float va[4], vb[4];
+  load(rbeg + lrow, i0 + lcol, va);
+  load(rbeg + lrow, j0 + lcol, vb);
+  for (int64_t r0 = rbeg; r0 < rend; r0 += 16) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { As[lrow][lcol + q] = (double)va[q]; Bs[lrow][lcol + q] = (double)vb[q]; }
     __syncthreads();
+    if (r0 + 16 < rend) {           // prefetch the next 16 rows while this block computes
+      load(r0 + 16 + lrow, i0 + lcol, va);
+      load(r0 + 16 + lrow, j0 + lcol, vb);
+    }
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
-      double a[4], b[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) { a[q] = As[k][ty * 4 + q]; b[q] = Bs[k][tx * 4 + q]; }
+      const double2 a01 = *reinterpret_cast<const double2*>(&As[k][ty * 4]);
+      const double2 a23 = *reinterpret_cast<const double2*>(&As[k][ty * 4 + 2]);
+      const double2 b01 = *reinterpret_cast<const double2*>(&Bs[k][tx * 4]);
+      const double2 b23 = *reinterpret_cast<const double2*>(&Bs[k][tx * 4 + 2]);
+      const double a[4] = {a01.x, a01.y, a23.x, a23.y}, b[4] = {b01.x, b01.y, b23.x, b23.y};
 #pragma unroll
       for (int x = 0; x < 4; ++x)
 #pragma unroll
         for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
     }
     __syncthreads();
+  }
+  if (nch > 1) {
+    double* P = part + ((size_t)ch * ntiles + blockIdx.x) * 4096;
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) P[(ty * 4 + x) * 64 + tx * 4 + y] = acc[x][y];
+    return;
   }
 #pragma unroll
   for (int x = 0; x < 4; ++x)
@@ -1576,9 +1608,45 @@ __global__ void __launch_bounds__(256) syrk_f64_kernel(const float* __restrict__
     }
 }
 
-cudaError_t launch_syrk_f64(const float* A, int64_t n, int64_t ld, int64_t d, double* AtA, cudaStream_t s) {
+__global__ void __launch_bounds__(256) syrk_reduce_kernel(const double* __restrict__ part, int nch, int64_t d,
+                                                          double* __restrict__ AtA) {
+  int ti, tj;
+  tri_index(blockIdx.x, ti, tj);
+  const int ntiles = gridDim.x;
+  for (int e = threadIdx.x; e < 4096; e += blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < nch; ++c) s += part[((size_t)c * ntiles + blockIdx.x) * 4096 + e];
+    const int64_t i = (int64_t)ti * 64 + (e >> 6), j = (int64_t)tj * 64 + (e & 63);
+    if (i < d && j < d) {
+      AtA[i * d + j] += s;
+      if (ti != tj) AtA[j * d + i] += s;
+    }
+  }
+}
+
+int syrk_chunks(int64_t n, int64_t d) {
   const int nt = (int)((d + 63) / 64);
-  syrk_f64_kernel<<<nt * (nt + 1) / 2, 256, 0, s>>>(A, n, ld, d, AtA);
+  const int ntiles = nt * (nt + 1) / 2;
+  int nch = (6 * kNumSMs + ntiles - 1) / ntiles;     // ~6 CTAs per SM
+  nch = std::min<int64_t>(nch, std::max<int64_t>(1, n / 256));
+  return std::max(1, std::min(nch, 16));
+}
+
+size_t syrk_partial_bytes(int64_t n, int64_t d) {
+  const int nch = syrk_chunks(n, d);
+  if (nch <= 1) return 0;
+  const int nt = (int)((d + 63) / 64);
+  return (size_t)nch * (nt * (nt + 1) / 2) * 4096 * sizeof(double);
+}
+
+cudaError_t launch_syrk_f64(const float* A, int64_t n, int64_t ld, int64_t d, double* AtA, double* part,
+                            size_t part_bytes, cudaStream_t s) {
+  const int nt = (int)((d + 63) / 64);
+  const int ntiles = nt * (nt + 1) / 2;
+  int nch = syrk_chunks(n, d);
+  if (nch > 1 && (!part || part_bytes < syrk_partial_bytes(n, d))) nch = 1;
+  syrk_f64_kernel<<<dim3(ntiles, nch), 256, 0, s>>>(A, n, ld, d, AtA, part, nch);
+  if (nch > 1) syrk_reduce_kernel<<<ntiles, 256, 0, s>>>(part, nch, d, AtA);
   return cudaGetLastError();
 }
 

@@ -38,12 +38,17 @@ def gather_and_merge(B_local, stats_local: dict, merge_fn, group=None):
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     if world == 1:
         return B_local, dict(stats_local)
-    gathered = torch.empty((world,) + tuple(B_local.shape), dtype=B_local.dtype, device=B_local.device)
-    if dist.get_backend(group) == "nccl":
+    nccl = dist.get_backend(group) == "nccl"
+    if nccl:
+        gathered = torch.empty((world,) + tuple(B_local.shape), dtype=B_local.dtype, device=B_local.device)
         dist.all_gather_into_tensor(gathered, B_local.contiguous(), group=group)
-    else:  # gloo (CPU tests): list form of the same gather
-        dist.all_gather(list(gathered.unbind(0)), B_local.contiguous(), group=group)
-    vec = torch.tensor([float(stats_local[k]) for k in STAT_KEYS], dtype=torch.float64, device=B_local.device)
+    else:  # gloo: list form of the same gather on host copies, result back on B's device
+        Bh = B_local.detach().to("cpu").contiguous()
+        gh = torch.empty((world,) + tuple(Bh.shape), dtype=Bh.dtype)
+        dist.all_gather(list(gh.unbind(0)), Bh, group=group)
+        gathered = gh.to(B_local.device)
+    vec = torch.tensor([float(stats_local[k]) for k in STAT_KEYS], dtype=torch.float64,
+                       device=B_local.device if nccl else "cpu")
     dist.all_reduce(vec, group=group)
     B, mst = merge_fn(gathered)
     out = {k: float(v) for k, v in zip(STAT_KEYS, vec.tolist())}

@@ -32,7 +32,9 @@ def _read_golden_rules():
 
 @pytest.mark.parametrize("case", _read_golden_rules())
 def test_reduce_rank_hand_examples(case):
-    """SPEC.md:183-194 hand examples of the FD / alpha-FD / iSVD rules."""
+    """SPEC.md hand examples of the FD / alpha-FD / iSVD rules (PAPER.md:248, 254,
+    319-325), the paper-literal Fast alpha-FD and ReduceRank-SS
+    (PAPER.md:405-411), values re-derived by hand in tests/golden."""
     rule, alpha, ell, s_in, s_out, delta = case
     L = len(s_in)
     d = L + 1
@@ -40,8 +42,11 @@ def test_reduce_rank_hand_examples(case):
     rng = np.random.default_rng(0)
     Q, _ = np.linalg.qr(rng.standard_normal((d, d)))
     Bf = np.diag(s_in) @ Q[:L]
-    r = oracle.RULE_ISVD if rule == "isvd" else oracle.RULE_FD
-    B, dl, removed = oracle.reduce_rank(Bf, ell, r, alpha)
+    if rule == "fastpfd":
+        B, dl, removed = oracle.reduce_rank_t(Bf, ell, alpha)
+    else:
+        r = {"isvd": oracle.RULE_ISVD, "ss": oracle.RULE_SS}.get(rule, oracle.RULE_FD)
+        B, dl, removed = oracle.reduce_rank(Bf, ell, r, alpha)
     sv = np.linalg.svd(B, compute_uv=False)
     expect = np.zeros(len(sv))
     expect[: len(s_out)] = s_out
@@ -435,28 +440,19 @@ def test_fd_t_indices_reading():
     assert oracle.fd_t_indices(50, 0.02) == (49, 49)       # m = 1: only sigma_ell shrinks
 
 
-def test_fast_alpha_fd_paper_rule_closed_form():
-    """One ReduceRank of a buffer with known singular values (rows s_j e_{pi(j)}):
-    PAPER.md:391 -- delta = sigma_t^2, sigma'_j^2 = sigma_j^2 for j <= ell - alpha ell,
-    max(sigma_j^2 - delta, 0) for the last alpha ell -- written out here directly."""
-    ell, alpha, d = 20, 0.4, 31
-    rng = np.random.default_rng(5)
-    s = np.sort(rng.uniform(1.0, 9.0, ell))[::-1]
-    perm = rng.permutation(d)[:ell]
-    Bf = np.zeros((ell, d))
-    for j in range(ell):
-        Bf[j, perm[j]] = s[j]
-    Bf = Bf[rng.permutation(ell)]           # row order of the buffer must not matter
-    t, R = oracle.fd_t_indices(ell, alpha)
-    m = oracle.alpha_m(ell, alpha)
-    B, delta, removed = oracle.reduce_rank_t(Bf, ell, alpha)
-    assert abs(delta - s[t - 1] ** 2) < 1e-12 * s[0] ** 2
-    sp2 = np.where(np.arange(1, ell + 1) <= ell - m, s ** 2, np.maximum(s ** 2 - delta, 0.0))
-    sp2[R:] = 0.0
-    got = np.sort(np.sum(B ** 2, axis=1))[::-1]
-    np.testing.assert_allclose(got, sp2, atol=1e-10 * s[0] ** 2)
-    assert np.all(np.sum(B[R:] ** 2, axis=1) == 0.0)
-    assert abs(removed - (np.sum(s ** 2) - np.sum(sp2))) < 1e-10 * s[0] ** 2
+def test_cfd_spec_hand_example():
+    """Compensative FD's final step (sigma_hat_j = sqrt(sigma'_j^2 + Delta)),
+    by hand: ell = 2, rows 2e1, e2, e2 (d = 2).  The lazy ReduceRank of [2e1; e2] (spectrum (2, 1))
+    shrinks by delta = 1 -> (sqrt3, 0); e2 takes the free slot; the final step on [sqrt3 e1; e2]
+    (spectrum (sqrt3, 1)) shrinks by delta = 1 -> sigma' = (sqrt2, 0) and compensates with
+    Delta = 1 + 1 = 2 -> sigma_hat = (sqrt(2 + 2), sqrt(0 + 2)) = (2, sqrt2); the mass
+    ||A||_F^2 = 6 = 4 + 2 is preserved."""
+    A = np.array([[2, 0], [0, 1], [0, 1]], np.float32)
+    r = oracle.sketch(A, 2, "cfd")
+    sv = np.linalg.svd(r.B, compute_uv=False)
+    np.testing.assert_allclose(sv, [2.0, np.sqrt(2.0)], atol=1e-12)
+    assert abs(r.delta_total - 2.0) < 1e-12
+    assert r.n_shrinks == 2
 
 
 def test_fast_alpha_fd_paper_alpha1_is_fast_fd():
