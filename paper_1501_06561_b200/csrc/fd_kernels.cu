@@ -16,6 +16,7 @@
 // ell-1 retained eigenvectors, and a fp32 Householder back-transform.
 #include <cuda_runtime.h>
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <float.h>
 #include <math.h>
@@ -359,6 +360,7 @@ constexpr int kNW = kEigThreads / 32;  // 16 warps
 #define FD_EIG_CTAS 3
 #endif
 constexpr int kEigPreCtasPerSM = FD_EIG_CTAS;     // resident CTAs of the lean (tridiagonal-input) variant
+constexpr int kPreZst = 132;          // lean variant: fp32 inverse-iteration scratch stride (>= 129 vectors)
 constexpr int kSmallCl = 8;             // clusters up to this size: warp MGS; larger: block CGS2
 #ifndef FD_INV_ITERS
 #define FD_INV_ITERS 2
@@ -516,14 +518,14 @@ __device__ __forceinline__ T coarse_pt(int t, int fam, int H, T gl, T gu) {
 // Large clusters (> kSmallCl members) of the inverse iteration: panels of 8 members,
 // block Gram-Schmidt twice against the earlier members + warp MGS inside the panel (see
 // the call site).  Out of line so its registers do not perturb the solver loop's.
-template <int NM, int kNT>
+template <int NM, int kNT, typename ZT>
 __device__
 #ifdef FD_PANEL_INLINE
 __forceinline__
 #else
 __noinline__
 #endif
-void panel_cgs(double* __restrict__ Zs, int kMaxN, double* __restrict__ pscl,
+void panel_cgs(ZT* __restrict__ Zs, int kMaxN, double* __restrict__ pscl,
                                        double* __restrict__ cpart, const int* __restrict__ cstart,
                                        const int* __restrict__ clen, int ncl, int N) {
   constexpr int kNW = kNT / 32;
@@ -578,7 +580,7 @@ void panel_cgs(double* __restrict__ Zs, int kMaxN, double* __restrict__ pscl,
             }
             __syncthreads();
             for (int i = tid; i < N; i += kNT) {
-              double* zi = Zs + (size_t)i * kMaxN;
+              ZT* zi = Zs + (size_t)i * kMaxN;
               double z[8];
 #pragma unroll
               for (int m = 0; m < 8; ++m) z[m] = (m < pb) ? zi[p0 + m] : 0.0;
@@ -606,7 +608,7 @@ void panel_cgs(double* __restrict__ Zs, int kMaxN, double* __restrict__ pscl,
         }
         if (warp == 0) {   // the panel itself: MGS twice, normalise (registers)
           for (int k = p0; k < p0 + pb; ++k) {
-            double* zk = Zs + k;
+            ZT* zk = Zs + k;
             double zr[NM / 32];
 #pragma unroll
             for (int t = 0; t < NM / 32; ++t) {
@@ -615,7 +617,7 @@ void panel_cgs(double* __restrict__ Zs, int kMaxN, double* __restrict__ pscl,
             }
             for (int pass = 0; pass < 2; ++pass)
               for (int q = p0; q < k; ++q) {
-                const double* zq = Zs + q;
+                const ZT* zq = Zs + q;
                 double zqr[NM / 32];
                 double hh = 0.0;
 #pragma unroll
@@ -689,10 +691,17 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
   __shared__ T s_gl, s_gu, s_a1, s_a2;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // element-major (coalesced across threads): LF[i][cl], RD[i][cl], Zs[i][j]
-  double* LF = slot;
-  double* RD = slot + (size_t)kMaxN * kMaxN;
-  double* Zs = slot + (size_t)2 * kMaxN * kMaxN;
+  // element-major (coalesced across threads): LF[i][j] (multipliers), Zs[i][j] (vectors),
+  // row stride zst.  The lean variant stores them in fp32 with stride kPreZst (its <= 129
+  // vectors): 444 resident slots x 2 x 256 x 132 x 4 B = 120 MB stay in L2, where the fp64
+  // full-stride layout (2 MB per slot) streamed from HBM (round-1 ncu: 18x the algorithmic
+  // bytes).  The recurrences themselves run in fp64 registers; the Gram (3xTF32) and the
+  // tridiagonal form (fp32) already carry errors far above fp32 rounding of the vectors.
+  using ZT = typename std::conditional<PRE, float, double>::type;
+  const int zst = PRE ? kPreZst : kMaxN;
+  ZT* LF = reinterpret_cast<ZT*>(slot);
+  ZT* Zs = reinterpret_cast<ZT*>(slot + (size_t)kMaxN * kMaxN);
+  double* RD = slot + (size_t)2 * kMaxN * kMaxN;
 
   for (int pi = blockIdx.x; pi < count; pi += gridDim.x) {
     const Prob P = probs[pi];
@@ -1058,7 +1067,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
     // One thread per vector j < JX (3 iterations, shift lam[j]); after every
     // iteration the members of each multi-member cluster are orthonormalised by
     // one warp (modified Gram-Schmidt, twice), so a member converges inside the
-    // complement of the earlier ones.  Scratch is element-major (z[i * kMaxN + j]):
+    // complement of the earlier ones.  Scratch is element-major (z[i * zst + j]):
     // the per-thread recurrences are coalesced across threads.
     const int ncl = s_ncl;
     const int JX = s_jx;
@@ -1088,8 +1097,8 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
       for (int it = 0; it < kInvIters; ++it) {
         for (int j = tid >> 1; j < JX; j += blockDim.x >> 1) {
           if (!vact[j]) continue;
-          double* lf = LF + j;   // lf[i * kMaxN]: l_i (i < m), u_i (i >= m)
-          double* z = Zs + j;    // z[i * kMaxN]
+          ZT* lf = LF + j;   // lf[i * zst]: l_i (i < m), u_i (i >= m)
+          ZT* z = Zs + j;    // z[i * zst]
           const double sc = pscl[j];
           const double mu = (double)lam[j];
           auto rhs = [&](int i, double zi) -> double {
@@ -1105,7 +1114,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
             double zb[kSB];
             if (it > 0) {
 #pragma unroll
-              for (int q = 0; q < kSB; ++q) zb[q] = (k0 + q < cnt) ? z[(size_t)(ist + dir * (k0 + q)) * kMaxN] : 0.0;
+              for (int q = 0; q < kSB; ++q) zb[q] = (k0 + q < cnt) ? z[(size_t)(ist + dir * (k0 + q)) * zst] : 0.0;
             }
 #pragma unroll
             for (int q = 0; q < kSB; ++q) {
@@ -1119,7 +1128,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
                   w = bi;
                 } else {
                   const double li = eprev * rd;
-                  lf[(size_t)(i - 1 + side) * kMaxN] = li;
+                  lf[(size_t)(i - 1 + side) * zst] = li;
                   dpi = ((double)dd[i] - mu) - li * eprev;
                   w = bi - li * w;
                 }
@@ -1131,12 +1140,12 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
             }
 #pragma unroll
             for (int q = 0; q < kSB; ++q)
-              if (k0 + q < cnt) z[(size_t)(ist + dir * (k0 + q)) * kMaxN] = zb[q];
+              if (k0 + q < cnt) z[(size_t)(ist + dir * (k0 + q)) * zst] = zb[q];
           }
           double tS = 0.0, wS = 0.0;   // this side's term of the twist row
           if (cnt > 0) {
             const double l = eprev * rd;   // l_{m-1} (top) / u_m (bottom)
-            lf[(size_t)(m - 1 + side) * kMaxN] = l;
+            lf[(size_t)(m - 1 + side) * zst] = l;
             tS = l * eprev;
             wS = l * w;
           }
@@ -1146,10 +1155,10 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
           const double wA = side ? wO : wS, wB = side ? wS : wO;
           double gm = (((double)dd[m] - mu) - tA) - tB;
           if (fabs(gm) < tiny) gm = (gm < 0.0) ? -tiny : tiny;
-          const double bm = rhs(m, (it > 0) ? z[(size_t)m * kMaxN] : 0.0);
+          const double bm = rhs(m, (it > 0) ? z[(size_t)m * zst] : 0.0);
           const double zm = ((bm - wA) - wB) * rcp_d(gm);
           __syncwarp(pmask);   // both lanes read z[m] before it is overwritten
-          if (side == 0) z[(size_t)m * kMaxN] = zm;
+          if (side == 0) z[(size_t)m * zst] = zm;
           double nr = side ? 0.0 : zm * zm;
           // back-substitution outwards from m: top i = m-1..0 (l_i = lf[i]),
           // bottom i = m+1..N-1 (u_{i-1} = lf[i-1])
@@ -1161,8 +1170,8 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
             for (int q = 0; q < kSB; ++q) {
               const int i = bst + bdir * (k0 + q);
               const bool ok = k0 + q < cnt;
-              zb[q] = ok ? z[(size_t)i * kMaxN] : 0.0;
-              lb[q] = ok ? lf[(size_t)(i - side) * kMaxN] : 0.0;
+              zb[q] = ok ? z[(size_t)i * zst] : 0.0;
+              lb[q] = ok ? lf[(size_t)(i - side) * zst] : 0.0;
             }
 #pragma unroll
             for (int q = 0; q < kSB; ++q) {
@@ -1174,7 +1183,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
             }
 #pragma unroll
             for (int q = 0; q < kSB; ++q)
-              if (k0 + q < cnt) z[(size_t)(bst + bdir * (k0 + q)) * kMaxN] = zb[q];
+              if (k0 + q < cnt) z[(size_t)(bst + bdir * (k0 + q)) * zst] = zb[q];
           }
           nr += __shfl_xor_sync(pmask, nr, 1);
           if (side == 0) pscl[j] = (nr > 0.0) ? 1.0 / sqrt(nr) : 0.0;
@@ -1187,23 +1196,23 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
           const int j0 = cstart[c], j1 = cstart[c] + clen[c];
           if (j1 - j0 < 2 || j1 - j0 > kSmallCl) continue;
           for (int k = j0; k < j1; ++k) {
-            double* zk = Zs + k;
+            ZT* zk = Zs + k;
             double zr[NM / 32];
             const double s0 = pscl[k];
 #pragma unroll
             for (int t = 0; t < NM / 32; ++t) {
               const int i = 32 * t + lane;
-              zr[t] = (i < N) ? zk[(size_t)i * kMaxN] * s0 : 0.0;
+              zr[t] = (i < N) ? zk[(size_t)i * zst] * s0 : 0.0;
             }
             for (int pass = 0; pass < 2; ++pass)
               for (int q = j0; q < k; ++q) {
-                const double* zq = Zs + q;
+                const ZT* zq = Zs + q;
                 double zqr[NM / 32];
                 double h = 0.0;
 #pragma unroll
                 for (int t = 0; t < NM / 32; ++t) {
                   const int i = 32 * t + lane;
-                  zqr[t] = (i < N) ? zq[(size_t)i * kMaxN] : 0.0;
+                  zqr[t] = (i < N) ? zq[(size_t)i * zst] : 0.0;
                   h = fma(zqr[t], zr[t], h);
                 }
                 h = warp_sum_d(h);
@@ -1218,7 +1227,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
 #pragma unroll
             for (int t = 0; t < NM / 32; ++t) {
               const int i = 32 * t + lane;
-              if (i < N) zk[(size_t)i * kMaxN] = zr[t] * inv;
+              if (i < N) zk[(size_t)i * zst] = zr[t] * inv;
             }
             __syncwarp();
             if (lane == 0) pscl[k] = 1.0;
@@ -1234,7 +1243,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
         // update: a thread per row -- then one warp orthonormalises the panel itself
         // (modified Gram-Schmidt twice, registers).
         if constexpr (BIG) {   // merge launches: panels of 8 (block CGS2 + warp MGS)
-          panel_cgs<NM, kNT>(Zs, kMaxN, pscl, cpart, cstart, clen, ncl, N);
+          panel_cgs<NM, kNT, ZT>(Zs, zst, pscl, cpart, cstart, clen, ncl, N);
           __syncthreads();
         } else {
           double* chq = cpart + kNW * kCpStride;   // [NM] projection coefficients
@@ -1248,10 +1257,10 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
           if (nc <= kSmallCl) continue;
           const int rpw = (N + kNW - 1) / kNW;   // rows per warp
           for (int k = j0; k < j0 + nc; ++k) {
-            double* zk = Zs + k;
+            ZT* zk = Zs + k;
             const double s0 = pscl[k];
             __syncthreads();   // previous member finished; pscl stable
-            for (int i = tid; i < N; i += kNT) zk[(size_t)i * kMaxN] *= s0;
+            for (int i = tid; i < N; i += kNT) zk[(size_t)i * zst] *= s0;
             for (int pass = 0; pass < 2 && k > j0; ++pass) {
               __syncthreads();
               for (int q0 = 0; q0 < k - j0; q0 += 32) {
@@ -1264,13 +1273,13 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
                     double za[8], zb[8];
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
-                      za[u] = Zs[(size_t)(i + u) * kMaxN + q];
-                      zb[u] = zk[(size_t)(i + u) * kMaxN];
+                      za[u] = Zs[(size_t)(i + u) * zst + q];
+                      zb[u] = zk[(size_t)(i + u) * zst];
                     }
 #pragma unroll
                     for (int u = 0; u < 8; ++u) h = fma(za[u], zb[u], h);
                   }
-                  for (; i < ib; ++i) h = fma(Zs[(size_t)i * kMaxN + q], zk[(size_t)i * kMaxN], h);
+                  for (; i < ib; ++i) h = fma((double)Zs[(size_t)i * zst + q], (double)zk[(size_t)i * zst], h);
                 }
                 cpart[warp * kCpStride + q0 + lane] = h;
               }
@@ -1282,8 +1291,8 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
               }
               __syncthreads();
               for (int i = tid; i < N; i += kNT) {
-                double zi = zk[(size_t)i * kMaxN];
-                const double* zrow = Zs + (size_t)i * kMaxN + j0;
+                double zi = zk[(size_t)i * zst];
+                const ZT* zrow = Zs + (size_t)i * zst + j0;
                 const int nq = k - j0;
                 int q = 0;
                 for (; q + 8 <= nq; q += 8) {   // 8 independent loads in flight
@@ -1293,20 +1302,20 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
 #pragma unroll
                   for (int u = 0; u < 8; ++u) zi = fma(-chq[q + u], zr8[u], zi);
                 }
-                for (; q < nq; ++q) zi = fma(-chq[q], zrow[q], zi);
-                zk[(size_t)i * kMaxN] = zi;
+                for (; q < nq; ++q) zi = fma(-chq[q], (double)zrow[q], zi);
+                zk[(size_t)i * zst] = zi;
               }
             }
             __syncthreads();
             double n2 = 0.0;
-            for (int i = tid; i < N; i += kNT) { const double x = zk[(size_t)i * kMaxN]; n2 = fma(x, x, n2); }
+            for (int i = tid; i < N; i += kNT) { const double x = zk[(size_t)i * zst]; n2 = fma(x, x, n2); }
             n2 = warp_sum_d(n2);
             if (lane == 0) cpart[warp] = n2;
             __syncthreads();
             double tot = 0.0;
             for (int w = 0; w < kNW; ++w) tot += cpart[w];
             const double inv = (tot > 0.0) ? 1.0 / sqrt(tot) : 0.0;
-            for (int i = tid; i < N; i += kNT) zk[(size_t)i * kMaxN] *= inv;
+            for (int i = tid; i < N; i += kNT) zk[(size_t)i * zst] *= inv;
             if (tid == 0) pscl[k] = 1.0;
           }
         }
@@ -1322,26 +1331,26 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
     for (int r = 0; r < s_nrr; ++r) {
       const int c = cid[r];
       const int j0 = cstart[c], nc = clen[c];
-      double* H = LF;                   // nc x nc (ld nc)
+      double* H = slot;                 // nc x nc (ld nc), over the dead multipliers
       double* Q = RD;                   // nc x nc (ld nc)
-      double* Zc = Zs + (size_t)kMaxN * kMaxN;   // copy of Z_c (N x nc), 4th scratch region
+      double* Zc = slot + (size_t)3 * kMaxN * kMaxN;   // copy of Z_c (N x nc), 4th scratch region
       for (int x = tid; x < nc * nc; x += blockDim.x) {
         const int a = x / nc, b = x % nc;
-        const double* za = Zs + j0 + a;
-        const double* zb = Zs + j0 + b;
+        const ZT* za = Zs + j0 + a;
+        const ZT* zb = Zs + j0 + b;
         double h = 0.0;
         for (int i = 0; i < N; ++i) {
-          double tz = (double)dd[i] * zb[(size_t)i * kMaxN];
-          if (i > 0) tz += (double)ee[i - 1] * zb[(size_t)(i - 1) * kMaxN];
-          if (i < N - 1) tz += (double)ee[i] * zb[(size_t)(i + 1) * kMaxN];
-          h = fma(za[(size_t)i * kMaxN], tz, h);
+          double tz = (double)dd[i] * zb[(size_t)i * zst];
+          if (i > 0) tz += (double)ee[i - 1] * zb[(size_t)(i - 1) * zst];
+          if (i < N - 1) tz += (double)ee[i] * zb[(size_t)(i + 1) * zst];
+          h = fma((double)za[(size_t)i * zst], tz, h);
         }
         H[a * nc + b] = h;
         Q[a * nc + b] = (a == b) ? 1.0 : 0.0;
       }
       for (int x = tid; x < N * nc; x += blockDim.x) {
         const int i = x / nc, a = x % nc;
-        Zc[(size_t)i * nc + a] = Zs[(size_t)i * kMaxN + j0 + a];
+        Zc[(size_t)i * nc + a] = Zs[(size_t)i * zst + j0 + a];
       }
       __syncthreads();
       if (warp == 0) {
@@ -1399,7 +1408,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
         const int col = ord[k];
         double s = 0.0;
         for (int a = 0; a < nc; ++a) s = fma(Zc[(size_t)i * nc + a], Q[a * nc + col], s);
-        Zs[(size_t)i * kMaxN + j0 + k] = s;
+        Zs[(size_t)i * zst + j0 + k] = s;
       }
       __syncthreads();
     }
@@ -1418,7 +1427,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const int r = r0 + q * rs;
-            v[q] = (a && r < N) ? Zs[(size_t)r * kMaxN + j] : 0.0;
+            v[q] = (a && r < N) ? Zs[(size_t)r * zst + j] : 0.0;
           }
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -1441,12 +1450,12 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
       for (int q = 0; q < 4; ++q) {
         const int j = c0 + warp + kNW * q;
         act[q] = (j < J) && (wgt[j] != T(0));
-        const double* zg = Zs + (act[q] ? j : 0);
+        const ZT* zg = Zs + (act[q] ? j : 0);
         const double zs = act[q] ? (double)pvec[j] : 0.0;
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
           const int R = 32 * t + lane;
-          z[q][t] = (act[q] && R < N) ? (T)(zg[(size_t)R * kMaxN] * zs) : T(0);
+          z[q][t] = (act[q] && R < N) ? (T)(zg[(size_t)R * zst] * zs) : T(0);
         }
       }
       const bool any = act[0] || act[1] || act[2] || act[3];
