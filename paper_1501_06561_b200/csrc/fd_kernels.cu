@@ -282,11 +282,14 @@ __global__ void __launch_bounds__(256, 1) recon_pipe2_kernel(const Prob* __restr
       cp_async16(Bs + kr * kRc2BLd + nq, src, ok ? 16 : 0);
     }
   };
-  float acc[16][8];
+  // column pairs (2q, 2q+1) of the thread tile: packed FFMA2 (fma.rn.f32x2) with the
+  // A value as a broadcast scalar operand -- half the FMA instructions of FFMA, same
+  // flops and the same rounding (one fma per element)
+  float2 acc[16][4];
 #pragma unroll
   for (int i = 0; i < 16; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    for (int q = 0; q < 4; ++q) acc[i][q] = make_float2(0.f, 0.f);
 #pragma unroll
   for (int st = 0; st < kRc2Stages - 1; ++st) {
     if (st < nk) issue(st);
@@ -308,12 +311,14 @@ __global__ void __launch_bounds__(256, 1) recon_pipe2_kernel(const Prob* __restr
       for (int u = 0; u < 2; ++u) {
         const float4 b0 = *reinterpret_cast<const float4*>(&Bs[(kk + u) * kRc2BLd + 4 * lane]);
         const float4 b1 = *reinterpret_cast<const float4*>(&Bs[(kk + u) * kRc2BLd + 128 + 4 * lane]);
-        const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+        const float2 bb[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                              make_float2(b1.z, b1.w)};
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const float av = u ? a[i].y : a[i].x;
+          const float2 a2 = make_float2(av, av);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av, bb[j], acc[i][j]);
+          for (int q = 0; q < 4; ++q) acc[i][q] = __ffma2_rn(a2, bb[q], acc[i][q]);
         }
       }
     }
@@ -328,7 +333,7 @@ __global__ void __launch_bounds__(256, 1) recon_pipe2_kernel(const Prob* __restr
     for (int h = 0; h < 2; ++h) {
       const int c = 128 * h + 4 * lane;
       if (n0 + c >= p.ldb) continue;
-      const float4 o = (j < jrows) ? make_float4(acc[i][4 * h], acc[i][4 * h + 1], acc[i][4 * h + 2], acc[i][4 * h + 3])
+      const float4 o = (j < jrows) ? make_float4(acc[i][2 * h].x, acc[i][2 * h].y, acc[i][2 * h + 1].x, acc[i][2 * h + 1].y)
                                    : make_float4(0.f, 0.f, 0.f, 0.f);
       *reinterpret_cast<float4*>(dst + c) = o;
     }

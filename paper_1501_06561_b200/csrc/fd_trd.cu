@@ -46,7 +46,11 @@ struct TrdCfg {
   static_assert(2 * kFree >= NB, "not enough diagonal slots");
   static_assert(kThreads >= NM, "P4 needs a thread per row");
   static_assert(NB <= 8, "the alpha / sigma reductions assume at most 8 row blocks");
+  // resident CTAs per SM (the tail variant runs several problems per SM)
+  static constexpr int kMinBlocks = (NM <= 128) ? 3 : 1;
 };
+
+constexpr int kTrdTail = 128;   // trailing size handed from the head to the tail stage
 
 // sub-column cc (0..3) of a lane block row
 __device__ __forceinline__ float pick4(const float (&x)[4], int cc) {
@@ -136,9 +140,16 @@ __device__ __forceinline__ void tile_update(float (&t)[8][4], int r0, int c0, co
   }
 }
 
+// Staging (mode): the latency-bound steps of a large problem run at one CTA per SM,
+// its last kTrdTail steps at several.  mode 0: the whole reduction.  mode 1 (head,
+// NM > kTrdTail): steps 0 .. N-kTrdTail-1, then the trailing matrix
+// A^(N-kTrdTail-1)[N-kTrdTail:, N-kTrdTail:] (lower triangle, row-major, ld kTrdTail)
+// goes to the problem's Wt scratch (free until eig_kernel).  mode 2 (tail,
+// NM == kTrdTail): the remaining steps from that matrix (from G when N <= kTrdTail).
+// Householder vectors and d / e / tau keep the global (problem) indexing.
 template <int NM>
-__global__ void __launch_bounds__(TrdCfg<NM>::kThreads, 1)
-trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
+__global__ void __launch_bounds__(TrdCfg<NM>::kThreads, TrdCfg<NM>::kMinBlocks)
+trd_kernel(const Prob* __restrict__ probs, int count, Params p, int mode) {
   using C = TrdCfg<NM>;
   constexpr int NB = C::NB, W = C::kWarps;
   extern __shared__ __align__(16) float s_dyn[];    // diagonal tiles (full): s_dg[NB][32][32]
@@ -175,8 +186,20 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
   if (tid < (W + 3) / 4 * 4) s_xax[tid] = 0.f;   // padding stays zero
   for (int pi = blockIdx.x; pi < count; pi += gridDim.x) {
     const Prob P = probs[pi];
-    const int N = P.rows0 + P.rows1;
-    float* G = static_cast<float*>(P.G);
+    const int NG = P.rows0 + P.rows1;            // problem size (global indexing)
+    // this launch's steps: global s0 + local 0 .. send-1 on the local N x N matrix
+    int s0 = 0, send;
+    if (mode == 1) {
+      send = NG - kTrdTail;                      // local == global (s0 = 0)
+      if (send <= 0) continue;                   // the tail stage does all of it
+    } else {
+      if (mode == 2) s0 = NG > kTrdTail ? NG - kTrdTail : 0;
+      send = NG - s0 - 2;
+    }
+    const int N = NG - s0;
+    float* Vout = static_cast<float*>(P.G);       // packed reflectors + d / e / tau (global)
+    const float* G = (s0 > 0) ? static_cast<const float*>(P.Wt) : static_cast<const float*>(P.G);
+    const int64_t ldin = (s0 > 0) ? kTrdTail : p.ldg;
     // ---------------- load (zero outside N) ----------------
     float a0[8][4], a1[8][4];
     auto load_blk = [&](int TI, int TJ, float (&t)[8][4]) {
@@ -185,7 +208,7 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
       for (int k = 0; k < 8; ++k) {
         const int r = 32 * TI + 8 * rg + k;
         float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (r < N && c0 < N) x = *reinterpret_cast<const float4*>(G + (int64_t)r * p.ldg + c0);
+        if (r < N && c0 < N) x = *reinterpret_cast<const float4*>(G + (int64_t)r * ldin + c0);
         t[k][0] = x.x;
         t[k][1] = (c0 + 1 < N) ? x.y : 0.f;
         t[k][2] = (c0 + 2 < N) ? x.z : 0.f;
@@ -205,13 +228,13 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
     // and the partial sums of squares of its rows >= 2, per 32-row block
     if (warp < NB) {
       const int r = tid;
-      const float c = (r < N) ? G[(int64_t)r * p.ldg] : 0.f;
+      const float c = (r < N) ? G[(int64_t)r * ldin] : 0.f;
       s_x[r] = (r >= 1) ? c : 0.f;
       if (r == 0) s_d[0] = c;
       s_sq[r] = (r >= 2 && r < N) ? c * c : 0.f;
       s_v[r] = 0.f;
       s_w[r] = 0.f;
-      if (r == N - 1) s_dlast = G[(int64_t)r * p.ldg + r];
+      if (r == N - 1) s_dlast = G[(int64_t)r * ldin + r];
     }
     __syncthreads();  // G fully read before V overwrites it
     // diagonal tiles: mirror the lower triangle (the tensor-core Gram is symmetric
@@ -225,8 +248,7 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
       }
     }
     __syncthreads();
-    float* Vout = G;
-    const int offd = (N * (N + 1) / 2 + 3) / 4 * 4;
+    const int offd = (NG * (NG + 1) / 2 + 3) / 4 * 4;
     long long t_ph = clock64(), t_st = t_ph;
     const int cn = (N - 1) >> 5, ccn = (N - 1) & 3;
 
@@ -237,7 +259,7 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
     // off the critical path: the SYMV does not need the reflector).  The Householder x_s
     // differs from x~_s only in row s+1 (alpha - beta instead of alpha): the SYMV
     // runs on x~_s and phase B adds delta * A[:, s+1] (the look-ahead column).
-    for (int s = 0; s <= N - 3; ++s) {
+    for (int s = 0; s < send; ++s) {
       const int cs1 = (s + 1) >> 5, cc1 = (s + 1) & 3, cg1 = ((s + 1) & 31) >> 2;
       const bool last = (s == N - 3);
       float tau_s, scale, amb, beta_s, al;
@@ -359,7 +381,7 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
         s_v[r] = vr;
         s_w[r] = wr;
         s_x[r] = (r >= s + 2) ? col : 0.f;
-        if (r >= s + 2 && r < N) Vout[pk_off_t(s, N) - s + r] = vr;   // Householder vector s
+        if (r >= s + 2 && r < N) Vout[pk_off_t(s0 + s, NG) - s + r] = vr;   // Householder vector s0 + s
         if (r == s) { s_e[s] = beta_s; s_tau[s] = tau_s; }
         if (r == s + 1) s_d[s + 1] = col;
         s_sq[r] = (r >= s + 3 && r < N) ? col * col : 0.f;
@@ -371,6 +393,49 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
         p.dbg[12] += t_ - t_ph; t_ph = t_; p.dbg[14] += 1;
         p.dbg[20 + min(3, s / 64)] += t_ - t_st; t_st = t_;
       }
+    }
+    if (mode == 1) {
+      // ---------------- head: hand the trailing matrix A^(send-1)[send:, send:] to the tail ----------------
+      float* T = static_cast<float*>(P.Wt);
+      auto put_blk = [&](const float (&t)[8][4], int TI, int TJ) {   // lower entries r >= c >= send
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int r = 32 * TI + 8 * rg + k;
+          if (r < send || r >= N) continue;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int cc = 32 * TJ + 4 * cg + c;
+            if (cc >= send && cc <= r) T[(int64_t)(r - send) * kTrdTail + (cc - send)] = t[k][c];
+          }
+        }
+      };
+      if (ov[0] && 32 * oJ[0] + 31 >= send) {
+        tile_update<false>(a0, 32 * oI[0] + 8 * rg, 32 * oJ[0] + 4 * cg, s_v, s_w);
+        put_blk(a0, oI[0], oJ[0]);
+      }
+      if (ov[1] && 32 * oJ[1] + 31 >= send) {
+        tile_update<false>(a1, 32 * oI[1] + 8 * rg, 32 * oJ[1] + 4 * cg, s_v, s_w);
+        put_blk(a1, oI[1], oJ[1]);
+      }
+      _Pragma("unroll") for (int q = 0; q < 2; ++q) {
+        if (q >= nd) break;
+        const int D = dT[q];
+        if (32 * D + 31 < send) continue;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float4 x = *reinterpret_cast<const float4*>(&s_dg[D][8 * rg + k][4 * cg]);
+          a1[k][0] = x.x; a1[k][1] = x.y; a1[k][2] = x.z; a1[k][3] = x.w;
+        }
+        tile_update<true>(a1, 32 * D + 8 * rg, 32 * D + 4 * cg, s_v, s_w);
+        put_blk(a1, D, D);
+      }
+      for (int r = tid; r < send; r += blockDim.x) {
+        Vout[offd + r] = s_d[r];
+        Vout[offd + NG + r] = s_e[r];
+        Vout[offd + 2 * NG + r] = s_tau[r];
+      }
+      __syncthreads();
+      continue;
     }
     // ---------------- last entries, outputs ----------------
     if (tid == 0) {
@@ -384,21 +449,22 @@ trd_kernel(const Prob* __restrict__ probs, int count, Params p) {
     }
     __syncthreads();
     for (int r = tid; r < N; r += blockDim.x) {
-      Vout[offd + r] = s_d[r];
-      Vout[offd + N + r] = s_e[r];
-      Vout[offd + 2 * N + r] = s_tau[r];
+      Vout[offd + s0 + r] = s_d[r];
+      Vout[offd + NG + s0 + r] = s_e[r];
+      Vout[offd + 2 * NG + s0 + r] = s_tau[r];
     }
     __syncthreads();
   }
 }
 
 template <int NM>
-static cudaError_t launch_trd_t(const Prob* dev_probs, int count, const Params& p, cudaStream_t s) {
+static cudaError_t launch_trd_t(const Prob* dev_probs, int count, const Params& p, int mode, cudaStream_t s) {
   constexpr int dyn = TrdCfg<NM>::NB * 32 * 32 * (int)sizeof(float);
   static AttrOnce once;
   if (cudaError_t e = once.ensure(trd_kernel<NM>, dyn); e != cudaSuccess) return e;
-  const int grid = count < kNumSMs ? count : kNumSMs;
-  trd_kernel<NM><<<grid, TrdCfg<NM>::kThreads, dyn, s>>>(dev_probs, count, p);
+  const int slots = kNumSMs * TrdCfg<NM>::kMinBlocks;
+  const int grid = count < slots ? count : slots;
+  trd_kernel<NM><<<grid, TrdCfg<NM>::kThreads, dyn, s>>>(dev_probs, count, p, mode);
   return cudaGetLastError();
 }
 
@@ -406,10 +472,14 @@ bool trd_supported(int nmax, const Params& p) { return !p.f64 && nmax > 32 && nm
 
 cudaError_t launch_trd(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
-  if (nmax <= 64) return launch_trd_t<64>(dev_probs, count, p, s);
-  if (nmax <= 128) return launch_trd_t<128>(dev_probs, count, p, s);
-  if (nmax <= 192) return launch_trd_t<192>(dev_probs, count, p, s);
-  return launch_trd_t<256>(dev_probs, count, p, s);
+  if (nmax <= 64) return launch_trd_t<64>(dev_probs, count, p, 0, s);
+  if (nmax <= kTrdTail) return launch_trd_t<kTrdTail>(dev_probs, count, p, 0, s);
+  // head at one CTA per SM, then the last kTrdTail steps of every problem at
+  // TrdCfg<kTrdTail>::kMinBlocks CTAs per SM (requires Wt slots of >= kTrdTail^2 floats:
+  // wt_rows >= 128 and ldg >= nmax > kTrdTail)
+  cudaError_t e = (nmax <= 192) ? launch_trd_t<192>(dev_probs, count, p, 1, s) : launch_trd_t<256>(dev_probs, count, p, 1, s);
+  if (e != cudaSuccess) return e;
+  return launch_trd_t<kTrdTail>(dev_probs, count, p, 2, s);
 }
 
 }  // namespace fdk

@@ -21,6 +21,29 @@ __global__ void __launch_bounds__(1024) fma_kernel(T* out, int iters) {
   if (s == (T)-1) out[0] = s;
 }
 
+// packed fp32 FMA (FFMA2, fma.rn.f32x2): 8 independent float2 chains per thread
+__global__ void __launch_bounds__(1024) fma2_kernel(float* out, int iters) {
+  unsigned long long a[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float2 v = make_float2((float)(threadIdx.x + j), (float)(threadIdx.x - j));
+    a[j] = *reinterpret_cast<const unsigned long long*>(&v);
+  }
+  const float2 bf = make_float2(0.999999f, 0.999998f), cf = make_float2(1e-7f, 2e-7f);
+  const unsigned long long b = *reinterpret_cast<const unsigned long long*>(&bf);
+  const unsigned long long c = *reinterpret_cast<const unsigned long long*>(&cf);
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(a[j]) : "l"(b), "l"(c));
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float2 v = *reinterpret_cast<const float2*>(&a[j]);
+    s += v.x + v.y;
+  }
+  if (s == -1.f) out[0] = s;
+}
+
 // one CTA per SM; one thread issues M=128 x N=256 x K=8 tf32 MMAs back to back from
 // resident SW128 smem tiles into TMEM, committing every 32 MMAs to an mbarrier
 __global__ void __launch_bounds__(128, 1) tf32_kernel(int iters, int* sink) {
@@ -76,6 +99,13 @@ int main() {
   cudaEventSynchronize(e1);
   cudaEventElapsedTime(&ms, e0, e1);
   const double ffma = 2.0 * 8 * it * (double)sms * 2 * 1024 / (ms * 1e-3) / 1e12;
+  fma2_kernel<<<sms * 2, 1024>>>((float*)out, 16);
+  cudaEventRecord(e0);
+  fma2_kernel<<<sms * 2, 1024>>>((float*)out, it);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double ffma2 = 4.0 * 8 * it * (double)sms * 2 * 1024 / (ms * 1e-3) / 1e12;
   fma_kernel<double><<<sms * 2, 1024>>>((double*)out, 16);
   cudaEventRecord(e0);
   fma_kernel<double><<<sms * 2, 1024>>>((double*)out, it / 8);
@@ -94,9 +124,9 @@ int main() {
   cudaEventElapsedTime(&ms, e0, e1);
   const double tf32 = 2.0 * 128 * 256 * 8 * 32.0 * ti * sms / (ms * 1e-3) / 1e12;
   cudaError_t err = cudaGetLastError();
-  printf("{\"ffma_tflops\": %.2f, \"dfma_tflops\": %.2f, \"tf32_tcgen05_tflops\": %.2f, \"tf32x3_tflops\": %.2f, "
-         "\"error\": \"%s\", \"how\": \"tools/micro/peaks.cu: 296x1024 threads x 8 independent FMA chains (FFMA, DFMA); "
+  printf("{\"ffma_tflops\": %.2f, \"ffma2_tflops\": %.2f, \"dfma_tflops\": %.2f, \"tf32_tcgen05_tflops\": %.2f, \"tf32x3_tflops\": %.2f, "
+         "\"error\": \"%s\", \"how\": \"tools/micro/peaks.cu: 296x1024 threads x 8 independent FMA chains (FFMA, FFMA2 = fma.rn.f32x2, DFMA); "
          "148 CTAs each issuing back-to-back tcgen05.mma.kind::tf32 M128 N256 K8 from resident smem tiles, CUDA events\"}\n",
-         ffma, dfma, tf32, tf32 / 3.0, cudaGetErrorString(err));
+         ffma, ffma2, dfma, tf32, tf32 / 3.0, cudaGetErrorString(err));
   return 0;
 }
