@@ -126,20 +126,24 @@ __global__ void __launch_bounds__(kBtThreads, 1) bt_kernel(const Prob* __restric
       if (grp == 0) {
         // ---- W1 = V_b^T Z (thread: 4 reflectors x 4 columns, all rows) ----
         const int cb = 4 * wg8, jb = 4 * lane;
-        float acc[4][4] = {};
+        float2 acc[4][2];   // column pairs on packed FFMA2, the V entries as broadcast scalars
+#pragma unroll
+        for (int a = 0; a < 4; ++a) acc[a][0] = acc[a][1] = make_float2(0.f, 0.f);
 #pragma unroll 4
         for (int r = r0; r < N; ++r) {
           const float4 zz = *reinterpret_cast<const float4*>(&Zs[r * kZld + jb]);
           const float4 vv = *reinterpret_cast<const float4*>(&VbT[r * kVt + cb]);
-          const float za[4] = {zz.x, zz.y, zz.z, zz.w}, va[4] = {vv.x, vv.y, vv.z, vv.w};
+          const float2 z01 = make_float2(zz.x, zz.y), z23 = make_float2(zz.z, zz.w);
+          const float va[4] = {vv.x, vv.y, vv.z, vv.w};
 #pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) acc[a][q] = fmaf(va[a], za[q], acc[a][q]);
+          for (int a = 0; a < 4; ++a) {
+            acc[a][0] = __ffma2_rn(make_float2(va[a], va[a]), z01, acc[a][0]);
+            acc[a][1] = __ffma2_rn(make_float2(va[a], va[a]), z23, acc[a][1]);
+          }
         }
 #pragma unroll
         for (int a = 0; a < 4; ++a)
-          *reinterpret_cast<float4*>(&W1[(cb + a) * 128 + jb]) = make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
+          *reinterpret_cast<float4*>(&W1[(cb + a) * 128 + jb]) = make_float4(acc[a][0].x, acc[a][0].y, acc[a][1].x, acc[a][1].y);
       } else {
         // ---- S = V_b^T V_b (thread: row a, columns c4..c4+3), then T = U^-1 ----
         const int t = tid - 256, a = t >> 3, c4 = 4 * (t & 7);
@@ -204,17 +208,18 @@ __global__ void __launch_bounds__(kBtThreads, 1) bt_kernel(const Prob* __restric
         const int jb = 4 * lane;
         if (jb < Jp) {  // columns >= Jp of Z are zero
           for (int rbase = r0 + 8 * warp; rbase < N; rbase += 8 * (kBtThreads / 32)) {
-            float acc[8][4] = {};
+            float2 acc[8][2];
+#pragma unroll
+            for (int a = 0; a < 8; ++a) acc[a][0] = acc[a][1] = make_float2(0.f, 0.f);
 #pragma unroll 4
             for (int k = 0; k < kNbBt; ++k) {
               const float4 w4 = *reinterpret_cast<const float4*>(&W2[k * 128 + jb]);
+              const float2 w01 = make_float2(w4.x, w4.y), w23 = make_float2(w4.z, w4.w);
 #pragma unroll
               for (int a = 0; a < 8; ++a) {
                 const float v = VbT[(rbase + a) * kVt + k];   // rows >= N: never stored
-                acc[a][0] = fmaf(v, w4.x, acc[a][0]);
-                acc[a][1] = fmaf(v, w4.y, acc[a][1]);
-                acc[a][2] = fmaf(v, w4.z, acc[a][2]);
-                acc[a][3] = fmaf(v, w4.w, acc[a][3]);
+                acc[a][0] = __ffma2_rn(make_float2(v, v), w01, acc[a][0]);
+                acc[a][1] = __ffma2_rn(make_float2(v, v), w23, acc[a][1]);
               }
             }
 #pragma unroll
@@ -222,7 +227,7 @@ __global__ void __launch_bounds__(kBtThreads, 1) bt_kernel(const Prob* __restric
               const int r = rbase + a;
               if (r < N) {
                 float4 z = *reinterpret_cast<float4*>(&Zs[r * kZld + jb]);
-                z.x -= acc[a][0]; z.y -= acc[a][1]; z.z -= acc[a][2]; z.w -= acc[a][3];
+                z.x -= acc[a][0].x; z.y -= acc[a][0].y; z.z -= acc[a][1].x; z.w -= acc[a][1].y;
                 *reinterpret_cast<float4*>(&Zs[r * kZld + jb]) = z;
               }
             }

@@ -62,12 +62,16 @@ __device__ __forceinline__ float pick4(const float (&x)[4], int cc) {
 // lane-local part of x_I^T T x_J (its 8 x 4 block) in dot.
 __device__ __forceinline__ float col_sums(const float (&a)[8][4], const float (&vr)[8], const float (&vc)[4],
                                           int lane, float& dot) {
-  float cs[4] = {0.f, 0.f, 0.f, 0.f};
+  float cs[4];
+  {   // column pairs on packed FFMA2 (the row values as broadcast scalars)
+    float2 c01 = make_float2(0.f, 0.f), c23 = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const float vk = vr[k];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) cs[c] = fmaf(a[k][c], vk, cs[c]);
+    for (int k = 0; k < 8; ++k) {
+      const float2 vk = make_float2(vr[k], vr[k]);
+      c01 = __ffma2_rn(make_float2(a[k][0], a[k][1]), vk, c01);
+      c23 = __ffma2_rn(make_float2(a[k][2], a[k][3]), vk, c23);
+    }
+    cs[0] = c01.x; cs[1] = c01.y; cs[2] = c23.x; cs[3] = c23.y;
   }
   dot = fmaf(cs[3], vc[3], fmaf(cs[2], vc[2], fmaf(cs[1], vc[1], cs[0] * vc[0])));
   const bool hb = (lane >> 4) & 1;
@@ -87,13 +91,11 @@ __device__ __forceinline__ float col_sums(const float (&a)[8][4], const float (&
 // (lanes ^4, ^2, ^1); lane (rg, cg) returns row 8rg + cg.
 __device__ __forceinline__ float row_sums(const float (&a)[8][4], const float (&vc)[4], int lane) {
   float rs[8];
+  const float2 v01 = make_float2(vc[0], vc[1]), v23 = make_float2(vc[2], vc[3]);
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    float x = a[k][0] * vc[0];
-    x = fmaf(a[k][1], vc[1], x);
-    x = fmaf(a[k][2], vc[2], x);
-    x = fmaf(a[k][3], vc[3], x);
-    rs[k] = x;
+  for (int k = 0; k < 8; ++k) {   // (a0 v0 + a2 v2) + (a1 v1 + a3 v3): FMUL2 + FFMA2 + FADD
+    const float2 x = __ffma2_rn(make_float2(a[k][2], a[k][3]), v23, __fmul2_rn(make_float2(a[k][0], a[k][1]), v01));
+    rs[k] = x.x + x.y;
   }
   const bool b2 = (lane >> 2) & 1;
 #pragma unroll
@@ -132,10 +134,24 @@ __device__ __forceinline__ void tile_update(float (&t)[8][4], int r0, int c0, co
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const float vr = vrs[k], wr = wrs[k];
+    if (DIAG) {   // exactly symmetric: round(round(v_r w_c) + round(w_r v_c)), no contraction
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      if (DIAG) t[k][c] -= vr * wc[c] + wr * vc[c];   // exactly symmetric
-      else t[k][c] = fmaf(-wr, vc[c], fmaf(-vr, wc[c], t[k][c]));
+      for (int c = 0; c < 4; c += 2) {
+        const float2 s2 = __fadd2_rn(__fmul2_rn(make_float2(vr, vr), make_float2(wc[c], wc[c + 1])),
+                                     __fmul2_rn(make_float2(wr, wr), make_float2(vc[c], vc[c + 1])));
+        const float2 x = __fadd2_rn(make_float2(t[k][c], t[k][c + 1]), make_float2(-s2.x, -s2.y));
+        t[k][c] = x.x;
+        t[k][c + 1] = x.y;
+      }
+    } else {   // column pairs on packed FFMA2, the row values as broadcast scalars
+#pragma unroll
+      for (int c = 0; c < 4; c += 2) {
+        float2 x = make_float2(t[k][c], t[k][c + 1]);
+        x = __ffma2_rn(make_float2(-vr, -vr), make_float2(wc[c], wc[c + 1]), x);
+        x = __ffma2_rn(make_float2(-wr, -wr), make_float2(vc[c], vc[c + 1]), x);
+        t[k][c] = x.x;
+        t[k][c + 1] = x.y;
+      }
     }
   }
 }

@@ -11,5 +11,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 5000 --
 echo "ncu launch rc=$?" >> gpurun_out/ncu_launch.log
 timeout 300 python tools/prof_c4.py > gpurun_out/prof_c4_plain.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:trd_kernel|eig_kernel|bt_kernel|gram_tc|recon|ingest" \
-  -s 48 -c 6 -o gpurun_out/c4_full python tools/prof_c4.py > gpurun_out/ncu_full.log 2>&1
+  -s 56 -c 7 -o gpurun_out/c4_full python tools/prof_c4.py > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc=$?" >> gpurun_out/ncu_full.log
