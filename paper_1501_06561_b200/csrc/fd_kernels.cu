@@ -1537,7 +1537,9 @@ cudaError_t launch_eig(const Prob* dev_probs, int count, const Params& p, double
     return launch_eig_t<float, kMaxNS, false, true>(dev_probs, count, p, scratch, s);
   }
   if (p.zld <= kMaxNS) return launch_eig_t<float, kMaxNS, false>(dev_probs, count, p, scratch, s);
-  return launch_eig_t<float, kMaxN, true>(dev_probs, count, p, scratch, s);
+  // above kMaxNS (c3 ell = 200 merges, N = 398): wide spectra put 100+ eigenvalues in
+  // one cluster -> the panel block CGS2 (BIG)
+  return launch_eig_t<float, kMaxN, true, false, true>(dev_probs, count, p, scratch, s);
 }
 
 // ============================================================================
