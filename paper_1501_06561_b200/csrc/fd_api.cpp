@@ -291,6 +291,8 @@ Prob make_prob(fd_handle* h, int slot, const float* s0, int r0, const float* s1,
 
   p.stats = st;
   p.child0 = c0; p.child1 = c1;
+  p.ld1 = h->D.ldb;
+  p.acc1 = 0;
   return p;
 }
 
@@ -408,6 +410,7 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
   h->ws = static_cast<char*>(ws);
   h->stream = static_cast<cudaStream_t>(cuda_stream);
   h->device = cfg->device;
+  h->prm.nonfinite = nullptr;   // set below with the flag
   h->prm.d = D.d; h->prm.ldb = D.ldb; h->prm.ldg = D.ldg; h->prm.ell = D.ell; h->prm.rule = D.rule; h->prm.m = D.m;
   h->prm.ret = D.R; h->prm.tdel = D.t; h->prm.comp = 0; h->prm.merge = 0;
   h->prm.f64 = 0;
@@ -434,6 +437,7 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
 
   h->stats = reinterpret_cast<Stats*>(h->ws + Lo.stats);
   h->flag = reinterpret_cast<int*>(h->ws + Lo.flag);
+  h->prm.nonfinite = h->flag;
   h->eig = reinterpret_cast<double*>(h->ws + Lo.eig);
   h->state = D.prk ? reinterpret_cast<double*>(h->ws + Lo.state) : nullptr;
   h->arena = h->ws + Lo.arena;
@@ -640,6 +644,15 @@ static fd_status append_impl(fd_handle* h, const float* rows, int64_t n_rows, in
     plan_round(pocc, pst, prm, cur_ch);
     if (!cur_ch.empty()) { fd_status e0 = stage_round(cur_ch, 0); if (e0 != FD_OK) return e0; }
   }
+  // Rows that complete a buffer are read in place by the round's Gram and reconstruct
+  // (Prob.src1 = the rows themselves, ld1 = ld; the tcgen05 Gram accumulates their
+  // ||a||^2 and non-finite flag): only rows that stay in a buffer past this call are
+  // copied by ingest_kernel.  Needs 16-byte rows (ld % 4 == 0, aligned base, d == ldb)
+  // and the tcgen05 Gram; Compensative FD keeps full buffers across calls (lazy
+  // ReduceRank, reading C27) and always copies.
+  const bool direct = !h->D.cfd && !h->simt_gram && !use_f64(h->D, L) &&
+                      fdk::gram_tc_supported(L, h->prm) && (ld % 4) == 0 && h->D.d == h->D.ldb &&
+                      (reinterpret_cast<uintptr_t>(host ? stage : rows) % 16) == 0 && getenv("FD_INGEST_COPY") == nullptr;
   std::vector<Ingest> ing;
   std::vector<Prob> probs;
   ing.reserve(P);
@@ -653,19 +666,33 @@ static fd_status append_impl(fd_handle* h, const float* rows, int64_t n_rows, in
     for (int s = 0; s < P; ++s) {
       if (rem[s] == 0) continue;
       const int c = (int)std::min<int64_t>(L - h->occ[s], rem[s]);
+      const float* src = host ? stage + (size_t)(round & 1) * slot_floats + (size_t)ci * maxc * ld : rows + start[s] * ld;
+      ++ci;
+      start[s] += c;
+      rem[s] -= c;
+      const int occ0 = h->occ[s];
+      h->occ[s] += c;
+      const bool full = h->occ[s] == L && (!h->D.cfd || rem[s] > 0);   // CFD: lazy (reading C27)
+      if (full && direct) {   // [buffer rows 0..occ0) ; the c new rows in place
+        const int slot = (int)probs.size();
+        Prob pr = make_prob(h, slot, shard_buf(h, s, h->cur[s]), occ0, src, c, shard_buf(h, s, h->cur[s] ^ 1),
+                            h->stats + s);
+        pr.ld1 = ld;
+        pr.acc1 = 1;
+        probs.push_back(pr);
+        h->cur[s] ^= 1;
+        h->occ[s] = h->D.R;
+        continue;
+      }
       Ingest g;
-      g.src = host ? stage + (size_t)(round & 1) * slot_floats + (size_t)ci * maxc * ld : rows + start[s] * ld;
+      g.src = src;
       g.ld = ld;
-      g.dst = shard_buf(h, s, h->cur[s]) + (size_t)h->occ[s] * h->D.ldb;
+      g.dst = shard_buf(h, s, h->cur[s]) + (size_t)occ0 * h->D.ldb;
       g.nrows = c;
       g.pad = 0;
       g.stats = h->stats + s;
       ing.push_back(g);
-      ++ci;
-      start[s] += c;
-      rem[s] -= c;
-      h->occ[s] += c;
-      if (h->occ[s] == L && (!h->D.cfd || rem[s] > 0)) {   // CFD: lazy (reading C27)
+      if (full) {
         const int slot = (int)probs.size();
         probs.push_back(make_prob(h, slot, shard_buf(h, s, h->cur[s]), L, nullptr, 0, shard_buf(h, s, h->cur[s] ^ 1),
                                   h->stats + s));
@@ -673,22 +700,26 @@ static fd_status append_impl(fd_handle* h, const float* rows, int64_t n_rows, in
         h->occ[s] = h->D.R;
       }
     }
-    if (ing.empty()) break;
+    if (ing.empty() && probs.empty()) break;
     if (host) {
       // stage the next round while this one computes
       plan_round(pocc, pst, prm, next_ch);
       if (!next_ch.empty()) { fd_status e1 = stage_round(next_ch, (round + 1) & 1); if (e1 != FD_OK) return e1; }
       FD_CUDA(cudaStreamWaitEvent(h->stream, h->ev_copied[round & 1], 0));
     }
-    const Ingest* di = nullptr;
-    fd_status st = push_desc(h, ing, &di);
-    if (st != FD_OK) return st;
-    const int ni = (int)ing.size();
-    cudaError_t e = timed(h, K_INGEST, [&] { return fdk::launch_ingest(di, ni, h->prm, h->flag, h->stream); });
-    if (e != cudaSuccess) return cuda_fail(e, "ingest");
-    if (host) FD_CUDA(cudaEventRecord(h->ev_consumed[round & 1], h->stream));
+    fd_status st = FD_OK;
+    if (!ing.empty()) {
+      const Ingest* di = nullptr;
+      st = push_desc(h, ing, &di);
+      if (st != FD_OK) return st;
+      const int ni = (int)ing.size();
+      cudaError_t e = timed(h, K_INGEST, [&] { return fdk::launch_ingest(di, ni, h->prm, h->flag, h->stream); });
+      if (e != cudaSuccess) return cuda_fail(e, "ingest");
+    }
     st = run_reduce(h, probs);
     if (st != FD_OK) return st;
+    // the staged rows were read by the ingest and (in place) by the round's Gram / reconstruct
+    if (host) FD_CUDA(cudaEventRecord(h->ev_consumed[round & 1], h->stream));
     if (host) cur_ch.swap(next_ch);
     ++round;
   }

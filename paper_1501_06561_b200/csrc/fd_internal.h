@@ -34,6 +34,9 @@ struct Prob {
   Stats* stats;  // accumulates delta / removed / shrinks of this ReduceRank
   const Stats* child0;  // merges: stats = child0 + child1 before accumulating
   const Stats* child1;
+  int64_t ld1;   // row stride of src1 (floats): Params.ldb, or the caller's ld when src1 is A itself
+  int acc1;      // 1: src1 rows are new stream rows read in place from A (no ingest copy) --
+                 // the Gram adds their fp64 sum of squares to stats->frob and flags non-finite values
 };
 
 // One shard stream's rows of an append call for the persistent per-row kernel
@@ -78,6 +81,7 @@ struct Params {
   int pretrd;    // 1: the Gram scratch already holds the tridiagonal form (trd_kernel)
   int zld;       // eig_kernel fp64 scratch stride (>= every problem size of the handle)
   long long* dbg;  // optional phase clock trace of problem 0 (FD_DEBUG_EIG), else null
+  int* nonfinite;  // sticky device flag (Prob.acc1 rows)
 };
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) applies to the current device

@@ -97,7 +97,7 @@ cudaError_t launch_ingest(const Ingest* dev_desc, int count, const Params& p, in
 __device__ __forceinline__ const float* prob_row(const Prob& P, int r, int64_t ldb) {
   if (r < P.rows0) return P.src0 + (int64_t)r * ldb;
   r -= P.rows0;
-  if (r < P.rows1) return P.src1 + (int64_t)r * ldb;
+  if (r < P.rows1) return P.src1 + (int64_t)r * P.ld1;
   return nullptr;
 }
 

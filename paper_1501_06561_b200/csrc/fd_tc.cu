@@ -24,10 +24,16 @@ constexpr int kTcThreads = 256;
 constexpr int kTile = 256 * 128;   // bytes of one 256-row x 32-value SW128 tile
 constexpr int kAccs = 4;           // K-split accumulators of the NP = 128 Gram (4 x 128 TMEM columns)
 
+__device__ __forceinline__ double warp_sum_d_tc(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 __device__ __forceinline__ const float* row_ptr(const Prob& P, int r, int64_t ldb) {
   if (r < P.rows0) return P.src0 + (int64_t)r * ldb;
   r -= P.rows0;
-  return P.src1 + (int64_t)r * ldb;
+  return P.src1 + (int64_t)r * P.ld1;
 }
 
 // load 32-column K-chunk kc of rows [0, NP) of Bf (zero outside N / ldb) into registers
@@ -90,12 +96,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) gram_tc_kernel(const Prob* __re
   const uint32_t id1 = tc::idesc_tf32(128, 256, 0, 0);
   constexpr int NI = NP * 8 / kTcThreads;
 
+  __shared__ double s_fr[kTcThreads / 32];
   for (int pi = blockIdx.x; pi < count; pi += gridDim.x) {
     const Prob P = probs[pi];
     const int N = P.rows0 + P.rows1;
     const int nk = (int)((p.ldb + 31) / 32);
+    // new rows read in place from A (Prob.acc1): ||a||^2 in fp64 and the non-finite
+    // check ride on the staging loads (the ingest pass of row 1 of SURVEY 8(a))
+    double fr = 0.0;
+    bool bad = false;
+    auto acc_rows = [&](const float4 (&v)[NI]) {
+#pragma unroll
+      for (int j = 0; j < NI; ++j) {
+        const int r = (threadIdx.x + kTcThreads * j) >> 3;
+        if (r >= P.rows0) {   // zero outside N
+          bad |= !(isfinite(v[j].x) && isfinite(v[j].y) && isfinite(v[j].z) && isfinite(v[j].w));
+          fr += (double)v[j].x * v[j].x + (double)v[j].y * v[j].y + (double)v[j].z * v[j].z + (double)v[j].w * v[j].w;
+        }
+      }
+    };
     float4 x[NI];
     gram_load<NP>(P, N, p.ldb, 0, x);
+    if (P.acc1) acc_rows(x);
     gram_store<NP>(sm, sm + kTile, x);
     tc::fence_async_smem();
     __syncthreads();
@@ -127,6 +149,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gram_tc_kernel(const Prob* __re
       }
       if (kc + 1 < nk) {
         gram_load<NP>(P, N, p.ldb, kc + 1, x);
+        if (P.acc1) acc_rows(x);
         const int nb = b ^ 1;
         if (kc >= 1) {  // buffer nb was read by the MMAs of chunk kc-1
           tc::mbar_wait(&mbar[nb], uses[nb] & 1);
@@ -145,6 +168,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) gram_tc_kernel(const Prob* __re
       ++uses[bl];
     }
     tc::fence_after_sync();
+    if (P.acc1) {   // fixed-order reduction: lanes, then warps (deterministic)
+      fr = warp_sum_d_tc(fr);
+      if (lane == 0) s_fr[warp] = fr;
+      bad = __syncthreads_or(bad);
+      if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kTcThreads / 32; ++w) t += s_fr[w];
+        P.stats->frob += t;
+        if (bad && p.nonfinite) atomicOr(p.nonfinite, 1);
+      }
+    }
     // epilogue: warps 0-3 hold TMEM lanes 0-127 (= tile rows)
     if (warp < 4) {
       float* G = static_cast<float*>(P.G);
