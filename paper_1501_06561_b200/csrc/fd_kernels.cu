@@ -1546,29 +1546,37 @@ cudaError_t launch_eig(const Prob* dev_probs, int count, const Params& p, double
 // Evaluator: AtA += A^T A (fp64 products / accumulation), one CTA per 64x64
 // lower tile, fixed row order -> deterministic.
 // ============================================================================
-// fp64 SYRK: 64 x 64 lower-triangular tiles of A^T A (products of fp32 values are
-// exact in fp64), rows split into `nch` contiguous chunks so every SM holds several
-// CTAs (d = 1024: 136 tiles x 7 chunks).  Chunk c of tile t writes its partial to
-// part[(c * ntiles + t) * 4096] (nch > 1) or adds straight into AtA (nch == 1); the
-// partials are summed in chunk order by syrk_reduce_kernel (deterministic).
-__global__ void __launch_bounds__(256) syrk_f64_kernel(const float* __restrict__ A, int64_t n, int64_t ld,
-                                                       int64_t d, double* __restrict__ AtA, double* __restrict__ part,
-                                                       int nch) {
+// fp64 SYRK: 128 x 128 lower-triangular tiles of A^T A (products of fp32 values are
+// exact in fp64), rows split into `nch` contiguous chunks (several waves of one CTA
+// per SM).  Thread tile 8 x 8 (rows 32 x' + 2 ty + e, columns 32 y' + 2 tx + f): per
+// K row 4 + 4 conflict-free double2 shared loads feed 64 DFMA.  K steps of 8 rows,
+// the next step's fp32 values register-prefetched (one float4 per operand per
+// thread).  Chunk c of tile t writes its partial to part[(c * ntiles + t) * 16384]
+// (nch > 1) or adds straight into AtA (nch == 1); the partials are summed in chunk
+// order by syrk_reduce_kernel (deterministic).
+constexpr int kSyT = 128;               // tile edge
+constexpr int kSyK = 8;                 // rows per K step
+constexpr int kSyLd = kSyT + 2;         // smem row stride (doubles)
+
+__global__ void __launch_bounds__(256, 1) syrk_f64_kernel(const float* __restrict__ A, int64_t n, int64_t ld,
+                                                          int64_t d, double* __restrict__ AtA,
+                                                          double* __restrict__ part, int nch) {
   int ti, tj;
   tri_index(blockIdx.x, ti, tj);
   const int ntiles = gridDim.x, ch = blockIdx.y;
   const int64_t rows_per = (n + nch - 1) / nch;
   const int64_t rbeg = (int64_t)ch * rows_per, rend = min(n, rbeg + rows_per);
-  const int64_t i0 = (int64_t)ti * 64, j0 = (int64_t)tj * 64;
-  __shared__ __align__(16) double As[16][68];
-  __shared__ __align__(16) double Bs[16][68];
+  const int64_t i0 = (int64_t)ti * kSyT, j0 = (int64_t)tj * kSyT;
+  __shared__ __align__(16) double As[2][kSyK][kSyLd];
+  __shared__ __align__(16) double Bs[2][kSyK][kSyLd];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  double acc[4][4];
+  double acc[8][8];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < 8; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  const int lrow = threadIdx.x >> 4, lcol = (threadIdx.x & 15) * 4;
+    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+  // staging: thread -> (row lr of the K step, 4 columns lc..lc+3) of each operand tile
+  const int lr = threadIdx.x >> 5, lc = (threadIdx.x & 31) * 4;
   const bool vec = ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
   auto load = [&](int64_t r, int64_t c0, float (&v)[4]) {
     if (r < rend && vec && c0 + 3 < d) {
@@ -1580,43 +1588,50 @@ __global__ void __launch_bounds__(256) syrk_f64_kernel(const float* __restrict__
     }
   };
   float va[4], vb[4];
-  load(rbeg + lrow, i0 + lcol, va);
-  load(rbeg + lrow, j0 + lcol, vb);
-  for (int64_t r0 = rbeg; r0 < rend; r0 += 16) {
+  load(rbeg + lr, i0 + lc, va);
+  load(rbeg + lr, j0 + lc, vb);
+  int buf = 0;
+  for (int64_t r0 = rbeg; r0 < rend; r0 += kSyK) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) { As[lrow][lcol + q] = (double)va[q]; Bs[lrow][lcol + q] = (double)vb[q]; }
+    for (int q = 0; q < 4; ++q) { As[buf][lr][lc + q] = (double)va[q]; Bs[buf][lr][lc + q] = (double)vb[q]; }
     __syncthreads();
-    if (r0 + 16 < rend) {           // prefetch the next 16 rows while this block computes
-      load(r0 + 16 + lrow, i0 + lcol, va);
-      load(r0 + 16 + lrow, j0 + lcol, vb);
+    if (r0 + kSyK < rend) {           // prefetch the next K step while this one computes
+      load(r0 + kSyK + lr, i0 + lc, va);
+      load(r0 + kSyK + lr, j0 + lc, vb);
     }
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const double2 a01 = *reinterpret_cast<const double2*>(&As[k][ty * 4]);
-      const double2 a23 = *reinterpret_cast<const double2*>(&As[k][ty * 4 + 2]);
-      const double2 b01 = *reinterpret_cast<const double2*>(&Bs[k][tx * 4]);
-      const double2 b23 = *reinterpret_cast<const double2*>(&Bs[k][tx * 4 + 2]);
-      const double a[4] = {a01.x, a01.y, a23.x, a23.y}, b[4] = {b01.x, b01.y, b23.x, b23.y};
+    for (int k = 0; k < kSyK; ++k) {
+      double a[8], b[8];
 #pragma unroll
-      for (int x = 0; x < 4; ++x)
+      for (int x = 0; x < 4; ++x) {
+        const double2 u = *reinterpret_cast<const double2*>(&As[buf][k][32 * x + 2 * ty]);
+        const double2 v = *reinterpret_cast<const double2*>(&Bs[buf][k][32 * x + 2 * tx]);
+        a[2 * x] = u.x; a[2 * x + 1] = u.y;
+        b[2 * x] = v.x; b[2 * x + 1] = v.y;
+      }
 #pragma unroll
-        for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+      for (int x = 0; x < 8; ++x)
+#pragma unroll
+        for (int y = 0; y < 8; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
     }
-    __syncthreads();
+    buf ^= 1;   // the other buffer is written next; the barrier above orders the reuse
   }
+  auto row_of = [&](int x) { return 32 * (x >> 1) + 2 * ty + (x & 1); };
+  auto col_of = [&](int y) { return 32 * (y >> 1) + 2 * tx + (y & 1); };
   if (nch > 1) {
-    double* P = part + ((size_t)ch * ntiles + blockIdx.x) * 4096;
+    double* P = part + ((size_t)ch * ntiles + blockIdx.x) * (kSyT * kSyT);
 #pragma unroll
-    for (int x = 0; x < 4; ++x)
+    for (int x = 0; x < 8; ++x)
 #pragma unroll
-      for (int y = 0; y < 4; ++y) P[(ty * 4 + x) * 64 + tx * 4 + y] = acc[x][y];
+      for (int y = 0; y < 8; y += 2)
+        *reinterpret_cast<double2*>(&P[row_of(x) * kSyT + col_of(y)]) = make_double2(acc[x][y], acc[x][y + 1]);
     return;
   }
 #pragma unroll
-  for (int x = 0; x < 4; ++x)
+  for (int x = 0; x < 8; ++x)
 #pragma unroll
-    for (int y = 0; y < 4; ++y) {
-      const int64_t i = i0 + ty * 4 + x, j = j0 + tx * 4 + y;
+    for (int y = 0; y < 8; ++y) {
+      const int64_t i = i0 + row_of(x), j = j0 + col_of(y);
       if (i < d && j < d) {
         AtA[i * d + j] += acc[x][y];
         if (ti != tj) AtA[j * d + i] += acc[x][y];
@@ -1629,10 +1644,10 @@ __global__ void __launch_bounds__(256) syrk_reduce_kernel(const double* __restri
   int ti, tj;
   tri_index(blockIdx.x, ti, tj);
   const int ntiles = gridDim.x;
-  for (int e = threadIdx.x; e < 4096; e += blockDim.x) {
+  for (int e = threadIdx.x; e < kSyT * kSyT; e += blockDim.x) {
     double s = 0.0;
-    for (int c = 0; c < nch; ++c) s += part[((size_t)c * ntiles + blockIdx.x) * 4096 + e];
-    const int64_t i = (int64_t)ti * 64 + (e >> 6), j = (int64_t)tj * 64 + (e & 63);
+    for (int c = 0; c < nch; ++c) s += part[((size_t)c * ntiles + blockIdx.x) * (kSyT * kSyT) + e];
+    const int64_t i = (int64_t)ti * kSyT + e / kSyT, j = (int64_t)tj * kSyT + e % kSyT;
     if (i < d && j < d) {
       AtA[i * d + j] += s;
       if (ti != tj) AtA[j * d + i] += s;
@@ -1641,23 +1656,23 @@ __global__ void __launch_bounds__(256) syrk_reduce_kernel(const double* __restri
 }
 
 int syrk_chunks(int64_t n, int64_t d) {
-  const int nt = (int)((d + 63) / 64);
+  const int nt = (int)((d + kSyT - 1) / kSyT);
   const int ntiles = nt * (nt + 1) / 2;
-  int nch = (6 * kNumSMs + ntiles - 1) / ntiles;     // ~6 CTAs per SM
-  nch = std::min<int64_t>(nch, std::max<int64_t>(1, n / 256));
-  return std::max(1, std::min(nch, 16));
+  int nch = (4 * kNumSMs + ntiles - 1) / ntiles;     // ~4 waves of one CTA per SM
+  nch = std::min<int64_t>(nch, std::max<int64_t>(1, n / 1024));
+  return std::max(1, std::min(nch, 32));
 }
 
 size_t syrk_partial_bytes(int64_t n, int64_t d) {
   const int nch = syrk_chunks(n, d);
   if (nch <= 1) return 0;
-  const int nt = (int)((d + 63) / 64);
-  return (size_t)nch * (nt * (nt + 1) / 2) * 4096 * sizeof(double);
+  const int nt = (int)((d + kSyT - 1) / kSyT);
+  return (size_t)nch * (nt * (nt + 1) / 2) * (kSyT * kSyT) * sizeof(double);
 }
 
 cudaError_t launch_syrk_f64(const float* A, int64_t n, int64_t ld, int64_t d, double* AtA, double* part,
                             size_t part_bytes, cudaStream_t s) {
-  const int nt = (int)((d + 63) / 64);
+  const int nt = (int)((d + kSyT - 1) / kSyT);
   const int ntiles = nt * (nt + 1) / 2;
   int nch = syrk_chunks(n, d);
   if (nch > 1 && (!part || part_bytes < syrk_partial_bytes(n, d))) nch = 1;
