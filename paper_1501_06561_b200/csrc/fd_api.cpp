@@ -182,7 +182,7 @@ struct fd_handle {
   bool dead;
   bool legacy_trd;    // FD_LEGACY_TRD set: tridiagonalise inside eig_kernel (A/B checks)
   bool simt_gemm;     // FD_SIMT_GEMM set: FP32 SIMT Gram / reconstruct instead of tcgen05 (A/B checks)
-  bool simt_gram, simt_recon, simt_bt;  // per-GEMM variants (FD_SIMT_GRAM; FD_TC_RECON opts into the TC reconstruct)
+  bool simt_gram, simt_recon;  // per-GEMM variants (FD_SIMT_GRAM; FD_TC_RECON opts into the TC reconstruct)
   // live profiling: event pairs around launches
   bool prof;
   struct Rec { int kind; cudaEvent_t a, b; };
@@ -270,10 +270,7 @@ fd_status run_reduce(fd_handle* h, const std::vector<Prob>& probs, bool comp = f
     return cuda_fail(e, "trd");
   if ((e = timed(h, K_EIG, [&] { return fdk::launch_eig(dp, n, prm, h->eig, h->stream); })) != cudaSuccess)
     return cuda_fail(e, "eig");
-  const bool tc_bt = !h->simt_bt && fdk::bt_tc_supported(nmax, prm);
-  if (prm.pretrd && (e = timed(h, K_BT, [&] {
-                       return tc_bt ? fdk::launch_bt_tc(dp, n, prm, h->stream) : fdk::launch_bt(dp, n, prm, h->stream);
-                     })) != cudaSuccess)
+  if (prm.pretrd && (e = timed(h, K_BT, [&] { return fdk::launch_bt(dp, n, prm, h->stream); })) != cudaSuccess)
     return cuda_fail(e, "bt");
   const bool tc_recon = !h->simt_recon && fdk::recon_tc_supported(nmax, prm);
   if ((e = timed(h, K_RECON, [&] {
@@ -422,7 +419,6 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
   h->legacy_trd = getenv("FD_LEGACY_TRD") != nullptr;
   h->simt_gemm = getenv("FD_SIMT_GEMM") != nullptr;
   h->simt_gram = h->simt_gemm || getenv("FD_SIMT_GRAM") != nullptr;
-  h->simt_bt = h->simt_gemm || getenv("FD_SIMT_BT") != nullptr;
   // the tensor-core reconstruct is opt-in (accumulation bias, fd_tc.cu)
   h->simt_recon = h->simt_gemm || getenv("FD_TC_RECON") == nullptr;
   h->prm.dbg = nullptr;

@@ -118,9 +118,6 @@ cudaError_t launch_recon_tc(const Prob* dev_probs, int count, int nmax, const Pa
 cudaError_t launch_trd(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s);
 // Blocked (compact WY) back-transform + Wt = diag(w) U^T (fd_bt.cu), after eig when p.pretrd.
 cudaError_t launch_bt(const Prob* dev_probs, int count, const Params& p, cudaStream_t s);
-// the same back-transform on tcgen05 (fd_bt_tc.cu): the default when supported
-bool bt_tc_supported(int nmax, const Params& p);
-cudaError_t launch_bt_tc(const Prob* dev_probs, int count, const Params& p, cudaStream_t s);
 
 // Persistent per-row kernel (fd_perrow.cu): every row of an append call,
 // one thread-block cluster per shard stream, fp64 state, arrowhead eigen-updates.
