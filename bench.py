@@ -418,7 +418,10 @@ def run_ours(args):
     roof["traffic"] = None
     if os.path.exists(traffic_file):
         with open(traffic_file) as f:
-            tr = json.load(f).get(roof["kernel"])
+            trj = json.load(f)
+            # the captured launch names of the step kernels (tcgen05 Gram, pipelined reconstruct)
+            alias = {"gram_kernel": "gram_tc_kernel", "recon_kernel": "recon_pipe2_kernel"}
+            tr = trj.get(roof["kernel"]) or trj.get(alias.get(roof["kernel"], ""))
         if tr:
             # bytes per problem from the committed capture x problems per launch of this run
             roof["traffic"] = tr["bytes_per_problem"] * shrinks_per_step / max(kern[dom][1], 1) * args.steps
