@@ -410,7 +410,7 @@ struct EigCfg {
   static constexpr int kNWc = (PRE ? 256 : kEigThreads) / 32;
   static constexpr size_t kCgs = (size_t)(kNWc * (NM + 1) + NM) * sizeof(double);
   static_assert(PRE || (size_t)kPart * sizeof(T) >= kCgs, "CGS scratch must fit the SYMV workspaces");
-  static constexpr size_t kBytes = kT * sizeof(T) + (4 * NM + kNWc * 32) * sizeof(int) + NM * sizeof(double) + 16 +
+  static constexpr size_t kBytes = kT * sizeof(T) + (4 * NM + kNWc * 32) * sizeof(int) + 2 * NM * sizeof(double) + 16 +
                                    (PRE ? kCgs : 0);
 };
 
@@ -691,7 +691,8 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
   int* ccnt = ord + NM;                       // [kNT] coarse bisection counts
   constexpr size_t kOffD = C::kT * sizeof(T) + (4 * NM + kNT) * sizeof(int);
   double* pscl = reinterpret_cast<double*>(smraw + kOffD + 8 - (kOffD & 7));  // per-vector scale (fp64)
-  double* cpart = PRE ? pscl + NM : reinterpret_cast<double*>(ppart);  // [kNW][kCpStride] block-CGS dots
+  double* lamd = pscl + NM;   // fp64 shifts of the inverse iteration (refined inside large clusters)
+  double* cpart = PRE ? pscl + 2 * NM : reinterpret_cast<double*>(ppart);  // [kNW][kCpStride] block-CGS dots
   __shared__ int s_ncl, s_jx, s_nrr;
   __shared__ T s_gl, s_gu, s_a1, s_a2;
 
@@ -1067,6 +1068,110 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
       s_ncl = ncl; s_jx = jx; s_nrr = nrr;
     }
     __syncthreads();
+    // fp64 shifts.  The fp32 Sturm counts resolve an eigenvalue only to ~eps32 ||T||, hence
+    // ctol; when ||T|| is dominated by a few large eigenvalues (merged sketches, the
+    // c3 pixel data's mean direction) the whole noise band falls inside ctol and the
+    // clusters reach 100+ members, whose block Gram-Schmidt dominates the solve.  Members
+    // of clusters larger than kSmallCl are re-bisected with fp64 Sturm counts inside
+    // lambda_j +- 2 ctol to ~1e-13 ||T|| and the clusters are rebuilt at 1e-10 ||T||
+    // (inverse-iteration vectors are accurate to ~(shift error) / gap).
+    for (int j = tid; j < s_jx; j += blockDim.x) lamd[j] = (double)lam[j];
+#ifndef FD_NO_REFINE
+    if constexpr (sizeof(T) == 4) {
+      bool big = false;
+      for (int c = 0; c < s_ncl; ++c) big |= clen[c] > kSmallCl;
+      if (big) {
+        // members of the large clusters -> ccnt[0..nbig) (the coarse counts are dead here)
+        __shared__ int s_nbig;
+        if (tid == 0) {
+          int nb = 0;
+          for (int c = 0; c < s_ncl; ++c)
+            if (clen[c] > kSmallCl)
+              for (int j = cstart[c]; j < cstart[c] + clen[c]; ++j) ccnt[nb++] = j;
+          s_nbig = nb;
+        }
+        __syncthreads();
+        const int nbig = s_nbig;
+        // multisection: g threads per member (aligned lane groups), 2 interleaved points
+        // each -> 2g + 1 sub-intervals per step, counts exchanged by ballot
+        int g = 1;
+        while (g < 8 && 2 * g * nbig <= (int)blockDim.x) g <<= 1;
+        const int mi = tid / g, sub = tid % g;
+        const unsigned gmask = (g == 32) ? 0xffffffffu : (((1u << g) - 1u) << ((lane / g) * g));
+        const int base = (lane / g) * g;
+        const double ctol = 1e-5 * (double)bnorm, pv = 1e-290, stop = 1e-12 * (double)bnorm;
+        const int j = (mi < nbig) ? ccnt[mi] : 0;
+        const int target = N - j;   // lambda_j is the target-th smallest
+        double lo = (double)lam[j] - 2.0 * ctol, hi = (double)lam[j] + 2.0 * ctol;
+        bool ok = mi < nbig;
+        auto cnt2 = [&](double x0, double x1, int& c0, int& c1) {
+          double q0 = (double)dd[0] - x0, q1 = (double)dd[0] - x1;
+          if (fabs(q0) < pv) q0 = -pv;
+          if (fabs(q1) < pv) q1 = -pv;
+          int n0 = q0 < 0.0, n1 = q1 < 0.0;
+          for (int i = 1; i < N; ++i) {
+            const double di = (double)dd[i], ei = (double)e2[i - 1];
+            q0 = (di - x0) - ei * rcp_d(q0);
+            q1 = (di - x1) - ei * rcp_d(q1);
+            if (fabs(q0) < pv) q0 = -pv;
+            if (fabs(q1) < pv) q1 = -pv;
+            n0 += q0 < 0.0;
+            n1 += q1 < 0.0;
+          }
+          c0 = n0;
+          c1 = n1;
+        };
+        {   // the bracket must hold lambda_j, else keep the fp32 value
+          int clo = 0, chi = N;
+          if (ok) cnt2(lo, hi, clo, chi);
+          ok = ok && clo < target && chi >= target;
+        }
+        const int P = 2 * g;
+        for (int it = 0; it < 64; ++it) {
+          const bool need = ok && (hi - lo > stop);
+          if (!__syncthreads_or(need)) break;
+          const double step = (hi - lo) / (double)(P + 1);
+          int c0 = 0, c1 = 0;
+          if (need) cnt2(lo + step * (double)(sub + 1), lo + step * (double)(sub + g + 1), c0, c1);
+          const unsigned m0 = __ballot_sync(0xffffffffu, need && c0 >= target) & gmask;
+          const unsigned m1 = __ballot_sync(0xffffffffu, need && c1 >= target) & gmask;
+          int ss = P;   // first point at or above lambda_j
+          if (m0) ss = __ffs(m0) - 1 - base;
+          else if (m1) ss = __ffs(m1) - 1 - base + g;
+          if (need) {
+            const double nlo = (ss == 0) ? lo : lo + step * (double)ss;
+            const double nhi = (ss == P) ? hi : lo + step * (double)(ss + 1);
+            lo = nlo;
+            hi = fmax(nhi, nlo);
+          }
+        }
+        if (ok && sub == 0) lamd[j] = fmax(0.5 * (lo + hi), 0.0);
+        __syncthreads();
+        if (tid == 0) {   // rebuild the clusters (same rules) on the fp64 shifts
+          const double ctol2 = 1e-10 * (double)bnorm;
+          const int bnd = (p.rule == RULE_ISVD) ? J : ((p.m < ell) ? ell - p.m : -1);
+          const int jx0 = s_jx;
+          int ncl = 0, jx = 0;
+          for (int j = 0; j < jx0; ++j) {
+            const bool cont = (j > 0) && (lamd[j - 1] - lamd[j] <= ctol2);
+            if (!cont) {
+              if (j >= J) break;
+              cstart[ncl] = j; clen[ncl] = 0; ++ncl;
+            }
+            clen[ncl - 1]++;
+            jx = j + 1;
+          }
+          int nrr = 0;
+          for (int c = 0; c < ncl; ++c) {
+            const int a = cstart[c], b = cstart[c] + clen[c];
+            if (bnd > a && bnd < b) cid[nrr++] = c;
+          }
+          s_ncl = ncl; s_jx = jx; s_nrr = nrr;
+        }
+      }
+    }
+#endif
+    __syncthreads();
     if (p.dbg && blockIdx.x == 0 && tid == 0) { const long long t_ = clock64(); p.dbg[4] += t_ - t_ph0; t_ph0 = t_; }
     // ---------------- eigenvectors of T: fp64 inverse iteration ----------------
     // One thread per vector j < JX (3 iterations, shift lam[j]); after every
@@ -1105,7 +1210,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
           ZT* lf = LF + j;   // lf[i * zst]: l_i (i < m), u_i (i >= m)
           ZT* z = Zs + j;    // z[i * zst]
           const double sc = pscl[j];
-          const double mu = (double)lam[j];
+          const double mu = lamd[j];
           auto rhs = [&](int i, double zi) -> double {
             return (it == 0) ? 1.0 + 0.5 * (double)(((i + 1) * 7919 + (j + 3) * 104729) % 211) / 211.0 : zi * sc;
           };
