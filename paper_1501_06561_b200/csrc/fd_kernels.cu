@@ -1570,18 +1570,30 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
       }
       const bool any = act[0] || act[1] || act[2] || act[3];
       if (any) {
-        for (int i = N - 3; i >= 0; --i) {
-          const T ti = tau[i];
-          if (ti == T(0)) continue;
+        // reflector i's entries are register-prefetched during reflector i+1 (the
+        // packed matrix sits in global / L2 scratch for N > kMaxNS: one L2 round trip
+        // per reflector otherwise serialises the loop)
+        auto vload = [&](int i, T (&v)[NT]) {
           const int base = pk_off(i, N) - i;
-          T v[NT];
-          T s[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
             const int R = 32 * t + lane;
-            v[t] = T(0);
-            if (32 * t + 31 < i + 1) continue;  // warp-uniform
             v[t] = (R == i + 1) ? T(1) : ((R > i + 1 && R < N) ? Apk[base + R] : T(0));
+          }
+        };
+        T vn[NT];
+        if (N >= 3) vload(N - 3, vn);
+        for (int i = N - 3; i >= 0; --i) {
+          T v[NT];
+#pragma unroll
+          for (int t = 0; t < NT; ++t) v[t] = vn[t];
+          if (i > 0) vload(i - 1, vn);
+          const T ti = tau[i];
+          if (ti == T(0)) continue;
+          T s[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            if (32 * t + 31 < i + 1) continue;  // warp-uniform
 #pragma unroll
             for (int q = 0; q < 4; ++q) s[q] = fma(v[t], z[q][t], s[q]);
           }
