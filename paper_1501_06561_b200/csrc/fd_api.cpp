@@ -174,6 +174,7 @@ struct fd_handle {
   cudaEvent_t ev[2];
   cudaStream_t copy_stream;     // host-input staging (fd_append_rows_host)
   cudaEvent_t ev_copied[2], ev_consumed[2];
+  cudaEvent_t ev_copied_desc;   // descriptor uploads on the copy stream (host-input path)
   int half;
   size_t half_used;
   size_t max_pitch;   // cudaDevAttrMaxPitch: larger 2-D copy pitches fall back to 1-D copies
@@ -198,21 +199,24 @@ float* shard_buf(fd_handle* h, int s, int which) { return h->buf[which] + (size_
 
 // Copy a block of descriptors to the device arena; returns the device pointer.
 template <typename T>
-fd_status push_desc(fd_handle* h, const std::vector<T>& v, const T** out) {
+fd_status push_desc(fd_handle* h, const std::vector<T>& v, const T** out, cudaStream_t sx = nullptr) {
+  if (!sx) sx = h->stream;   // the host-input path uploads on the copy stream (append_impl)
   const size_t bytes = align_up(v.size() * sizeof(T), 64);
   if (bytes > kArenaHalf) return fail(FD_ERR_INVALID_ARG, "descriptor batch larger than arena");
   if (h->half_used + bytes > kArenaHalf) {
-    // switch halves: the other half's previous H2D copy must be done before
-    // its pinned host mirror is overwritten
+    // switch halves: the other half's previous H2D copies (either stream) must be done
+    // before its pinned host mirror is overwritten
     FD_CUDA(cudaEventRecord(h->ev[h->half], h->stream));
+    FD_CUDA(cudaEventRecord(h->ev_copied_desc, h->copy_stream));
     h->half ^= 1;
     FD_CUDA(cudaEventSynchronize(h->ev[h->half]));
+    FD_CUDA(cudaEventSynchronize(h->ev_copied_desc));
     h->half_used = 0;
   }
   char* hp = h->host_arena + (size_t)h->half * kArenaHalf + h->half_used;
   char* dp = h->arena + (size_t)h->half * kArenaHalf + h->half_used;
   memcpy(hp, v.data(), v.size() * sizeof(T));
-  FD_CUDA(cudaMemcpyAsync(dp, hp, v.size() * sizeof(T), cudaMemcpyHostToDevice, h->stream));
+  FD_CUDA(cudaMemcpyAsync(dp, hp, v.size() * sizeof(T), cudaMemcpyHostToDevice, sx));
   h->half_used += bytes;
   *out = reinterpret_cast<const T*>(dp);
   return FD_OK;
@@ -243,13 +247,17 @@ cudaError_t timed(fd_handle* h, int kind, F f) {
   return e;
 }
 
-fd_status run_reduce(fd_handle* h, const std::vector<Prob>& probs, bool comp = false, bool merge = false) {
+fd_status run_reduce(fd_handle* h, const std::vector<Prob>& probs, bool comp = false, bool merge = false,
+                     const Prob* pushed = nullptr) {
   if (probs.empty()) return FD_OK;
   int nmax = 0;
   for (const Prob& p : probs) nmax = std::max(nmax, p.rows0 + p.rows1);
-  const Prob* dp = nullptr;
-  fd_status s = push_desc(h, probs, &dp);
-  if (s != FD_OK) return s;
+  const Prob* dp = pushed;
+  if (!dp) {
+    fd_status s = push_desc(h, probs, &dp);
+    if (s != FD_OK) return s;
+  }
+  fd_status s = FD_OK;
   const int n = (int)probs.size();
   Params prm = h->prm;
   prm.merge = merge ? 1 : 0;
@@ -460,6 +468,10 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
     e = cudaEventCreateWithFlags(&h->ev_copied[k], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_consumed[k], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventRecord(h->ev_consumed[k], h->stream);
+  }
+  if (e == cudaSuccess) {
+    e = cudaEventCreateWithFlags(&h->ev_copied_desc, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(h->ev_copied_desc, h->copy_stream);
   }
   if (e == cudaSuccess) e = cudaEventRecord(h->ev[0], h->stream);
   if (e == cudaSuccess) e = cudaEventRecord(h->ev[1], h->stream);
@@ -701,22 +713,30 @@ static fd_status append_impl(fd_handle* h, const float* rows, int64_t n_rows, in
       }
     }
     if (ing.empty() && probs.empty()) break;
+    // this round's descriptors go to the device before the next round's staging copy is
+    // enqueued: host -> device copies share the copy engine in issue order, and a small
+    // descriptor upload queued behind a ~1 GB staging copy would hold the round back
+    // (host input: on the copy stream, behind this round's staging copy and ahead of the
+    // next one; the compute stream waits for both)
+    fd_status st = FD_OK;
+    const Ingest* di = nullptr;
+    const Prob* dp = nullptr;
+    cudaStream_t ds = host ? h->copy_stream : h->stream;
+    if (!ing.empty() && (st = push_desc(h, ing, &di, ds)) != FD_OK) return st;
+    if (!probs.empty() && (st = push_desc(h, probs, &dp, ds)) != FD_OK) return st;
     if (host) {
+      FD_CUDA(cudaEventRecord(h->ev_copied_desc, h->copy_stream));   // staging of this round + descriptors
+      FD_CUDA(cudaStreamWaitEvent(h->stream, h->ev_copied_desc, 0));
       // stage the next round while this one computes
       plan_round(pocc, pst, prm, next_ch);
       if (!next_ch.empty()) { fd_status e1 = stage_round(next_ch, (round + 1) & 1); if (e1 != FD_OK) return e1; }
-      FD_CUDA(cudaStreamWaitEvent(h->stream, h->ev_copied[round & 1], 0));
     }
-    fd_status st = FD_OK;
     if (!ing.empty()) {
-      const Ingest* di = nullptr;
-      st = push_desc(h, ing, &di);
-      if (st != FD_OK) return st;
       const int ni = (int)ing.size();
       cudaError_t e = timed(h, K_INGEST, [&] { return fdk::launch_ingest(di, ni, h->prm, h->flag, h->stream); });
       if (e != cudaSuccess) return cuda_fail(e, "ingest");
     }
-    st = run_reduce(h, probs);
+    st = run_reduce(h, probs, false, false, dp);
     if (st != FD_OK) return st;
     // the staged rows were read by the ingest and (in place) by the round's Gram / reconstruct
     if (host) FD_CUDA(cudaEventRecord(h->ev_consumed[round & 1], h->stream));
@@ -849,6 +869,7 @@ fd_status fd_destroy(fd_handle* h) {
   cudaEventDestroy(h->ev[0]);
   cudaEventDestroy(h->ev[1]);
   for (int k = 0; k < 2; ++k) { cudaEventDestroy(h->ev_copied[k]); cudaEventDestroy(h->ev_consumed[k]); }
+  cudaEventDestroy(h->ev_copied_desc);
   cudaStreamDestroy(h->copy_stream);
   cudaFreeHost(h->host_arena);
   delete h;
