@@ -47,6 +47,7 @@ namespace fdk {
 namespace {
 
 constexpr int kPrThreads = 256;
+constexpr int kPrMaxCluster = 16;         // CTAs per stream (column slices of the state)
 constexpr int kPrMaxRows = 128;           // state rows the register tiles cover (16 groups x 8)
 constexpr int kPrColsPass = 64;           // columns per tile pass (16 lanes x 4)
 constexpr int kPL = 2 * kPrMaxRows + 2;   // partial vector: c[128], nrm[128], ||a||^2
@@ -265,10 +266,12 @@ size_t perrow_smem_bytes(int ell, int64_t d, int C) {
 
 // Cluster size of a per-row stream: enough CTAs that the state slice fits in shared
 // memory and the per-row reconstruct (~ell^2 dc fp64 FMAs per CTA) stays short.
+// Clusters above 8 CTAs are a non-portable size (opted into at launch); a 16-CTA
+// cluster fits in one B200 GPC.
 int perrow_cluster(int ell, int64_t d) {
   const double work = (double)ell * ell * (double)d;
   int C = 1;
-  while (C < 8 && (work / C > 65536.0 || perrow_smem_bytes(ell, d, C) > kPrSmemMax)) C *= 2;
+  while (C < kPrMaxCluster && (work / C > 32768.0 || perrow_smem_bytes(ell, d, C) > kPrSmemMax)) C *= 2;
   if (perrow_smem_bytes(ell, d, C) > kPrSmemMax) return 0;
   return C;
 }
@@ -396,12 +399,13 @@ perrow_kernel(const RowJob* __restrict__ jobs, Params p, int C, int lazy, int* _
     phase(1);
     for (int e = tid; e <= 2 * kPrMaxRows; e += kPrThreads) {
       const bool used = (e < k) || (e >= kPrMaxRows && e < kPrMaxRows + k) || e == 2 * kPrMaxRows;
-      double v[8];
+      double v[kPrMaxCluster];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) v[r] = (used && r < C) ? (r == crank ? pt : cluster.map_shared_rank(pt, r))[e] : 0.0;
+      for (int r = 0; r < kPrMaxCluster; ++r)
+        v[r] = (used && r < C) ? (r == crank ? pt : cluster.map_shared_rank(pt, r))[e] : 0.0;
       double s = 0.0;
 #pragma unroll
-      for (int r = 0; r < 8; ++r) s += v[r];
+      for (int r = 0; r < kPrMaxCluster; ++r) s += v[r];
       full[e] = s;
     }
     __syncthreads();
@@ -781,6 +785,17 @@ cudaError_t launch_perrow(const RowJob* dev_jobs, int count, const Params& p, in
   const int smem = (int)perrow_smem_bytes(p.ell, p.d, C);
   static AttrOnce once;
   if (cudaError_t e = once.ensure(perrow_kernel, smem); e != cudaSuccess) return e;
+  if (C > 8) {
+    static AttrOnce np;   // per device, like the smem attribute
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 64 || !((np.done >> dev) & 1ull)) {
+      if (cudaError_t e = cudaFuncSetAttribute(perrow_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+          e != cudaSuccess)
+        return e;
+      if (dev < 64) np.done |= 1ull << dev;
+    }
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(count * C));
   cfg.blockDim = dim3(kPrThreads);
