@@ -19,10 +19,17 @@ Workloads ("next round" item 1; BASELINE.json configs):
 A sharded run (P_total > 1) is computed shard by shard: shard s is
 `oracle.sketch(rows of shard s, n_shards=1)` -- the same stream + final
 ReduceRank that `oracle.sketch(A, n_shards=P)` runs for it (C10 ranges
-floor(n/P) + (s < n mod P)) -- cached under .golden_cache/ so the multi-hour c4
-runs resume, then merged with tests/oracle_tree.merge_tree (the oracle's own
+floor(n/P) + (s < n mod P)) -- cached under .golden_cache/ so the long runs
+resume, then merged with tests/oracle_tree.merge_tree (the oracle's own
 recursive-halving tree, pinned to oracle.merge in test_oracle_pins.py).  The
 cov-err's A^T A is oracle.gram over fixed row chunks, summed in chunk order.
+
+c4 (64 000 ReduceRanks of 256 x 1024 per variant) runs on oracle/alg1_svd.py,
+Alg. 1 with a library SVD as the paper itself runs it: the
+Jacobi oracle needs ~1.3 s per ReduceRank there (~7 CPU hours per variant), the
+SVD formulation ~0.05 s.  It is pinned to oracle.c's sketch and merge to fp64
+rounding in tests/test_oracle_pins.py (test_alg1_svd_*); shards and the tree run
+in worker threads with single-threaded BLAS.
 
     python tests/golden/make_goldens.py [--only KEY[,KEY..]] [--threads T]
 """
@@ -35,6 +42,10 @@ import os
 import sys
 import time
 
+# single-threaded BLAS: the parallelism is over shards / tree nodes
+for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -43,6 +54,7 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 import fdgen  # noqa: E402
 import oracle  # noqa: E402
+from oracle import alg1_svd  # noqa: E402
 from oracle_tree import merge_tree  # noqa: E402
 
 CACHE = os.path.join(ROOT, ".golden_cache")
@@ -63,7 +75,8 @@ def jobs_table():
         for v in ("fast_fd", "fast_alpha_fd"):
             J.append(dict(key=f"c3_{v}_l{ell}_p{C3_P}", cfg="c3", variant=v, ell=ell, alpha=0.2, P=C3_P))
     for v in ("fast_fd", "fast_alpha_fd"):
-        J.append(dict(key=f"c4_{v}_l128_p{C4_P}", cfg="c4", variant=v, ell=128, alpha=0.2, P=C4_P))
+        J.append(dict(key=f"c4_{v}_l128_p{C4_P}", cfg="c4", variant=v, ell=128, alpha=0.2, P=C4_P,
+                      engine="svd"))
     return J
 
 
@@ -92,10 +105,14 @@ def shard_task(job, w, s):
         return s
     r0, nr = shard_range(w.n, job["P"], s)
     A = fdgen.host_rows(w, r0, nr, nthreads=1)
-    res = oracle.sketch(A, job["ell"], job["variant"], alpha=job["alpha"], n_shards=1, nthreads=1)
-    st = np.array([res.frob_sq, res.delta_total, res.removed, res.n_shrinks, res.rows_seen])
+    if job.get("engine") == "svd":
+        B, st = alg1_svd.sketch_stream(A, job["ell"], job["variant"], alpha=job["alpha"])
+    else:
+        res = oracle.sketch(A, job["ell"], job["variant"], alpha=job["alpha"], n_shards=1, nthreads=1)
+        B = res.B
+        st = np.array([res.frob_sq, res.delta_total, res.removed, res.n_shrinks, res.rows_seen])
     tmp = path + ".tmp.npz"
-    np.savez(tmp, B=res.B, stats=st)
+    np.savez(tmp, B=B, stats=st)
     os.replace(tmp, path)
     return s
 
@@ -164,7 +181,10 @@ def run_job(job, threads, log):
                 z = np.load(os.path.join(CACHE, job["key"], f"shard_{s:05d}.npz"))
                 S[s] = z["B"]
                 stats += z["stats"]
-            B, mst = merge_tree(S, job["ell"], job["variant"], alpha=job["alpha"], nthreads=threads)
+            mf = None
+            if job.get("engine") == "svd":
+                mf = lambda X, Y: alg1_svd.merge(X, Y, job["ell"], job["variant"], alpha=job["alpha"])  # noqa: E731
+            B, mst = merge_tree(S, job["ell"], job["variant"], alpha=job["alpha"], nthreads=threads, merge_fn=mf)
             stats[1:4] += mst[1:4]
             del S
             G, f = full_gram(job["cfg"], w, ex)

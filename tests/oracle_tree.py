@@ -30,9 +30,10 @@ def _build(lo, hi, nodes):
     return len(nodes) - 1, h
 
 
-def merge_tree(sketches, ell, variant, alpha=None, nthreads=0, progress=None):
+def merge_tree(sketches, ell, variant, alpha=None, nthreads=0, progress=None, merge_fn=None):
     """Root of the recursive-halving tree over `sketches` (count x ell x d, fp64 or fp32)
-    with pairwise `oracle.merge`.  Returns (B, stats5) with stats5 = the merges' own
+    with pairwise `oracle.merge` (or `merge_fn(X, Y) -> (B, stats5)`, e.g.
+    oracle.alg1_svd.merge).  Returns (B, stats5) with stats5 = the merges' own
     [0, Delta, removed, n_shrinks, 0] summed (as `oracle.merge` reports them)."""
     S = np.asarray(sketches)
     count = S.shape[0]
@@ -47,7 +48,10 @@ def merge_tree(sketches, ell, variant, alpha=None, nthreads=0, progress=None):
 
     def run(i):
         a, b = nodes[i][1]
-        B, st = oracle.merge(np.stack([val[a], val[b]]), ell, variant, alpha=alpha)
+        if merge_fn is not None:
+            B, st = merge_fn(val[a], val[b])
+        else:
+            B, st = oracle.merge(np.stack([val[a], val[b]]), ell, variant, alpha=alpha)
         return i, B, st
 
     with cf.ThreadPoolExecutor(nthreads) as ex:

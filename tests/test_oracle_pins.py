@@ -613,3 +613,73 @@ def test_hash_sketch_unbiased_covariance():
     acc = np.array(acc)
     mean, se = acc.mean(0), acc.std(0) / np.sqrt(len(acc))
     assert np.all(np.abs(mean - AtA) <= 5 * se + 1e-9)
+
+
+# --------------------------------------------------------------------------
+# oracle/alg1_svd.py: Alg. 1 with a library SVD, used for the
+# c4 cached results.  Pinned to oracle.c's Gram + Jacobi formulation (independent:
+# no shared code, a different factorisation) and to the hand examples / bounds.
+# --------------------------------------------------------------------------
+from oracle import alg1_svd  # noqa: E402
+
+SVD_VARIANTS = ["fd", "fast_fd", "alpha_fd", "fast_alpha_fd", "isvd", "fast_isvd"]
+
+
+@pytest.mark.parametrize("variant", SVD_VARIANTS)
+def test_alg1_svd_matches_jacobi_oracle_c1(variant):
+    A = _c1()
+    B, st = alg1_svd.sketch_stream(A, 16, variant, alpha=0.2)
+    r = oracle.sketch(A, 16, variant, alpha=0.2)
+    assert np.abs(B.T @ B - r.B.T @ r.B).max() < 1e-11 * r.frob_sq
+    np.testing.assert_allclose(st, [r.frob_sq, r.delta_total, r.removed, r.n_shrinks, r.rows_seen],
+                               rtol=1e-11, atol=1e-11 * r.frob_sq)
+
+
+@pytest.mark.parametrize("variant", ["fast_fd", "fast_alpha_fd"])
+def test_alg1_svd_matches_jacobi_oracle_c4_shard(variant):
+    """A c4-shaped stream (d = 1024, ell = 128, L = 256): 400 rows (one buffer ReduceRank + the
+    final one), two 200-row shards and their merge."""
+    w = fdgen.config("c4")
+    A = fdgen.host_rows(w, 0, 400, nthreads=1)
+    B, st = alg1_svd.sketch_stream(A, 128, variant, alpha=0.2)
+    r = oracle.sketch(A, 128, variant, alpha=0.2, n_shards=2, want_shards=True)
+    X, sx = alg1_svd.sketch_stream(A[:200], 128, variant, alpha=0.2)
+    Y, sy = alg1_svd.sketch_stream(A[200:], 128, variant, alpha=0.2)
+    for S, ref in ((X, r.shards[0]), (Y, r.shards[1])):
+        assert np.linalg.norm(S.T @ S - ref.T @ ref, 2) < 1e-11 * r.frob_sq
+    M, sm = alg1_svd.merge(X, Y, 128, variant, alpha=0.2)
+    assert np.linalg.norm(M.T @ M - r.B.T @ r.B, 2) < 1e-11 * r.frob_sq
+    Mo, smo = oracle.merge(np.stack([r.shards[0], r.shards[1]]), 128, variant, alpha=0.2)
+    np.testing.assert_allclose(sm[1:4], smo[1:4], rtol=1e-10)
+    r1 = oracle.sketch(A, 128, variant, alpha=0.2)
+    assert np.linalg.norm(B.T @ B - r1.B.T @ r1.B, 2) < 1e-11 * r1.frob_sq
+    assert abs(st[1] - r1.delta_total) < 1e-10 * r1.delta_total and int(st[3]) == r1.n_shrinks
+
+
+@pytest.mark.parametrize("case", [c for c in _read_golden_rules() if c[0] in ("fd", "isvd")])
+def test_alg1_svd_hand_examples(case):
+    """The SPEC.md hand examples of the FD / alpha-FD / iSVD rules, on the SVD formulation."""
+    rule, alpha, ell, s_in, s_out, delta = case
+    L = len(s_in)
+    rng = np.random.default_rng(0)
+    Q, _ = np.linalg.qr(rng.standard_normal((L + 1, L + 1)))
+    Bf = np.diag(s_in) @ Q[:L]
+    m = ell if rule == "isvd" else max(1, int(np.floor(alpha * ell + 0.5)))
+    B, dl, removed = alg1_svd.reduce_rank(Bf, ell, "isvd" if rule == "isvd" else "fd", m)
+    sv = np.linalg.svd(B, compute_uv=False)
+    expect = np.zeros(len(sv))
+    expect[: len(s_out)] = s_out
+    np.testing.assert_allclose(sv ** 2, expect ** 2, atol=1e-12 * max(1.0, max(s_in) ** 2))
+    assert abs(dl - delta) < 1e-12 * max(1.0, max(s_in) ** 2)
+
+
+def test_alg1_svd_bounds_c2_prefix():
+    """Lemma 1 / Lemma 3 on the SVD formulation: 0 <= ||Ax||^2 - ||Bx||^2 <= Delta,
+    ||A||_F^2 - ||B||_F^2 = ell Delta (FD per-row)."""
+    w = fdgen.config("c2")
+    A = fdgen.host_rows(w, 0, 600, nthreads=1)
+    B, st = alg1_svd.sketch_stream(A, 20, "fd")
+    A64 = A.astype(np.float64)
+    ev = np.linalg.eigvalsh(A64.T @ A64 - B.T @ B)
+    assert ev[0] > -1e-10 * st[0] and ev[-1] <= st[1] * (1 + 1e-10)
+    assert abs(st[0] - np.sum(B ** 2) - 20 * st[1]) < 1e-10 * st[0]
