@@ -178,14 +178,19 @@ fd_status fd_destroy(fd_handle* h);
 /* Workspace bytes for the evaluator functions at dimension d. */
 size_t fd_cov_workspace_bytes(int64_t d);
 
-/* Scratch bytes fd_cov_gram_partial uses at (n, d) for its row-chunk partials (0: none). */
+/* Scratch bytes fd_cov_gram_partial needs at (n, d): the int8 digit planes of one row
+ * chunk (<= 512 MiB), the per-CTA fp64 partial tiles and the column maxima. */
 size_t fd_cov_gram_workspace_bytes(int64_t n, int64_t d);
 
 /* AtA [device] (d x d fp64, row-major, full symmetric) += A^T A for the n rows
- * of A [device] (fp32, ld).  Products of fp32 values are exact in fp64 and the
- * accumulation is fp64 in a fixed order (deterministic).  ws [device] of at least
- * fd_cov_gram_workspace_bytes(n, d) bytes lets the rows split into chunks that fill
- * the GPU (their partials are summed in chunk order); ws = NULL runs one chunk.
+ * of A [device] (fp32, ld) on the tensor cores (tcgen05 kind::i8; reading E3):
+ * per row chunk, column j is scaled by 2^(22 - e_j) (e_j = frexp exponent of the chunk's
+ * max |a_ij|) and rounded to an integer of <= 23 bits, split exactly into three int8
+ * digits; the digit products of weight 2^32, 2^24, 2^16 accumulate exactly in int32 TMEM
+ * accumulators and drain to fp64.  Error vs the exact fp64 A^T A: <= ~2^-22 of
+ * max|a_i| max|a_j| per row and term (~1e-11 of ||A||_F^2 in ||.||_2 on c4).  Fixed
+ * reduction order (deterministic).  A non-finite input makes AtA NaN.  ws [device]:
+ * fd_cov_gram_workspace_bytes(n, d) bytes (required: WORKSPACE otherwise).
  * Asynchronous. */
 fd_status fd_cov_gram_partial(const float* A, int64_t n, int64_t ld, int64_t d, double* AtA,
                               void* ws, size_t ws_bytes, void* cuda_stream);
@@ -230,14 +235,15 @@ size_t fd_proj_workspace_bytes(int64_t d, int32_t ell, int32_t k);
  * produced by fd_cov_gram_partial, summed over ranks) and frob_sq = ||A||_F^2
  * [host].  Outputs [host]: proj_err, num = ||A - pi_{B_k}(A)||_F^2 and
  * den = ||A - A_k||_F^2 (either may be NULL except proj_err).  1 <= k <= d.
- * Synchronises.  Errors: INVALID_ARG, ZERO_NORM (frob_sq <= 0, or den <= 0:
- * rank A <= k), WORKSPACE, CUDA. */
+ * Synchronises.  Errors: INVALID_ARG, ZERO_NORM (frob_sq <= 0, or den <= 1e-8 frob_sq:
+ * numerically rank A <= k, below the A^T A error of fd_cov_gram_partial), WORKSPACE, CUDA. */
 fd_status fd_proj_err_from_gram(const double* AtA, const float* B, int32_t ell, int64_t d, double frob_sq,
                                 int32_t k, double* proj_err, double* num, double* den,
                                 void* ws, size_t ws_bytes, void* cuda_stream);
 
 /* Single-GPU convenience: AtA from A [device] (fp32, ld), frob_sq = trace(A^T A),
- * then fd_proj_err_from_gram.  ws must hold fd_proj_workspace_bytes + d*d*8. */
+ * then fd_proj_err_from_gram.  ws must hold fd_proj_workspace_bytes + round_up(d*d*8, 256)
+ * + fd_cov_gram_workspace_bytes(n, d). */
 fd_status fd_proj_err(const float* A, int64_t n, int64_t ld, const float* B, int32_t ell, int64_t d, int32_t k,
                       double* proj_err, void* ws, size_t ws_bytes, void* cuda_stream);
 

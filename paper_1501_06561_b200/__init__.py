@@ -160,14 +160,14 @@ def _cov_ws(d, device):
 
 
 def cov_gram_partial(A, AtA, stream=None):
-    """AtA (d x d fp64 cuda) += A^T A (fp64 accumulation)."""
+    """AtA (d x d fp64 cuda) += A^T A (tcgen05 int8 slices, exact int32 sums, fp64 drains)."""
     torch = _torch()
     A = _as_rows(A, AtA.shape[0])
     s = stream if stream is not None else torch.cuda.current_stream(A.device)
     nb = lib().fd_cov_gram_workspace_bytes(A.shape[0], A.shape[1])
     ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=A.device)
     check(lib().fd_cov_gram_partial(A.data_ptr(), A.shape[0], A.stride(0), A.shape[1], AtA.data_ptr(),
-                                    ws.data_ptr() if nb else None, nb, s.cuda_stream))
+                                    ws.data_ptr(), nb, s.cuda_stream))
     return AtA
 
 
@@ -230,7 +230,7 @@ def proj_err(A, B, k=10, stream=None):
     A = _as_rows(A, d)
     B = B.contiguous()
     n = lib().fd_proj_workspace_bytes(int(d), int(B.shape[0]), int(k))
-    nb = n + (d * d * 8 + 255) // 256 * 256
+    nb = n + (d * d * 8 + 255) // 256 * 256 + lib().fd_cov_gram_workspace_bytes(A.shape[0], d)
     ws = torch.empty(nb, dtype=torch.uint8, device=A.device)
     s = stream if stream is not None else torch.cuda.current_stream(A.device)
     pe = ctypes.c_double()

@@ -128,13 +128,16 @@ cudaError_t launch_perrow(const RowJob* dev_jobs, int count, const Params& p, in
                           cudaStream_t s);
 
 // Evaluator.
-// AtA += A^T A (fp64); rows split into chunks whose partials (part, syrk_partial_bytes)
-// are summed in a fixed order; part == nullptr (or too small) -> one chunk, no partials
-int syrk_chunks(int64_t n, int64_t d);
-size_t syrk_partial_bytes(int64_t n, int64_t d);
-cudaError_t launch_syrk_f64(const float* A, int64_t n, int64_t ld, int64_t d, double* AtA, double* part,
-                            size_t part_bytes, cudaStream_t s);
+// AtA += A^T A on the tensor cores (fd_syrk_tc.cu: int8 digit planes of column-scaled
+// fixed-point A, tcgen05 kind::i8, exact int32 accumulation, fp64 drains); workspace
+// syrk_tc_workspace_bytes(n, d) (required)
+size_t syrk_tc_workspace_bytes(int64_t n, int64_t d);
+cudaError_t launch_syrk_tc(const float* A, int64_t n, int64_t ld, int64_t d, double* AtA, void* ws, size_t ws_bytes,
+                           cudaStream_t s);
 cudaError_t launch_sub_btb(double* M, const double* AtA, const float* B, int ell, int64_t d, cudaStream_t s);
+// Lanczos (fd_lanczos.cu): one cooperative grid, full re-orthogonalisation; work holds
+// lanczos_work_doubles(d, kmax) doubles, Q (kmax + 1) x d
+size_t lanczos_work_doubles(int64_t d, int kmax);
 cudaError_t launch_lanczos(const double* M, int64_t d, int kmax, double* Q, double* work, double* out2,
                            cudaStream_t s, int ntop = 0, double* top = nullptr);
 // Hashing / OSNAP (fd_hash.cu): B (ell x d fp64) += S A; partials: hash_ranges(d) * ell * d doubles

@@ -1659,145 +1659,6 @@ cudaError_t launch_eig(const Prob* dev_probs, int count, const Params& p, double
   return launch_eig_t<float, kMaxN, true, false, true>(dev_probs, count, p, scratch, s);
 }
 
-// ============================================================================
-// Evaluator: AtA += A^T A (fp64 products / accumulation), one CTA per 64x64
-// lower tile, fixed row order -> deterministic.
-// ============================================================================
-// fp64 SYRK: 128 x 128 lower-triangular tiles of A^T A (products of fp32 values are
-// exact in fp64), rows split into `nch` contiguous chunks (several waves of one CTA
-// per SM).  Thread tile 8 x 8 (rows 32 x' + 2 ty + e, columns 32 y' + 2 tx + f): per
-// K row 4 + 4 conflict-free double2 shared loads feed 64 DFMA.  K steps of 8 rows,
-// the next step's fp32 values register-prefetched (one float4 per operand per
-// thread).  Chunk c of tile t writes its partial to part[(c * ntiles + t) * 16384]
-// (nch > 1) or adds straight into AtA (nch == 1); the partials are summed in chunk
-// order by syrk_reduce_kernel (deterministic).
-constexpr int kSyT = 128;               // tile edge
-constexpr int kSyK = 8;                 // rows per K step
-constexpr int kSyLd = kSyT + 2;         // smem row stride (doubles)
-
-__global__ void __launch_bounds__(256, 1) syrk_f64_kernel(const float* __restrict__ A, int64_t n, int64_t ld,
-                                                          int64_t d, double* __restrict__ AtA,
-                                                          double* __restrict__ part, int nch) {
-  int ti, tj;
-  tri_index(blockIdx.x, ti, tj);
-  const int ntiles = gridDim.x, ch = blockIdx.y;
-  const int64_t rows_per = (n + nch - 1) / nch;
-  const int64_t rbeg = (int64_t)ch * rows_per, rend = min(n, rbeg + rows_per);
-  const int64_t i0 = (int64_t)ti * kSyT, j0 = (int64_t)tj * kSyT;
-  __shared__ __align__(16) double As[2][kSyK][kSyLd];
-  __shared__ __align__(16) double Bs[2][kSyK][kSyLd];
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  double acc[8][8];
-#pragma unroll
-  for (int a = 0; a < 8; ++a)
-#pragma unroll
-    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
-  // staging: thread -> (row lr of the K step, 4 columns lc..lc+3) of each operand tile
-  const int lr = threadIdx.x >> 5, lc = (threadIdx.x & 31) * 4;
-  const bool vec = ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
-  auto load = [&](int64_t r, int64_t c0, float (&v)[4]) {
-    if (r < rend && vec && c0 + 3 < d) {
-      const float4 x = __ldg(reinterpret_cast<const float4*>(A + r * ld + c0));
-      v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-    } else {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) v[q] = (r < rend && c0 + q < d) ? A[r * ld + c0 + q] : 0.f;
-    }
-  };
-  float va[4], vb[4];
-  load(rbeg + lr, i0 + lc, va);
-  load(rbeg + lr, j0 + lc, vb);
-  int buf = 0;
-  for (int64_t r0 = rbeg; r0 < rend; r0 += kSyK) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) { As[buf][lr][lc + q] = (double)va[q]; Bs[buf][lr][lc + q] = (double)vb[q]; }
-    __syncthreads();
-    if (r0 + kSyK < rend) {           // prefetch the next K step while this one computes
-      load(r0 + kSyK + lr, i0 + lc, va);
-      load(r0 + kSyK + lr, j0 + lc, vb);
-    }
-#pragma unroll
-    for (int k = 0; k < kSyK; ++k) {
-      double a[8], b[8];
-#pragma unroll
-      for (int x = 0; x < 4; ++x) {
-        const double2 u = *reinterpret_cast<const double2*>(&As[buf][k][32 * x + 2 * ty]);
-        const double2 v = *reinterpret_cast<const double2*>(&Bs[buf][k][32 * x + 2 * tx]);
-        a[2 * x] = u.x; a[2 * x + 1] = u.y;
-        b[2 * x] = v.x; b[2 * x + 1] = v.y;
-      }
-#pragma unroll
-      for (int x = 0; x < 8; ++x)
-#pragma unroll
-        for (int y = 0; y < 8; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
-    }
-    buf ^= 1;   // the other buffer is written next; the barrier above orders the reuse
-  }
-  auto row_of = [&](int x) { return 32 * (x >> 1) + 2 * ty + (x & 1); };
-  auto col_of = [&](int y) { return 32 * (y >> 1) + 2 * tx + (y & 1); };
-  if (nch > 1) {
-    double* P = part + ((size_t)ch * ntiles + blockIdx.x) * (kSyT * kSyT);
-#pragma unroll
-    for (int x = 0; x < 8; ++x)
-#pragma unroll
-      for (int y = 0; y < 8; y += 2)
-        *reinterpret_cast<double2*>(&P[row_of(x) * kSyT + col_of(y)]) = make_double2(acc[x][y], acc[x][y + 1]);
-    return;
-  }
-#pragma unroll
-  for (int x = 0; x < 8; ++x)
-#pragma unroll
-    for (int y = 0; y < 8; ++y) {
-      const int64_t i = i0 + row_of(x), j = j0 + col_of(y);
-      if (i < d && j < d) {
-        AtA[i * d + j] += acc[x][y];
-        if (ti != tj) AtA[j * d + i] += acc[x][y];
-      }
-    }
-}
-
-__global__ void __launch_bounds__(256) syrk_reduce_kernel(const double* __restrict__ part, int nch, int64_t d,
-                                                          double* __restrict__ AtA) {
-  int ti, tj;
-  tri_index(blockIdx.x, ti, tj);
-  const int ntiles = gridDim.x;
-  for (int e = threadIdx.x; e < kSyT * kSyT; e += blockDim.x) {
-    double s = 0.0;
-    for (int c = 0; c < nch; ++c) s += part[((size_t)c * ntiles + blockIdx.x) * (kSyT * kSyT) + e];
-    const int64_t i = (int64_t)ti * kSyT + e / kSyT, j = (int64_t)tj * kSyT + e % kSyT;
-    if (i < d && j < d) {
-      AtA[i * d + j] += s;
-      if (ti != tj) AtA[j * d + i] += s;
-    }
-  }
-}
-
-int syrk_chunks(int64_t n, int64_t d) {
-  const int nt = (int)((d + kSyT - 1) / kSyT);
-  const int ntiles = nt * (nt + 1) / 2;
-  int nch = (4 * kNumSMs + ntiles - 1) / ntiles;     // ~4 waves of one CTA per SM
-  nch = std::min<int64_t>(nch, std::max<int64_t>(1, n / 1024));
-  return std::max(1, std::min(nch, 32));
-}
-
-size_t syrk_partial_bytes(int64_t n, int64_t d) {
-  const int nch = syrk_chunks(n, d);
-  if (nch <= 1) return 0;
-  const int nt = (int)((d + kSyT - 1) / kSyT);
-  return (size_t)nch * (nt * (nt + 1) / 2) * (kSyT * kSyT) * sizeof(double);
-}
-
-cudaError_t launch_syrk_f64(const float* A, int64_t n, int64_t ld, int64_t d, double* AtA, double* part,
-                            size_t part_bytes, cudaStream_t s) {
-  const int nt = (int)((d + kSyT - 1) / kSyT);
-  const int ntiles = nt * (nt + 1) / 2;
-  int nch = syrk_chunks(n, d);
-  if (nch > 1 && (!part || part_bytes < syrk_partial_bytes(n, d))) nch = 1;
-  syrk_f64_kernel<<<dim3(ntiles, nch), 256, 0, s>>>(A, n, ld, d, AtA, part, nch);
-  if (nch > 1) syrk_reduce_kernel<<<ntiles, 256, 0, s>>>(part, nch, d, AtA);
-  return cudaGetLastError();
-}
-
 __global__ void sub_btb_kernel(double* __restrict__ M, const double* __restrict__ AtA, const float* __restrict__ B,
                                int ell, int64_t d) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1814,152 +1675,5 @@ cudaError_t launch_sub_btb(double* M, const double* AtA, const float* B, int ell
   return cudaGetLastError();
 }
 
-// Lanczos with full re-orthogonalisation (single CTA).  work layout (doubles):
-// alpha[kmax] | beta[kmax+1] | z[d] | h[kmax] | red[64]
-__device__ double block_sum_d(double v, double* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  v = warp_sum_d(v);
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  double s = 0.0;
-  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-  __syncthreads();
-  return s;
-}
-
-__device__ int sturm_count_d(const double* a, const double* b, int k, double x) {
-  int cnt = 0;
-  double q = a[0] - x;
-  const double piv = 1e-300;
-  if (fabs(q) < piv) q = -piv;
-  cnt += q < 0.0;
-  for (int i = 1; i < k; ++i) {
-    q = (a[i] - x) - b[i] * b[i] / q;
-    if (fabs(q) < piv) q = -piv;
-    cnt += q < 0.0;
-  }
-  return cnt;
-}
-
-__global__ void __launch_bounds__(1024, 1) lanczos_kernel(const double* __restrict__ M, int64_t d, int kmax,
-                                                          double* __restrict__ Q, double* __restrict__ work,
-                                                          double* __restrict__ out2, int ntop, double* __restrict__ top) {
-  double* alpha = work;
-  double* beta = alpha + kmax;       // beta[j] couples q_{j-1}, q_j (beta[0] unused)
-  double* z = beta + kmax + 1;
-  double* h = z + d;
-  __shared__ double red[32];
-  __shared__ int s_k;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  // q0
-  double ss = 0.0;
-  for (int64_t i = tid; i < d; i += blockDim.x) {
-    const double v = 1.0 + 0.001 * (double)((i * 7919) % 101);
-    Q[i] = v;
-    ss += v * v;
-  }
-  ss = block_sum_d(ss, red);
-  const double inv0 = 1.0 / sqrt(ss);
-  for (int64_t i = tid; i < d; i += blockDim.x) Q[i] *= inv0;
-  if (tid == 0) s_k = kmax;
-  __syncthreads();
-  double amax = 0.0;
-  for (int j = 0; j < kmax; ++j) {
-    const double* q = Q + (int64_t)j * d;
-    for (int64_t r = warp; r < d; r += nw) {
-      const double* Mr = M + r * d;
-      double s = 0.0;
-      for (int64_t c = lane; c < d; c += 32) s = fma(Mr[c], q[c], s);
-      s = warp_sum_d(s);
-      if (lane == 0) z[r] = s;
-    }
-    __syncthreads();
-    double a = 0.0;
-    for (int64_t r = tid; r < d; r += blockDim.x) a = fma(q[r], z[r], a);
-    a = block_sum_d(a, red);
-    if (tid == 0) alpha[j] = a;
-    amax = fmax(amax, fabs(a));
-    for (int pass = 0; pass < 2; ++pass) {
-      for (int i = warp; i <= j; i += nw) {
-        const double* qi = Q + (int64_t)i * d;
-        double s = 0.0;
-        for (int64_t c = lane; c < d; c += 32) s = fma(qi[c], z[c], s);
-        s = warp_sum_d(s);
-        if (lane == 0) h[i] = s;
-      }
-      __syncthreads();
-      for (int64_t r = tid; r < d; r += blockDim.x) {
-        double zr = z[r];
-        for (int i = 0; i <= j; ++i) zr = fma(-h[i], Q[(int64_t)i * d + r], zr);
-        z[r] = zr;
-      }
-      __syncthreads();
-    }
-    double b = 0.0;
-    for (int64_t r = tid; r < d; r += blockDim.x) b = fma(z[r], z[r], b);
-    b = sqrt(block_sum_d(b, red));
-    if (tid == 0) beta[j + 1] = b;
-    if (j + 1 == kmax || b <= 1e-12 * amax) {
-      if (tid == 0) s_k = j + 1;
-      break;
-    }
-    double* qn = Q + (int64_t)(j + 1) * d;
-    const double ib = 1.0 / b;
-    for (int64_t r = tid; r < d; r += blockDim.x) qn[r] = z[r] * ib;
-    __syncthreads();
-  }
-  __syncthreads();
-  // extreme eigenvalues of the k x k tridiagonal by bisection (fp64)
-  const int k = s_k;
-  // top-ntop Ritz values (descending) for the proj-err denominator: thread 2 + t
-  // bisects the (k - t)-th smallest; t >= k (Krylov space exhausted) -> 0
-  if (tid >= 2 && tid < 2 + ntop) {
-    const int t = tid - 2;
-    if (t >= k) {
-      top[t] = 0.0;
-    } else {
-      double gl = 1e308, gu = -1e308;
-      for (int i = 0; i < k; ++i) {
-        const double em = (i > 0) ? fabs(beta[i]) : 0.0;
-        const double ep = (i + 1 < k) ? fabs(beta[i + 1]) : 0.0;
-        gl = fmin(gl, alpha[i] - em - ep);
-        gu = fmax(gu, alpha[i] + em + ep);
-      }
-      double lo = gl - 1e-12 * fabs(gl) - 1e-300, hi = gu + 1e-12 * fabs(gu) + 1e-300;
-      for (int it = 0; it < 200; ++it) {
-        const double mid = 0.5 * (lo + hi);
-        if (mid <= lo || mid >= hi) break;
-        if (sturm_count_d(alpha, beta, k, mid) >= k - t) hi = mid;
-        else lo = mid;
-      }
-      top[t] = 0.5 * (lo + hi);
-    }
-  }
-  if (tid < 2) {
-    double gl = 1e308, gu = -1e308;
-    for (int i = 0; i < k; ++i) {
-      const double em = (i > 0) ? fabs(beta[i]) : 0.0;
-      const double ep = (i + 1 < k) ? fabs(beta[i + 1]) : 0.0;
-      gl = fmin(gl, alpha[i] - em - ep);
-      gu = fmax(gu, alpha[i] + em + ep);
-    }
-    double lo = gl - 1e-12 * fabs(gl) - 1e-300, hi = gu + 1e-12 * fabs(gu) + 1e-300;
-    const int target = (tid == 0) ? k : 1;  // tid0: largest (count < x == k), tid1: smallest
-    for (int it = 0; it < 200; ++it) {
-      const double mid = 0.5 * (lo + hi);
-      if (mid <= lo || mid >= hi) break;
-      const int cnt = sturm_count_d(alpha, beta, k, mid);
-      if (cnt >= target) hi = mid;
-      else lo = mid;
-    }
-    out2[tid] = 0.5 * (lo + hi);
-  }
-}
-
-cudaError_t launch_lanczos(const double* M, int64_t d, int kmax, double* Q, double* work, double* out2,
-                           cudaStream_t s, int ntop, double* top) {
-  lanczos_kernel<<<1, 1024, 0, s>>>(M, d, kmax, Q, work, out2, ntop, top);
-  return cudaGetLastError();
-}
 
 }  // namespace fdk

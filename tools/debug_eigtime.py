@@ -19,5 +19,6 @@ for variant, ell, P in [("fast_fd", 128, 148), ("fast_fd", 64, 148), ("fd", 32, 
     cnt = max(t[10], 1)
     ph = {names[i]: t[i + 1] / cnt for i in range(6)}
     print(variant, ell, "N", t[9], "problems(block0)", t[10], "avg clusters", t[7] / cnt, "max cluster", t[8], {k: f"{v/1.9e3:.1f}us" for k, v in ph.items()})
+    print("   invit sub-phases us (solves, small-cluster MGS, block CGS):", [round(t[i] / cnt / 1.9e3, 1) for i in (16, 17, 18)])
     print("   per kernel ms:", {k: (round(v[0], 2), v[1]) for k, v in prof.items()})
     sk.close()
