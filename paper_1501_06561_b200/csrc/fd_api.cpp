@@ -183,7 +183,7 @@ struct fd_handle {
   bool dead;
   bool legacy_trd;    // FD_LEGACY_TRD set: tridiagonalise inside eig_kernel (A/B checks)
   bool simt_gemm;     // FD_SIMT_GEMM set: FP32 SIMT Gram / reconstruct instead of tcgen05 (A/B checks)
-  bool simt_gram, simt_recon;  // per-GEMM variants (FD_SIMT_GRAM; FD_TC_RECON opts into the TC reconstruct)
+  bool simt_gram, simt_recon;  // per-GEMM variants (FD_SIMT_GRAM, FD_SIMT_RECON: the FP32 SIMT kernels, A/B only)
   // live profiling: event pairs around launches
   bool prof;
   struct Rec { int kind; cudaEvent_t a, b; };
@@ -280,9 +280,9 @@ fd_status run_reduce(fd_handle* h, const std::vector<Prob>& probs, bool comp = f
     return cuda_fail(e, "eig");
   if (prm.pretrd && (e = timed(h, K_BT, [&] { return fdk::launch_bt(dp, n, prm, h->stream); })) != cudaSuccess)
     return cuda_fail(e, "bt");
-  const bool tc_recon = !h->simt_recon && fdk::recon_tc_supported(nmax, prm);
+  const bool tc_recon = !h->simt_recon && fdk::recon_i8_supported(nmax, prm);
   if ((e = timed(h, K_RECON, [&] {
-         return tc_recon ? fdk::launch_recon_tc(dp, n, nmax, prm, h->stream) : fdk::launch_recon(dp, n, nmax, prm, h->stream);
+         return tc_recon ? fdk::launch_recon_i8(dp, n, nmax, prm, h->stream) : fdk::launch_recon(dp, n, nmax, prm, h->stream);
        })) != cudaSuccess)
     return cuda_fail(e, "recon");
   return FD_OK;
@@ -428,7 +428,7 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
   h->simt_gemm = getenv("FD_SIMT_GEMM") != nullptr;
   h->simt_gram = h->simt_gemm || getenv("FD_SIMT_GRAM") != nullptr;
   // the tensor-core reconstruct is opt-in (accumulation bias, fd_tc.cu)
-  h->simt_recon = h->simt_gemm || getenv("FD_TC_RECON") == nullptr;
+  h->simt_recon = h->simt_gemm || getenv("FD_SIMT_RECON") != nullptr;
   h->prm.dbg = nullptr;
   if (getenv("FD_DEBUG_EIG")) {
     void* dbgp = nullptr;

@@ -113,8 +113,10 @@ bool trd_supported(int nmax, const Params& p);
 // tcgen05 3xTF32 GEMMs (fd_tc.cu)
 bool gram_tc_supported(int nmax, const Params& p);
 cudaError_t launch_gram_tc(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s);
-bool recon_tc_supported(int nmax, const Params& p);
-cudaError_t launch_recon_tc(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s);
+// reconstruct B' = Wt Bf on tcgen05 kind::i8 (fd_recon_i8.cu: int8 digit planes of row- /
+// column-scaled fixed point, exact int32 accumulation); N <= 256, ret <= 128
+bool recon_i8_supported(int nmax, const Params& p);
+cudaError_t launch_recon_i8(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s);
 cudaError_t launch_trd(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s);
 // Blocked (compact WY) back-transform + Wt = diag(w) U^T (fd_bt.cu), after eig when p.pretrd.
 cudaError_t launch_bt(const Prob* dev_probs, int count, const Params& p, cudaStream_t s);

@@ -1,8 +1,8 @@
-// fd_tc.cu — tensor-core (tcgen05, kind::tf32) GEMMs of one ReduceRank with an
-// FP32-accurate 3xTF32 split (x = hi + lo, hi = tf32(x); a.b ~ hi.hi + hi.lo + lo.hi,
-// fp32 accumulation in TMEM).  SURVEY §8(a) rows a2 / a5:
+// fd_tc.cu — the buffer Gram of one ReduceRank on the tensor cores (tcgen05,
+// kind::tf32) with an FP32-accurate 3xTF32 split (x = hi + lo, hi = tf32(x);
+// a.b ~ hi.hi + hi.lo + lo.hi, fp32 accumulation in TMEM).  SURVEY §8(a) row a2:
 //   gram:  G = Bf Bf^T                (buffer Gram; "svd(B_[i])", Alg. 1)
-//   recon: B' = Wt Bf, Wt = diag(w) U^T  ("B_[i] <- S'V^T")
+// (the reconstruct, row a5, is fd_recon_i8.cu: int8 digit planes, exact accumulation)
 //
 // One CTA per problem (persistent over the launch's problems), 256 threads:
 // all threads stream 32-column K-chunks of the operands from global memory into
@@ -221,202 +221,6 @@ static cudaError_t launch_gram_tc_t(const Prob* dev_probs, int count, const Para
   if (cudaError_t e = once.ensure(gram_tc_kernel<NP>, dyn); e != cudaSuccess) return e;
   const int grid = count < kNumSMs ? count : kNumSMs;
   gram_tc_kernel<NP><<<grid, kTcThreads, dyn, s>>>(dev_probs, count, p);
-  return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------------------
-// Reconstruct B' = Wt Bf (rows 0..ell-2; row ell-1 = 0) on tcgen05, 3xTF32.
-// Wt: (ell-1) x N (ldg), Bf: N x d rows of the problem (ldb).  M = 128 (ell-1 <=
-// 127), N-tiles of 128 columns of d, K = N in 32-row chunks; both operands K-major
-// SW128 (A = Wt rows; B = Bf^T, transposed while staging).
-//
-// Accuracy: the tensor core's fp32 accumulation truncates (~0.5 ulp per MMA step).
-// Accumulating all K = 256 in TMEM shrinks every reconstructed row by ~1e-6 per
-// ReduceRank, which compounds through the retained rows.  Here each
-// 32-row chunk accumulates into fresh TMEM partials (hi.hi and the small cross
-// terms apart: 4 and 8 steps), double-buffered, and the partials are drained into
-// fp32 register running sums (round-to-nearest adds) while the next chunk's MMAs
-// run.  Warps w and w+4 share TMEM lanes 32 (w % 4).. and split the 128 columns.
-// ---------------------------------------------------------------------------
-namespace {
-constexpr int kRA = 128 * 128;      // A tile bytes (128 rows x 32 values)
-constexpr int kRB = 128 * 128;      // B tile bytes (128 rows (n) x 32 values (k))
-constexpr int kRStage = 2 * kRA + 2 * kRB;
-
-struct ReconRegs {
-  float4 a[4];   // A: 128 rows x 8 float4 = 1024 items / 256 threads
-  float4 b[4];   // B: k-rows 4g..4g+3 of columns n0 + 4q .. +3 (q = tid & 31, g = tid >> 5)
-};
-
-__device__ __forceinline__ void recon_load(const Prob& P, const Params& p, int N, int jrows, int kc, int n0,
-                                           ReconRegs& R) {
-  const float* Wt = static_cast<const float*>(P.Wt);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int it = threadIdx.x + kTcThreads * j;
-    const int r = it >> 3, c4 = it & 7;
-    const int k = kc * 32 + 4 * c4;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (r < jrows && k < N) {
-      v = *reinterpret_cast<const float4*>(Wt + (int64_t)r * p.ldg + k);
-      if (k + 1 >= N) v.y = 0.f;
-      if (k + 2 >= N) v.z = 0.f;
-      if (k + 3 >= N) v.w = 0.f;
-    }
-    R.a[j] = v;
-  }
-  const int q = threadIdx.x & 31, g = threadIdx.x >> 5;
-  const int64_t n = n0 + 4 * q;
-#pragma unroll
-  for (int kk = 0; kk < 4; ++kk) {
-    const int k = kc * 32 + 4 * g + kk;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (k < N && n < p.ldb) v = __ldg(reinterpret_cast<const float4*>(row_ptr(P, k, p.ldb) + n));
-    R.b[kk] = v;
-  }
-}
-
-__device__ __forceinline__ void st_split(unsigned char* hi, unsigned char* lo, uint32_t off, float4 x) {
-  float4 h, l;
-  tc::split_tf32(x.x, h.x, l.x);
-  tc::split_tf32(x.y, h.y, l.y);
-  tc::split_tf32(x.z, h.z, l.z);
-  tc::split_tf32(x.w, h.w, l.w);
-  *reinterpret_cast<float4*>(hi + off) = h;
-  *reinterpret_cast<float4*>(lo + off) = l;
-}
-
-__device__ __forceinline__ float comp(const float4& v, int e) {
-  return e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w));
-}
-
-__device__ __forceinline__ void recon_store(unsigned char* st, const ReconRegs& R) {
-  unsigned char* ahi = st;
-  unsigned char* alo = st + kRA;
-  unsigned char* bhi = st + 2 * kRA;
-  unsigned char* blo = st + 2 * kRA + kRB;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int it = threadIdx.x + kTcThreads * j;
-    const int r = it >> 3, c4 = it & 7;
-    st_split(ahi, alo, tc::sw128_off(r, 4 * c4), R.a[j]);
-  }
-  const int q = threadIdx.x & 31, g = threadIdx.x >> 5;
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const float4 v = make_float4(comp(R.b[0], e), comp(R.b[1], e), comp(R.b[2], e), comp(R.b[3], e));
-    st_split(bhi, blo, tc::sw128_off(4 * q + e, 4 * g), v);
-  }
-}
-}  // namespace
-
-__global__ void __launch_bounds__(kTcThreads, 1) recon_tc_kernel(const Prob* __restrict__ probs, int count, Params p) {
-  extern __shared__ unsigned char smraw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
-  __shared__ __align__(8) uint64_t mbar[2];
-  __shared__ uint32_t s_tmem;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (warp == 0) tc::tmem_alloc(&s_tmem, 512);
-  if (tid == 0) {
-    tc::mbar_init(&mbar[0], 1);
-    tc::mbar_init(&mbar[1], 1);
-    tc::fence_mbar_init();
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  const uint32_t tbase = s_tmem;
-  uint32_t uses[2] = {0, 0};
-  const uint32_t idesc = tc::idesc_tf32(128, 128, 0, 0);
-  const int ell = p.ell, jrows = p.ret;
-  // TMEM: partials of chunk parity b: hi.hi at 128 b, cross terms at 256 + 128 b
-  const uint32_t lanebase = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
-  const int half = warp >> 2;                    // columns 64 half .. 64 half + 63 of the tile
-  const int m = 32 * (warp & 3) + lane;          // tile row (= TMEM lane)
-
-  for (int pi = blockIdx.x; pi < count; pi += gridDim.x) {
-    const Prob P = probs[pi];
-    const int N = P.rows0 + P.rows1;
-    const int nk = (N + 31) / 32;
-    for (int n0 = 0; n0 < p.ldb; n0 += 128) {
-      float acc[64];
-#pragma unroll
-      for (int c = 0; c < 64; ++c) acc[c] = 0.f;
-      ReconRegs R;
-      recon_load(P, p, N, jrows, 0, n0, R);
-      recon_store(sm, R);
-      tc::fence_async_smem();
-      __syncthreads();
-      for (int kc = 0; kc <= nk; ++kc) {
-        const int b = kc & 1;
-        if (kc < nk && tid == 0) {
-          tc::fence_after_sync();
-          unsigned char* st = sm + b * kRStage;
-          const uint32_t ahi = tc::smem_u32(st), alo = tc::smem_u32(st + kRA);
-          const uint32_t bhi = tc::smem_u32(st + 2 * kRA), blo = tc::smem_u32(st + 2 * kRA + kRB);
-          const uint32_t thh = tbase + 128 * b, tx = tbase + 256 + 128 * b;
-#pragma unroll
-          for (int ks = 0; ks < 4; ++ks) {
-            const uint32_t ka = ks * 32;
-            tc::mma_tf32(thh, tc::desc_k_sw128(ahi + ka), tc::desc_k_sw128(bhi + ka), idesc, ks > 0 ? 1u : 0u);
-            tc::mma_tf32(tx, tc::desc_k_sw128(ahi + ka), tc::desc_k_sw128(blo + ka), idesc, ks > 0 ? 1u : 0u);
-            tc::mma_tf32(tx, tc::desc_k_sw128(alo + ka), tc::desc_k_sw128(bhi + ka), idesc, 1u);
-          }
-          tc::commit(&mbar[b]);
-        }
-        if (kc + 1 < nk) recon_load(P, p, N, jrows, kc + 1, n0, R);
-        if (kc >= 1) {
-          // chunk kc-1: MMAs complete -> drain its partials, its smem stage is free
-          const int pb = b ^ 1;
-          tc::mbar_wait(&mbar[pb], uses[pb] & 1);
-          ++uses[pb];
-          tc::fence_after_sync();
-#pragma unroll
-          for (int c0 = 0; c0 < 64; c0 += 16) {
-            float vh[16], vx[16];
-            tc::tmem_ld16(lanebase + 128 * pb + 64 * half + c0, vh);
-            tc::tmem_ld16(lanebase + 256 + 128 * pb + 64 * half + c0, vx);
-#pragma unroll
-            for (int q = 0; q < 16; ++q) acc[c0 + q] += vh[q] + vx[q];
-          }
-        }
-        if (kc + 1 < nk) {
-          recon_store(sm + (b ^ 1) * kRStage, R);
-          tc::fence_async_smem();
-        }
-        tc::fence_before_sync();
-        __syncthreads();
-      }
-      // epilogue: row m, columns n0 + 64 half .. +63
-      if (m < ell) {
-        float* dst = P.dst + (int64_t)m * p.ldb + n0 + 64 * half;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          if (n0 + 64 * half + 4 * q + 4 <= p.ldb) {
-            const float4 o = (m < jrows) ? make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3])
-                                         : make_float4(0.f, 0.f, 0.f, 0.f);
-            *reinterpret_cast<float4*>(dst + 4 * q) = o;
-          }
-        }
-      }
-    }
-  }
-  __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tbase, 512);
-}
-
-bool recon_tc_supported(int nmax, const Params& p) {
-  return !p.f64 && p.ret <= 128 && nmax >= 1 && nmax <= 1024 && (p.ldg % 4) == 0 && (p.ldb % 4) == 0;
-}
-
-cudaError_t launch_recon_tc(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s) {
-  (void)nmax;
-  if (count <= 0) return cudaSuccess;
-  constexpr int dyn = 2 * kRStage + 1024;
-  static AttrOnce once;
-  if (cudaError_t e = once.ensure(recon_tc_kernel, dyn); e != cudaSuccess) return e;
-  const int grid = count < kNumSMs ? count : kNumSMs;
-  recon_tc_kernel<<<grid, kTcThreads, dyn, s>>>(dev_probs, count, p);
   return cudaGetLastError();
 }
 
