@@ -66,7 +66,9 @@ __global__ void __launch_bounds__(1024, 1) jacobi_kernel(double* __restrict__ G,
         double c = 1.0, s = 0.0;
         if (q < n) {
           const double apq = G[(int64_t)p * n + q], app = G[(int64_t)p * n + p], aqq = G[(int64_t)q * n + q];
-          if (apq != 0.0 && fabs(apq) > 1e-17 * sqrt(fabs(app) * fabs(aqq))) {
+          // rotate unless |apq| is at the fp64 noise level of its diagonal (a threshold
+          // below eps would keep rotating noise until the sweep cap)
+          if (apq != 0.0 && fabs(apq) > 1e-15 * sqrt(fabs(app) * fabs(aqq))) {
             const double th = (aqq - app) / (2.0 * apq);
             const double t = (fabs(th) > 1e150) ? 0.5 / th : ((th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0)));
             c = 1.0 / sqrt(t * t + 1.0);
@@ -100,6 +102,14 @@ __global__ void __launch_bounds__(1024, 1) jacobi_kernel(double* __restrict__ G,
         const double gp = G[(int64_t)p * n + k], gq = G[(int64_t)q * n + k];
         G[(int64_t)p * n + k] = c * gp - s * gq;
         G[(int64_t)q * n + k] = s * gp + c * gq;
+      }
+      __syncthreads();
+      // the rotated pair is exactly decoupled (as in the oracle's Jacobi)
+      for (int i = tid; i < npair; i += nt) {
+        const int p = pp[i], q = qq[i];
+        if (q < 0 || sn[i] == 0.0) continue;
+        G[(int64_t)p * n + q] = 0.0;
+        G[(int64_t)q * n + p] = 0.0;
       }
       __syncthreads();
     }
