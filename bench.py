@@ -62,7 +62,8 @@ def peaks():
     if os.path.exists(g):
         with open(g) as fh:
             m = json.load(fh)
-        p.update({k: m[k] for k in ("ffma_tflops", "dfma_tflops", "tf32_tcgen05_tflops") if k in m})
+        p.update({k: m[k] for k in ("ffma_tflops", "dfma_tflops", "tf32_tcgen05_tflops", "i8_tcgen05_tops",
+                                    "i8_tcgen05_n64_tops") if k in m})
         p["micro_source"] = "measured (profiles/round2_peaks_microbench.json, tools/micro/peaks.cu)"
     return p
 
@@ -122,6 +123,16 @@ def tf32x3_peak_tflops(pk):
     if "tf32_tcgen05_tflops" in pk:
         return pk["tf32_tcgen05_tflops"] / 3.0
     return pk["bf16_tflops"] / 2.0 / 3.0
+
+
+# the int8 reconstruct (fd_recon_i8.cu) forms each fp32-accurate product from 9 int8
+# digit products (3 W digits x 4 Bf digits, weights >= 2^16)
+RECON_I8_PRODUCTS = 9
+
+
+def i8_recon_peak_tflops(pk):
+    # measured tcgen05 kind::i8 throughput / 9 (fp32-equivalent flops), else bf16 x 2 / 9
+    return pk.get("i8_tcgen05_tops", 2.0 * pk["bf16_tflops"]) / RECON_I8_PRODUCTS
 
 
 def fp64_peak_tflops(pk):
@@ -381,6 +392,8 @@ def run_ours(args):
     shrinks_per_step = st["n_shrinks"]
     simt_peak = fp32_simt_peak_tflops(pk.get("sm_max_mhz", 1965.0), pk)
     tf32x3 = tf32x3_peak_tflops(pk)
+    # the reconstruct runs on tcgen05 kind::i8 unless FD_SIMT_RECON / FD_SIMT_GEMM (or N > 256)
+    recon_tc = (not (os.environ.get("FD_SIMT_RECON") or os.environ.get("FD_SIMT_GEMM"))) and N <= 256 and R_ <= 128
     dom = max(kern, key=lambda k: kern[k][0])
     dom_ms = kern[dom][0] / args.steps
     perrow = dom == "perrow"
@@ -397,6 +410,10 @@ def run_ours(args):
         flops_step = work["gram"] * shrinks_per_step
         roof = {"bound": "tensor", "achieved": flops_step / (dom_ms / 1e3) / 1e12, "peak": tf32x3,
                 "unit": "TFLOP/s"}
+    elif dom == "recon" and recon_tc:
+        flops_step = work["recon"] * shrinks_per_step
+        roof = {"bound": "tensor", "achieved": flops_step / (dom_ms / 1e3) / 1e12, "peak": i8_recon_peak_tflops(pk),
+                "unit": "TFLOP/s"}
     else:
         flops_step = work[dom] * shrinks_per_step
         roof = {"bound": "alu", "achieved": flops_step / (dom_ms / 1e3) / 1e12, "peak": simt_peak, "unit": "TFLOP/s"}
@@ -411,7 +428,8 @@ def run_ours(args):
         "alu": (f"FP64 DFMA, {micro}" if perrow else
                 (f"FP32 FFMA, {micro}" if micro else
                  f"FP32 SIMT: 148 SM x 128 lanes x 2 flop x {pk.get('sm_max_mhz', 1965.0):.0f} MHz (derived)")),
-        "tensor": (f"tcgen05 kind::tf32 / 3 (3xTF32), {micro}" if micro else
+        "tensor": ((f"tcgen05 kind::i8 / {RECON_I8_PRODUCTS} (digit products per fp32-equivalent product), {micro}"
+                    if dom == "recon" else f"tcgen05 kind::tf32 / 3 (3xTF32), {micro}") if micro else
                    f"3xTF32 = (bf16_tflops {pk['bf16_tflops']} / 2) / 3, {pk['source']}"),
         "hbm": f"hbm_gbs {pk['source']}"}[roof["bound"]]
     traffic_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -420,14 +438,16 @@ def run_ours(args):
         with open(traffic_file) as f:
             trj = json.load(f)
             # the captured launch names of the step kernels (tcgen05 Gram, pipelined reconstruct)
-            alias = {"gram_kernel": "gram_tc_kernel", "recon_kernel": "recon_pipe2_kernel"}
+            alias = {"gram_kernel": "gram_tc_kernel",
+                     "recon_kernel": "recon_i8_kernel" if recon_tc else "recon_pipe2_kernel"}
             tr = trj.get(roof["kernel"]) or trj.get(alias.get(roof["kernel"], ""))
         if tr:
             # bytes per problem from the committed capture x problems per launch of this run
             roof["traffic"] = tr["bytes_per_problem"] * shrinks_per_step / max(kern[dom][1], 1) * args.steps
             roof["traffic_source"] = tr["source"]
     # north_star roofline: slower of HBM (4d bytes/row) and the Gram + reconstruct flops
-    # on the pipes this build uses (Gram: tcgen05 3xTF32; reconstruct: FP32 SIMT)
+    # on the pipes this build uses (Gram: tcgen05 3xTF32; reconstruct: tcgen05 int8 digit
+    # products, or FP32 SIMT where the int8 kernel does not apply)
     n_rows = w.n / world
     hbm_s = n_rows * 4 * w.d / (pk["hbm_gbs"] * 1e9)
     if perrow:
@@ -439,11 +459,14 @@ def run_ours(args):
             "note": f"{P} dependent stream(s): at most {P} x C of 148 SMs busy; latency-bound by design"}
     else:
         gram_s = work["gram"] * shrinks_per_step / (tf32x3 * 1e12)
-        recon_s = work["recon"] * shrinks_per_step / (simt_peak * 1e12)
+        recon_peak = i8_recon_peak_tflops(pk) if recon_tc else simt_peak
+        recon_s = work["recon"] * shrinks_per_step / (recon_peak * 1e12)
         t_roof = max(hbm_s, gram_s + recon_s)
         roof["north_star"] = {
             "R_roof_rows_per_s_per_gpu": n_rows / t_roof, "t_roof_ms": t_roof * 1e3,
-            "pipes": "Gram tcgen05 3xTF32, reconstruct FP32 SIMT", "hbm_ms": hbm_s * 1e3,
+            "pipes": "Gram tcgen05 3xTF32, reconstruct " + (
+                f"tcgen05 int8 ({RECON_I8_PRODUCTS} digit products)" if recon_tc else "FP32 SIMT"),
+            "hbm_ms": hbm_s * 1e3,
             "frac": (value / world) / (n_rows / t_roof)}
         eig_flops = (work["trd"] + work["bt"]) * shrinks_per_step
         roof["eigensolver_inclusive"] = {

@@ -780,34 +780,44 @@ perrow_kernel(const RowJob* __restrict__ jobs, Params p, int C, int lazy, int* _
 cudaError_t launch_perrow(const RowJob* dev_jobs, int count, const Params& p, int lazy, int* nonfinite,
                           cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
-  const int C = perrow_cluster(p.ell, p.d);
+  int C = perrow_cluster(p.ell, p.d);
   if (C <= 0) return cudaErrorInvalidValue;
-  const int smem = (int)perrow_smem_bytes(p.ell, p.d, C);
-  static AttrOnce once;
-  if (cudaError_t e = once.ensure(perrow_kernel, smem); e != cudaSuccess) return e;
-  if (C > 8) {
-    static AttrOnce np;   // per device, like the smem attribute
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev >= 64 || !((np.done >> dev) & 1ull)) {
-      if (cudaError_t e = cudaFuncSetAttribute(perrow_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-          e != cudaSuccess)
-        return e;
-      if (dev < 64) np.done |= 1ull << dev;
-    }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static AttrOnce np;   // per device, like the smem attribute
+  if (dev >= 64 || !((np.done >> dev) & 1ull)) {
+    if (cudaError_t e = cudaFuncSetAttribute(perrow_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        e != cudaSuccess)
+      return e;
+    if (dev < 64) np.done |= 1ull << dev;
   }
+  static AttrOnce once;
+  if (cudaError_t e = once.ensure(perrow_kernel, (int)kPrSmemMax); e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(count * C));
   cfg.blockDim = dim3(kPrThreads);
-  cfg.dynamicSmemBytes = (size_t)smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = (unsigned)C;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  // the streams are dependent chains that all run for the whole call: every cluster must
+  // be resident at once.  Clusters of 16 fit about one per GPC, so with many streams the
+  // cluster shrinks (more column work per CTA) until all of them are co-resident.
+  for (;;) {
+    at[0].val.clusterDim.x = (unsigned)C;
+    cfg.gridDim = dim3((unsigned)(count * C));
+    cfg.dynamicSmemBytes = perrow_smem_bytes(p.ell, p.d, C);
+    if (C == 1 || perrow_smem_bytes(p.ell, p.d, C / 2) > kPrSmemMax) break;
+    int active = 0;
+    if (cudaOccupancyMaxActiveClusters(&active, perrow_kernel, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      break;
+    }
+    if (active >= count) break;
+    C /= 2;
+  }
   return cudaLaunchKernelEx(&cfg, perrow_kernel, dev_jobs, p, C, lazy, nonfinite);
 }
 
