@@ -371,6 +371,9 @@ constexpr int kSmallCl = 8;             // clusters up to this size: warp MGS; l
 #define FD_INV_ITERS 2
 #endif
 constexpr int kInvIters = FD_INV_ITERS;
+#ifndef FD_EIG_DISCARD
+#define FD_EIG_DISCARD 1
+#endif
 #ifndef FD_SOLVE_BATCH
 #define FD_SOLVE_BATCH 4
 #endif
@@ -1623,6 +1626,19 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
     for (int j = J + warp; j < p.ret; j += kNW)
       for (int r = lane; r < p.ldg; r += 32) Wt[(int64_t)j * p.ldg + r] = T(0);
     __syncthreads();
+#if FD_EIG_DISCARD
+    if (PRE) {
+      // the inverse-iteration scratch of this problem is dead (the next problem of this
+      // slot writes before it reads): drop its dirty L2 lines instead of writing them back
+      const size_t nl = ((size_t)N * zst * sizeof(ZT) + 127) / 128;
+      char* b0 = reinterpret_cast<char*>(LF);
+      char* b1 = reinterpret_cast<char*>(Zs);
+      for (size_t l = tid; l < nl; l += blockDim.x) {
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(b0 + l * 128) : "memory");
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(b1 + l * 128) : "memory");
+      }
+    }
+#endif
     if (p.dbg && blockIdx.x == 0 && tid == 0) {
       p.dbg[6] += clock64() - t_ph0;
       int mx = 0;
