@@ -393,7 +393,8 @@ def run_ours(args):
     simt_peak = fp32_simt_peak_tflops(pk.get("sm_max_mhz", 1965.0), pk)
     tf32x3 = tf32x3_peak_tflops(pk)
     # the reconstruct runs on tcgen05 kind::i8 unless FD_SIMT_RECON / FD_SIMT_GEMM (or N > 256)
-    recon_tc = (not (os.environ.get("FD_SIMT_RECON") or os.environ.get("FD_SIMT_GEMM"))) and N <= 256 and R_ <= 128
+    recon_tc = ((not (os.environ.get("FD_SIMT_RECON") or os.environ.get("FD_SIMT_GEMM"))) and 224 <= N <= 256
+                and 112 <= R_ <= 128)   # fd_recon_i8.cu recon_i8_supported
     dom = max(kern, key=lambda k: kern[k][0])
     dom_ms = kern[dom][0] / args.steps
     perrow = dom == "perrow"

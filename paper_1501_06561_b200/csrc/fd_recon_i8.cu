@@ -316,8 +316,13 @@ __global__ void __launch_bounds__(kRiThreads, 1) recon_i8_kernel(const Prob* __r
   if (warp == 0) tc::tmem_dealloc(tbase, 512);
 }
 
+// Used where it beats the FP32 SIMT reconstruct: its cost is set by the 128-row MMA tile
+// and the 256-row quantisation pass, so it needs the retained rows to fill M (c4: ret = 127,
+// N = 256: 55 vs 90 ms per pass); at c3 ell = 100 (ret = 99, N = 200) SIMT is faster
+// (3.1 vs 3.8 ms), at ell = 50 more so (3.0 vs 3.7 ms).
 bool recon_i8_supported(int nmax, const Params& p) {
-  return !p.f64 && p.ret <= 128 && nmax >= 1 && nmax <= kRiMaxN && (p.ldg % 4) == 0 && (p.ldb % 4) == 0;
+  return !p.f64 && p.ret >= 112 && p.ret <= 128 && nmax >= 224 && nmax <= kRiMaxN && (p.ldg % 4) == 0 &&
+         (p.ldb % 4) == 0;
 }
 
 cudaError_t launch_recon_i8(const Prob* dev_probs, int count, int nmax, const Params& p, cudaStream_t s) {

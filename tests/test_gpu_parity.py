@@ -682,3 +682,33 @@ def test_proj_err_rank_deficient_A_is_an_error():
     B = rng.standard_normal((6, 24)).astype(np.float32)
     with pytest.raises(m.FdError):
         m.proj_err(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), k=5)
+
+
+# ---------------------------------------------------------------------------
+# the int8 tensor-core reconstruct (reading C29) at a small size: ell = 128 Fast FD
+# (ret = 127, N = 256, its operating point) on c2 rows (d = 500: a ragged last
+# 64-column tile), against the oracle and against the FP32 SIMT reconstruct
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("variant", ["fast_fd", "fast_alpha_fd"])
+def test_parity_int8_reconstruct_ell128(variant):
+    from oracle import alg1_svd
+    A = _c2()[:3000]
+    Bg, st, Ad = gpu_sketch(A, 128, variant, n_shards=2)
+    X, sx = alg1_svd.sketch_stream(A[:1500], 128, variant, alpha=0.2)
+    Y, sy = alg1_svd.sketch_stream(A[1500:], 128, variant, alpha=0.2)
+    Bo, sm = alg1_svd.merge(X, Y, 128, variant, alpha=0.2)
+    frob = sx[0] + sy[0]
+    assert abs(st["frob_sq"] - frob) <= 1e-9 * frob
+    assert st["n_shrinks"] == int(sx[3] + sy[3] + sm[3])
+    assert spec_norm(Bg.T @ Bg - Bo.T @ Bo) <= SKETCH_TOL * frob
+    assert abs((st["frob_sq"] - np.sum(Bg ** 2)) - st["removed_mass"]) <= 1e-4 * frob
+    eo = oracle.cov_err(A, Bo)["err"]
+    eg = fd().cov_err(Ad, torch.from_numpy(Bg.astype(np.float32)).cuda())["err"]
+    assert abs(eg - eo) <= ERR_TOL * eo + err_floor(Bo, frob)
+    # the FP32 SIMT reconstruct (FD_SIMT_RECON, read at fd_create) on the same input
+    os.environ["FD_SIMT_RECON"] = "1"
+    try:
+        Bs, sts, _ = gpu_sketch(A, 128, variant, n_shards=2)
+    finally:
+        del os.environ["FD_SIMT_RECON"]
+    assert spec_norm(Bg.T @ Bg - Bs.T @ Bs) <= 1e-5 * frob
