@@ -20,7 +20,10 @@ namespace fdk {
 
 namespace {
 
-constexpr int kTcThreads = 256;
+#ifndef FD_TC_THREADS
+#define FD_TC_THREADS 256
+#endif
+constexpr int kTcThreads = FD_TC_THREADS;   // staging threads (warps 0-3 also run the epilogue)
 constexpr int kTile = 256 * 128;   // bytes of one 256-row x 32-value SW128 tile
 constexpr int kAccs = 4;           // K-split accumulators of the NP = 128 Gram (4 x 128 TMEM columns)
 
