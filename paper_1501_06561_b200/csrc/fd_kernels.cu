@@ -371,6 +371,9 @@ constexpr int kSmallCl = 8;             // clusters up to this size: warp MGS; l
 #define FD_INV_ITERS 2
 #endif
 constexpr int kInvIters = FD_INV_ITERS;
+#ifndef FD_INV_F32
+#define FD_INV_F32 1
+#endif
 #ifndef FD_EIG_DISCARD
 #define FD_EIG_DISCARD 1
 #endif
@@ -381,6 +384,7 @@ constexpr int kSB = FD_SOLVE_BATCH;   // rows per load batch of the twisted solv
 
 // fp64 reciprocal: fp32 estimate + two Newton steps (each squares the ~6e-8
 // relative error of the estimate), cheaper than the IEEE division.
+__device__ __forceinline__ float rcp_rt(float x) { return __frcp_rn(x); }
 __device__ __forceinline__ double rcp_d(double x) {
   if (!(fabs(x) > 1e-30 && fabs(x) < 1e30)) return 1.0 / x;   // outside the fp32 estimate's range
   double r = (double)__frcp_rn((float)x);
@@ -388,6 +392,7 @@ __device__ __forceinline__ double rcp_d(double x) {
   r = r * fma(-x, r, 2.0);
   return r;
 }
+__device__ __forceinline__ double rcp_rt(double x) { return rcp_d(x); }
 // fp64 scratch per CTA slot (stride zld): LDL^T factors and Z (element-major
 // [i][j], zld x zld each), a Rayleigh-Ritz copy region, then, for problems above
 // kMaxNS, the packed matrix (global / L2 instead of shared memory).
@@ -1197,7 +1202,9 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
     }
     __syncthreads();
     {
-      const double tiny = 2.3e-16 * (double)bnorm + 1e-300;
+      // recurrence precision of the twisted solves (FD_INV_F32: fp32 A/B)
+      using RT = typename std::conditional<PRE && FD_INV_F32, float, double>::type;
+      const RT tiny = (sizeof(RT) == 4) ? (RT)(1.2e-7 * (double)bnorm + 1e-30) : (RT)(2.3e-16 * (double)bnorm + 1e-300);
       long long t_iv = clock64();
       // Twisted solves: vector j is solved by the lane pair (2j', 2j'+1); the even
       // lane eliminates rows 0..m-1 top-down (T - mu I = L D+ L^T part), the odd lane
@@ -1212,19 +1219,19 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
           if (!vact[j]) continue;
           ZT* lf = LF + j;   // lf[i * zst]: l_i (i < m), u_i (i >= m)
           ZT* z = Zs + j;    // z[i * zst]
-          const double sc = pscl[j];
-          const double mu = lamd[j];
-          auto rhs = [&](int i, double zi) -> double {
-            return (it == 0) ? 1.0 + 0.5 * (double)(((i + 1) * 7919 + (j + 3) * 104729) % 211) / 211.0 : zi * sc;
+          const RT sc = (RT)pscl[j];
+          const RT mu = (RT)lamd[j];
+          auto rhs = [&](int i, RT zi) -> RT {
+            return (it == 0) ? (RT)(1.0 + 0.5 * (double)(((i + 1) * 7919 + (j + 3) * 104729) % 211) / 211.0) : zi * sc;
           };
           // Both lanes run ONE instruction stream (no divergence): step k of a side is
           // row i = i0 + dir k; the coupling to the previous row of its elimination
           // order is e[ec] with ec = i - 1 (top) / i (bottom), stored multiplier lf[ec].
           const int cnt = side ? (N - 1 - m) : m;     // rows of this side (<= m)
           const int dir = side ? -1 : 1, ist = side ? N - 1 : 0;
-          double rd = 0.0, w = 0.0, eprev = 0.0;
+          RT rd = 0, w = 0, eprev = 0;
           for (int k0 = 0; k0 < m; k0 += kSB) {
-            double zb[kSB];
+            RT zb[kSB];
             if (it > 0) {
 #pragma unroll
               for (int q = 0; q < kSB; ++q) zb[q] = (k0 + q < cnt) ? z[(size_t)(ist + dir * (k0 + q)) * zst] : 0.0;
@@ -1234,51 +1241,51 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
               const int k = k0 + q;
               if (k < cnt) {
                 const int i = ist + dir * k;
-                const double bi = rhs(i, zb[q]);
-                double dpi;
+                const RT bi = rhs(i, zb[q]);
+                RT dpi;
                 if (k == 0) {
-                  dpi = (double)dd[i] - mu;
+                  dpi = (RT)dd[i] - mu;
                   w = bi;
                 } else {
-                  const double li = eprev * rd;
+                  const RT li = eprev * rd;
                   lf[(size_t)(i - 1 + side) * zst] = li;
-                  dpi = ((double)dd[i] - mu) - li * eprev;
+                  dpi = ((RT)dd[i] - mu) - li * eprev;
                   w = bi - li * w;
                 }
-                if (fabs(dpi) < tiny) dpi = (dpi < 0.0) ? -tiny : tiny;
-                rd = rcp_d(dpi);
+                if (fabs(dpi) < tiny) dpi = (dpi < (RT)0) ? -tiny : tiny;
+                rd = rcp_rt(dpi);
                 zb[q] = w * rd;
-                eprev = (double)ee[i - side];
+                eprev = (RT)ee[i - side];
               }
             }
 #pragma unroll
             for (int q = 0; q < kSB; ++q)
               if (k0 + q < cnt) z[(size_t)(ist + dir * (k0 + q)) * zst] = zb[q];
           }
-          double tS = 0.0, wS = 0.0;   // this side's term of the twist row
+          RT tS = 0, wS = 0;   // this side's term of the twist row
           if (cnt > 0) {
-            const double l = eprev * rd;   // l_{m-1} (top) / u_m (bottom)
+            const RT l = eprev * rd;   // l_{m-1} (top) / u_m (bottom)
             lf[(size_t)(m - 1 + side) * zst] = l;
             tS = l * eprev;
             wS = l * w;
           }
           // twist row m (both lanes, identical arithmetic)
-          const double tO = __shfl_xor_sync(pmask, tS, 1), wO = __shfl_xor_sync(pmask, wS, 1);
-          const double tA = side ? tO : tS, tB = side ? tS : tO;
-          const double wA = side ? wO : wS, wB = side ? wS : wO;
-          double gm = (((double)dd[m] - mu) - tA) - tB;
-          if (fabs(gm) < tiny) gm = (gm < 0.0) ? -tiny : tiny;
-          const double bm = rhs(m, (it > 0) ? z[(size_t)m * zst] : 0.0);
-          const double zm = ((bm - wA) - wB) * rcp_d(gm);
+          const RT tO = __shfl_xor_sync(pmask, tS, 1), wO = __shfl_xor_sync(pmask, wS, 1);
+          const RT tA = side ? tO : tS, tB = side ? tS : tO;
+          const RT wA = side ? wO : wS, wB = side ? wS : wO;
+          RT gm = (((RT)dd[m] - mu) - tA) - tB;
+          if (fabs(gm) < tiny) gm = (gm < (RT)0) ? -tiny : tiny;
+          const RT bm = rhs(m, (it > 0) ? (RT)z[(size_t)m * zst] : (RT)0);
+          const RT zm = ((bm - wA) - wB) * rcp_rt(gm);
           __syncwarp(pmask);   // both lanes read z[m] before it is overwritten
           if (side == 0) z[(size_t)m * zst] = zm;
-          double nr = side ? 0.0 : zm * zm;
+          double nr = side ? 0.0 : (double)zm * (double)zm;
           // back-substitution outwards from m: top i = m-1..0 (l_i = lf[i]),
           // bottom i = m+1..N-1 (u_{i-1} = lf[i-1])
-          double next = zm;
+          RT next = zm;
           const int bst = side ? m + 1 : m - 1, bdir = side ? 1 : -1;
           for (int k0 = 0; k0 < m; k0 += kSB) {
-            double zb[kSB], lb[kSB];
+            RT zb[kSB], lb[kSB];
 #pragma unroll
             for (int q = 0; q < kSB; ++q) {
               const int i = bst + bdir * (k0 + q);
@@ -1291,7 +1298,7 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
               if (k0 + q < cnt) {
                 next = zb[q] - lb[q] * next;
                 zb[q] = next;
-                nr += next * next;
+                nr += (double)next * (double)next;
               }
             }
 #pragma unroll
