@@ -371,6 +371,9 @@ constexpr int kSmallCl = 8;             // clusters up to this size: warp MGS; l
 #define FD_INV_ITERS 2
 #endif
 constexpr int kInvIters = FD_INV_ITERS;
+#ifndef FD_BISECT_LOOSE
+#define FD_BISECT_LOOSE 1
+#endif
 #ifndef FD_INV_F32
 #define FD_INV_F32 1
 #endif
@@ -966,7 +969,10 @@ eig_kernel(const Prob* __restrict__ probs, int count, Params p, double* __restri
         }
         hi = fmax(hi, lo);
       }
-      const T tol = (gu - gl) * (T)Lim<T>::btol;
+      // stream rounds of the lean variant: eigenvalues to ~eps32 ||T|| absolute (the fp32
+      // tridiagonalisation's own backward error; FD_BISECT_LOOSE); merges (eigenvalue
+      // ranges of 1e5-1e6) and the other variants keep the tight absolute width
+      const T tol = (gu - gl) * ((PRE && FD_BISECT_LOOSE && !p.merge && sizeof(T) == 4) ? (T)6e-8f : (T)Lim<T>::btol);
       const int P = 2 * g;
       for (int it = 0; it < 96; ++it) {
         // converged: absolute width tol, or a few ulps of the endpoints (fp resolution)
