@@ -181,6 +181,7 @@ struct fd_handle {
   std::vector<int> occ, cur;
   int64_t rows_seen;
   bool dead;
+  bool ingest_copy;   // FD_INGEST_COPY set: always copy new rows into the buffers (A/B checks)
   bool legacy_trd;    // FD_LEGACY_TRD set: tridiagonalise inside eig_kernel (A/B checks)
   bool simt_gemm;     // FD_SIMT_GEMM set: FP32 SIMT Gram / reconstruct instead of tcgen05 (A/B checks)
   bool simt_gram, simt_recon;  // per-GEMM variants (FD_SIMT_GRAM, FD_SIMT_RECON: the FP32 SIMT kernels, A/B only)
@@ -425,9 +426,10 @@ fd_status fd_create(const fd_config* cfg, void* ws, size_t ws_bytes, void* cuda_
   h->prm.pretrd = 0;
   h->prm.zld = D.ldg;
   h->legacy_trd = getenv("FD_LEGACY_TRD") != nullptr;
+  h->ingest_copy = getenv("FD_INGEST_COPY") != nullptr;
   h->simt_gemm = getenv("FD_SIMT_GEMM") != nullptr;
   h->simt_gram = h->simt_gemm || getenv("FD_SIMT_GRAM") != nullptr;
-  // the tensor-core reconstruct is opt-in (accumulation bias, fd_tc.cu)
+  // FP32 SIMT reconstruct instead of the int8 tensor-core one (A/B checks)
   h->simt_recon = h->simt_gemm || getenv("FD_SIMT_RECON") != nullptr;
   h->prm.dbg = nullptr;
   if (getenv("FD_DEBUG_EIG")) {
@@ -664,7 +666,7 @@ static fd_status append_impl(fd_handle* h, const float* rows, int64_t n_rows, in
   // ReduceRank, reading C27) and always copies.
   const bool direct = !h->D.cfd && !h->simt_gram && !use_f64(h->D, L) &&
                       fdk::gram_tc_supported(L, h->prm) && (ld % 4) == 0 && h->D.d == h->D.ldb &&
-                      (reinterpret_cast<uintptr_t>(host ? stage : rows) % 16) == 0 && getenv("FD_INGEST_COPY") == nullptr;
+                      (reinterpret_cast<uintptr_t>(host ? stage : rows) % 16) == 0 && !h->ingest_copy;
   std::vector<Ingest> ing;
   std::vector<Prob> probs;
   ing.reserve(P);
