@@ -124,26 +124,33 @@ __global__ void __launch_bounds__(kBtThreads, 1) bt_kernel(const Prob* __restric
         if (tid < kNbBt) tpf = taug[i0n + tid];
       }
       if (grp == 0) {
-        // ---- W1 = V_b^T Z (thread: 4 reflectors x 4 columns, all rows) ----
-        const int cb = 4 * wg8, jb = 4 * lane;
-        float2 acc[4][2];   // column pairs on packed FFMA2, the V entries as broadcast scalars
+        // ---- W1 = V_b^T Z: warp (h, g) takes reflectors 8g..8g+7 x columns 4 lane..+3
+        // over row half h (thread tile 8 x 4: one Z float4 and two broadcast V_b float4s
+        // per 16 FFMA2, where a 4 x 4 tile over all rows spent 5 shared-memory wavefronts
+        // per 8 FFMA2 and was bound by them); half 0 -> W1, half 1 -> W2 (summed below) ----
+        const int g8 = wg8 & 3, hh = wg8 >> 2, cb = 8 * g8, jb = 4 * lane;
+        const int rm = r0 + ((N - r0) >> 1);
+        const int ra = hh ? rm : r0, rb = hh ? N : rm;
+        float2 acc[8][2];   // column pairs on packed FFMA2, the V entries as broadcast scalars
 #pragma unroll
-        for (int a = 0; a < 4; ++a) acc[a][0] = acc[a][1] = make_float2(0.f, 0.f);
-#pragma unroll 4
-        for (int r = r0; r < N; ++r) {
+        for (int a = 0; a < 8; ++a) acc[a][0] = acc[a][1] = make_float2(0.f, 0.f);
+#pragma unroll 2
+        for (int r = ra; r < rb; ++r) {
           const float4 zz = *reinterpret_cast<const float4*>(&Zs[r * kZld + jb]);
-          const float4 vv = *reinterpret_cast<const float4*>(&VbT[r * kVt + cb]);
+          const float4 v0 = *reinterpret_cast<const float4*>(&VbT[r * kVt + cb]);
+          const float4 v1 = *reinterpret_cast<const float4*>(&VbT[r * kVt + cb + 4]);
           const float2 z01 = make_float2(zz.x, zz.y), z23 = make_float2(zz.z, zz.w);
-          const float va[4] = {vv.x, vv.y, vv.z, vv.w};
+          const float va[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
-          for (int a = 0; a < 4; ++a) {
+          for (int a = 0; a < 8; ++a) {
             acc[a][0] = __ffma2_rn(make_float2(va[a], va[a]), z01, acc[a][0]);
             acc[a][1] = __ffma2_rn(make_float2(va[a], va[a]), z23, acc[a][1]);
           }
         }
+        float* Wh = hh ? W2 : W1;
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
-          *reinterpret_cast<float4*>(&W1[(cb + a) * 128 + jb]) = make_float4(acc[a][0].x, acc[a][0].y, acc[a][1].x, acc[a][1].y);
+        for (int a = 0; a < 8; ++a)
+          *reinterpret_cast<float4*>(&Wh[(cb + a) * 128 + jb]) = make_float4(acc[a][0].x, acc[a][0].y, acc[a][1].x, acc[a][1].y);
       } else {
         // ---- S = V_b^T V_b (thread: row a, columns c4..c4+3), then T = U^-1 ----
         const int t = tid - 256, a = t >> 3, c4 = 4 * (t & 7);
@@ -184,6 +191,14 @@ __global__ void __launch_bounds__(kBtThreads, 1) bt_kernel(const Prob* __restric
           }
           bar_group1();
         }
+      }
+      __syncthreads();
+      // W1 = sum of the two row-half partials (fixed order: half 0 + half 1)
+      for (int e = tid; e < kNbBt * 128 / 4; e += kBtThreads) {
+        float4 a = reinterpret_cast<float4*>(W1)[e];
+        const float4 b2 = reinterpret_cast<const float4*>(W2)[e];
+        a.x += b2.x; a.y += b2.y; a.z += b2.z; a.w += b2.w;
+        reinterpret_cast<float4*>(W1)[e] = a;
       }
       __syncthreads();
       // ---- W2 = T W1 (T upper triangular; thread: 2 reflectors x 4 columns) ----

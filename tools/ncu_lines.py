@@ -1,7 +1,9 @@
 """Summarise an ncu report's source page: top source lines by warp-stall samples."""
 import csv, subprocess, sys
 rep = sys.argv[1]; top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"], capture_output=True, text=True).stdout
+import os
+kf = os.environ.get("NCU_KERNEL")
+out = subprocess.run(["ncu", "-i", rep] + (["--kernel-name", "regex:" + kf] if kf else []) + ["--page", "source", "--csv", "--print-source", "cuda,sass"], capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 hdr = rows[2]; idx = {h: i for i, h in enumerate(hdr)}
 S = idx["Warp Stall Sampling (All Samples)"]
