@@ -13,6 +13,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "fd_internal.h"
 
@@ -36,9 +37,11 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   return x ^ (x >> 31);
 }
 
-__global__ void __launch_bounds__(512) hash_kernel(const float* __restrict__ A, int64_t n, int64_t ld, int64_t d,
+template <int BATCH>
+__global__ void __launch_bounds__(BATCH >= 64 ? 64 : 512) hash_kernel(const float* __restrict__ A, int64_t n, int64_t ld, int64_t d,
                                                    int ell, int s, uint64_t seed, int64_t row0, int64_t rows_per_range,
                                                    double* __restrict__ partials) {
+  static_assert(32 % BATCH == 0 || BATCH % 32 == 0, "hash batches (32 rows) and load batches nest");
   extern __shared__ double hacc[];   // [ell][64]: block j's bucket h at row j * lb + h
   const int lb = ell / s;
   const int c = threadIdx.x % kHashCols, j = threadIdx.x / kHashCols;
@@ -50,50 +53,58 @@ __global__ void __launch_bounds__(512) hash_kernel(const float* __restrict__ A, 
   const bool cv = col < d;
   double* my = hacc + (size_t)j * lb * kHashCols + c;
   const int lane = threadIdx.x & 31;
-  // rows of this range through a running pointer (32-bit steps); 16-row batches with
-  // the next batch loaded while this one accumulates
+  // rows of this range through a running pointer (32-bit steps); BATCH-row load batches
+  // with the next batch loaded while this one accumulates
   const float* pa = A + r0 * ld + (cv ? col : 0);
-  float cur[16], nxt[16];
+  float cur[BATCH], nxt[BATCH];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) cur[q] = (q < nrows && cv) ? __ldg(pa + (int64_t)q * ld) : 0.f;
-  int code = 0;
-  for (int k = 0; k < nrows; k += 16) {
+  for (int q = 0; q < BATCH; ++q) cur[q] = (q < nrows && cv) ? __ldg(pa + (int64_t)q * ld) : 0.f;
+  constexpr int NC = BATCH >= 32 ? BATCH / 32 : 1;   // hash groups of 32 rows per load batch
+  int code[NC];
+#pragma unroll
+  for (int t = 0; t < NC; ++t) code[t] = 0;
+  for (int k = 0; k < nrows; k += BATCH) {
     if ((k & 31) == 0) {
-      // lane l hashes row k + l for this warp's block j (the hash depends on the row and
-      // block only); the buckets / signs are broadcast by shuffles below
-      code = 0;
-      if (k + lane < nrows) {
-        const uint64_t i = (uint64_t)(row0 + r0 + k + lane);
-        const uint64_t x = mix64(seed ^ (i * (uint64_t)s + (uint64_t)j) * 0xD1B54A32D192ED03ull);
-        const uint32_t h = (uint32_t)(((uint64_t)(uint32_t)(x >> 32) * (uint64_t)lb) >> 32);   // multiply-shift range
-        code = (int)(h << 1) | (int)(x & 1ull);
+      // lane l hashes row kh + l for this warp's block j (the hash depends on the row and
+      // block only, so a row's bucket is warp-uniform); broadcast by shuffles below
+#pragma unroll
+      for (int t = 0; t < NC; ++t) {
+        const int kh = k + 32 * t;
+        code[t] = 0;
+        if (kh + lane < nrows) {
+          const uint64_t i = (uint64_t)(row0 + r0 + kh + lane);
+          const uint64_t x = mix64(seed ^ (i * (uint64_t)s + (uint64_t)j) * 0xD1B54A32D192ED03ull);
+          const uint32_t h = (uint32_t)(((uint64_t)(uint32_t)(x >> 32) * (uint64_t)lb) >> 32);   // multiply-shift range
+          code[t] = (int)(h << 1) | (int)(x & 1ull);
+        }
       }
     }
-    pa += 16 * ld;
-    if (k + 32 <= nrows && cv) {            // full next batch: no per-row predicates
+    pa += BATCH * ld;
+    if (k + 2 * BATCH <= nrows && cv) {      // full next batch: no per-row predicates
       const float* p = pa;
 #pragma unroll
-      for (int q = 0; q < 16; ++q) { nxt[q] = __ldg(p); p += ld; }
+      for (int q = 0; q < BATCH; ++q) { nxt[q] = __ldg(p); p += ld; }
     } else {
 #pragma unroll
-      for (int q = 0; q < 16; ++q) nxt[q] = (k + 16 + q < nrows && cv) ? __ldg(pa + (int64_t)q * ld) : 0.f;
+      for (int q = 0; q < BATCH; ++q) nxt[q] = (k + BATCH + q < nrows && cv) ? __ldg(pa + (int64_t)q * ld) : 0.f;
     }
     const int base = k & 31;
-    if (k + 16 <= nrows) {
+    const int nb = min(BATCH, nrows - k);
+    if (nb == BATCH) {
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const int cd = __shfl_sync(0xffffffffu, code, base + q);
+      for (int q = 0; q < BATCH; ++q) {
+        const int cd = __shfl_sync(0xffffffffu, code[q / 32], (base + q) & 31);
         my[(cd >> 1) * kHashCols] += (cd & 1) ? -(double)cur[q] : (double)cur[q];
       }
     } else {
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const int cd = __shfl_sync(0xffffffffu, code, base + q);
-        if (k + q < nrows) my[(cd >> 1) * kHashCols] += (cd & 1) ? -(double)cur[q] : (double)cur[q];
+      for (int q = 0; q < BATCH; ++q) {
+        const int cd = __shfl_sync(0xffffffffu, code[q / 32], (base + q) & 31);
+        if (q < nb) my[(cd >> 1) * kHashCols] += (cd & 1) ? -(double)cur[q] : (double)cur[q];
       }
     }
 #pragma unroll
-    for (int q = 0; q < 16; ++q) cur[q] = nxt[q];
+    for (int q = 0; q < BATCH; ++q) cur[q] = nxt[q];
   }
   __syncthreads();
   for (int e = threadIdx.x; e < ell * kHashCols; e += blockDim.x) {
@@ -131,13 +142,21 @@ cudaError_t launch_hash(const float* A, int64_t n, int64_t ld, int64_t d, int el
   const int R = hash_ranges(d);
   const int64_t rpr = (n + R - 1) / R;
   const int smem = ell * kHashCols * (int)sizeof(double);
-  static AttrOnce once;
+  // load batch: 64 rows for s = 1 (64 threads per CTA, 2 warps: more loads in flight per
+  // thread; c4 Hashing 24.6 / 17.6 / 15.1 ms at 16 / 32 / 64 rows), 16 rows otherwise (at
+  // 32, s = 4 needs 128 registers and 2 instead of 3 CTAs fit per SM: c4 OSNAP 35.6 -> 39.0
+  // ms).  FD_HASH_BATCH=16|32|64 overrides (A/B only).
+  static const int env_batch = [] { const char* e = getenv("FD_HASH_BATCH"); return e ? atoi(e) : 0; }();
+  int batch = (env_batch == 16 || env_batch == 32 || env_batch == 64) ? env_batch : (s <= 1 ? 64 : 16);
+  if (batch == 64 && s > 1) batch = 32;   // the 64-row kernel is built for 64-thread CTAs
+  auto kern = (batch == 64) ? hash_kernel<64> : (batch == 32) ? hash_kernel<32> : hash_kernel<16>;
+  static AttrOnce once[3];
   if (smem > 48 * 1024) {
-    if (cudaError_t e = once.ensure(hash_kernel, smem); e != cudaSuccess) return e;
+    if (cudaError_t e = once[batch / 32].ensure(kern, smem); e != cudaSuccess) return e;
   }
   if (n > 0) {
-    hash_kernel<<<dim3((unsigned)nslices, (unsigned)R), kHashCols * s, smem, st>>>(A, n, ld, d, ell, s, seed, row0,
-                                                                                  rpr, partials);
+    kern<<<dim3((unsigned)nslices, (unsigned)R), kHashCols * s, smem, st>>>(A, n, ld, d, ell, s, seed, row0,
+                                                                          rpr, partials);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int64_t ne = (int64_t)ell * d;
