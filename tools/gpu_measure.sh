@@ -5,7 +5,7 @@
 cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 mkdir -p gpurun_out
 python build.py > gpurun_out/build.log 2>&1
-for spec in "c4" "c4 --variant fast_alpha_fd" "c1" "c2" "c2 --shards 8" "c3" "c3 --ell 50" "c3 --ell 200" "c5"; do
+for spec in "c4" "c4 --variant fast_alpha_fd" "c4 --variant hashing" "c4 --variant osnap" "c1" "c2" "c2 --shards 8" "c3" "c3 --ell 50" "c3 --ell 200" "c5"; do
   name=$(echo $spec | tr ' ' '_' | tr -d '-')
   timeout 900 python bench.py --workload $spec --steps 5 --warmup 3 > gpurun_out/bench_$name.json 2> gpurun_out/bench_$name.err
 done
