@@ -90,3 +90,13 @@ def dist_cov_err(A_local, B, group=None, proj_k=0):
     if proj_k > 0:
         out["proj_err"] = proj_err_from_gram(AtA, B, frob, k=proj_k)["err"]
     return out
+
+
+def reduce_hash(B, group=None):
+    """Merge of the Hashing / OSNAP sketches: the sketch is
+    linear in the rows, B = S A = sum over ranks of S[:, rows_r] A[rows_r], so with every
+    rank hashing its rows by their GLOBAL index (fd_hash_sketch's row0 = the rank's first
+    row) the merge is one all_reduce(SUM) of the ell x d fp64 accumulators, in place."""
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(B, group=group)
+    return B

@@ -16,7 +16,7 @@ import torch.multiprocessing as mp
 
 import fdgen
 import oracle
-from paper_1501_06561_b200.dist import gather_and_merge, local_range, reduce_gram
+from paper_1501_06561_b200.dist import gather_and_merge, local_range, reduce_gram, reduce_hash
 
 WORLD = 2
 
@@ -114,3 +114,38 @@ def test_two_rank_gloo_matches_single_process(tmp_path, variant, P_total):
         assert abs(s[5] - frob) <= 1e-12 * frob
     # both ranks hold the identical sketch (deterministic local merge, no broadcast)
     assert np.array_equal(np.load(tmp_path / "B0.npy"), np.load(tmp_path / "B1.npy"))
+
+
+def _hash_worker(rank, port, ell, s_blocks, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        A = fdgen.host_rows(fdgen.config("c1"))
+        r0, r1 = local_range(A.shape[0] - 3, rank, WORLD)   # ragged split
+        # the oracle stands in for fd_hash_sketch(row0 = r0) on the GPU
+        Bp = oracle.hash_sketch(A[r0:r1], ell, s=s_blocks, seed=7, row0=r0)
+        B = reduce_hash(torch.from_numpy(Bp))
+        np.save(os.path.join(out_dir, f"H{rank}.npy"), B.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("s_blocks", [1, 4])
+def test_two_rank_gloo_hash_merge_is_a_sum(tmp_path, s_blocks):
+    """Hashing / OSNAP across ranks: ranks hash their rows by
+    global row index and all_reduce the fp64 accumulators; the result is the single-process
+    sketch of the same rows (sums reordered by rank only)."""
+    ell = 16
+    mp.start_processes(_hash_worker, args=(_port(), ell, s_blocks, str(tmp_path)), nprocs=WORLD,
+                       start_method="spawn", join=True)
+    A = fdgen.host_rows(fdgen.config("c1"))
+    n = A.shape[0] - 3
+    ref = oracle.hash_sketch(A[:n], ell, s=s_blocks, seed=7)
+    scale = np.abs(ref).max()
+    H0, H1 = np.load(tmp_path / "H0.npy"), np.load(tmp_path / "H1.npy")
+    assert np.abs(H0 - ref).max() <= 1e-13 * scale
+    assert np.array_equal(H0, H1)
+    # a rank that ignored its row offset would hash different buckets
+    wrong = oracle.hash_sketch(A[n // 2:n], ell, s=s_blocks, seed=7, row0=0)
+    right = oracle.hash_sketch(A[n // 2:n], ell, s=s_blocks, seed=7, row0=n // 2)
+    assert np.abs(wrong - right).max() > 1e-3 * scale
