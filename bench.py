@@ -641,6 +641,14 @@ def run_hash(args):
             "algorithmic_bytes": "n d 4 (read A) + 2 x partials (write + read, fp64) + B read/write",
             "traffic": None, "peak_source": f"hbm_gbs {pk['source']}", "ms_per_launch": kms}
     roof["frac"] = roof["achieved"] / roof["peak"]
+    # measured DRAM traffic of one launch (ncu --set full capture, c4 only, one GPU)
+    traffic_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if wl == "c4" and world == 1 and os.path.exists(traffic_file):
+        with open(traffic_file) as f:
+            tr = json.load(f).get(f"hash_kernel_s{s}")
+        if tr:
+            roof["traffic"] = tr["bytes_per_launch_captured"]
+            roof["traffic_source"] = tr["source"]
     # error of the hash sketch (GPU evaluator, outside the timed region)
     from paper_1501_06561_b200.dist import dist_cov_err
     Bf = B.to(torch.float32)

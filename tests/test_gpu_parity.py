@@ -628,20 +628,34 @@ def test_hash_multi_call_and_padded_rows():
         m.hash_sketch(Ad, 30, s=4)          # s must divide ell
 
 
-def test_hash_fullsize_c4_sampled_columns():
-    """c4 at full size (n = 8 388 608, d = 1024), OSNAP s = 4, ell = 128, the bench's
-    launch: the oracle recomputes 16 sampled columns (the hash depends on the row index
-    only) from the same device-generated rows."""
+@pytest.mark.parametrize("n,d,ell,s", [(8111, 1000, 32, 1), (27 * 256, 1024, 128, 1), (27 * 255 + 5, 1024, 16, 1),
+                                       (40000, 500, 128, 1)])
+def test_hash_parity_long_ranges(n, d, ell, s):
+    """Row ranges of >= 256 rows per CTA (d ~ 1000: 27 ranges), so the 64-row kernel's
+    steady-state loop (register ring, four full batches ahead) runs, ends at different
+    remainders (45 / 0 / ragged rows in the general loop) and meets ragged columns."""
+    rng = np.random.default_rng(n + d)
+    A = (rng.standard_normal((n, d)) * rng.uniform(0.1, 3.0, size=(1, d))).astype(np.float32)
+    Bg = fd().hash_sketch(torch.from_numpy(A).cuda(), ell, s=s, seed=3).cpu().numpy()
+    Bo = oracle.hash_sketch(A, ell, s=s, seed=3)
+    assert np.abs(Bg - Bo).max() <= _hash_tol(A)
+
+
+@pytest.mark.parametrize("s", [4, 1])
+def test_hash_fullsize_c4_sampled_columns(s):
+    """c4 at full size (n = 8 388 608, d = 1024), OSNAP s = 4 and Hashing s = 1, ell = 128,
+    the bench's launches: the oracle recomputes 16 sampled columns (the hash depends on the
+    row index only) from the same device-generated rows."""
     m = fd()
     w = fdgen.config("c4")
     gen = fdgen.DeviceGenerator(w)
     A = torch.empty((w.n, w.d), dtype=torch.float32, device="cuda")
     gen.fill(A)
-    B = m.hash_sketch(A, 128, s=4, seed=0).cpu().numpy()
+    B = m.hash_sketch(A, 128, s=s, seed=0).cpu().numpy()
     cols = np.random.default_rng(0).choice(w.d, 16, replace=False)
     As = A[:, torch.from_numpy(cols).cuda()].contiguous().cpu().numpy()
     del A
-    Bo = oracle.hash_sketch(As, 128, s=4, seed=0)
+    Bo = oracle.hash_sketch(As, 128, s=s, seed=0)
     assert np.abs(B[:, cols] - Bo).max() <= _hash_tol(As)
 
 
