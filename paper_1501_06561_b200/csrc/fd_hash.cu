@@ -38,7 +38,7 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
 }
 
 template <int BATCH>
-__global__ void __launch_bounds__(BATCH >= 64 ? 64 : 512) hash_kernel(const float* __restrict__ A, int64_t n, int64_t ld, int64_t d,
+__global__ void __launch_bounds__(BATCH >= 64 ? kHashCols : 512) hash_kernel(const float* __restrict__ A, int64_t n, int64_t ld, int64_t d,
                                                    int ell, int s, uint64_t seed, int64_t row0, int64_t rows_per_range,
                                                    double* __restrict__ partials) {
   static_assert(32 % BATCH == 0 || BATCH % 32 == 0, "hash batches (32 rows) and load batches nest");
